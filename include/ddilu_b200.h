@@ -1,0 +1,154 @@
+/*
+ * ddilu_b200.h -- C ABI of libddilu_b200.so (hand-written sm_100a CUDA).
+ *
+ * The reference (`ddilu`, pure Python + numba) has no FFI layer; its boundary is
+ * the public Python API (pkg/src/ddilu/__init__.py:11-59).  Each entry below
+ * replaces one numba kernel (or a numpy expression around it) of that package;
+ * the file:line it replaces is cited per function.  paper_2303_08881_b200/_lib.py
+ * binds these symbols with ctypes (INTEGRATION.md shows the same stub a
+ * maintainer of the reference would add).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless the name ends in _h,
+ *   - indices are int32 on the device (nnz < 2^31 is checked by the host side),
+ *     values are fp64; CSR rows have strictly increasing columns,
+ *   - `stream` is a cudaStream_t passed as void*; nothing synchronises the device,
+ *   - the return value is 0 on success, -1000 for a bad argument, or
+ *     -(cudaError_t) for a launch failure.
+ */
+#ifndef DDILU_B200_H
+#define DDILU_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- tuning knobs (no reference equivalent): "trsv_blocks_per_sm", "trsv_sleep_ns" */
+int ddilu_set_tuning(const char *key, int value);
+
+/* ---- primitives used by the count -> scan -> fill setup passes (the reference
+ * uses np.cumsum: e.g. sparse.py:449, factor.py:254-257) */
+long long ddilu_scan_tmp_elems(long long n);
+/* out[0..n] = exclusive prefix sums of in[0..n-1], out[n] = total; in == out allowed */
+int ddilu_exclusive_scan_i32(const int *in, int *out, long long n, int *tmp, void *stream);
+long long ddilu_sort_tmp_elems(long long n);
+/* stable LSD radix sort of (key, value) pairs on the low `bits` bits of the key */
+int ddilu_sort_pairs_i32(int *keys, int *vals, int *keys_alt, int *vals_alt, long long n, int bits, int *tmp,
+                         void *stream);
+
+/* ---- sparse.py:219-225 `_spmv` (+ the `b - A x` residual expressions of
+ * krylov.py:106,168 and precond.py:258,264,354,379).  Rows [row_begin,row_end).
+ * mode 0: y = A x; 1: y = b - A x; 2: y = b + A x.  y/b are indexed by row. */
+int ddilu_spmv_csr_f64(int row_begin, int row_end, const int *row_ptr, const int *col_idx, const double *values,
+                       const double *x, const double *b, double *y, int mode, void *stream);
+
+/* ---- level schedules (absent from the reference: SPEC.md:112; definition in
+ * lev[i] = 1 + max lev[j] over the dependencies of row i) */
+int ddilu_levels(int n, const int *row_ptr, const int *col_idx, int upper, int *lev, int *max_lev, void *stream);
+/* rows sorted by (level, index) [index descending for upper] into `rows`;
+ * level_ptr[n_levels+1]; slot_ptr[n_levels+1] = level starts padded to 32;
+ * order[n + 32*n_levels] = padded schedule (-1 = empty slot). */
+int ddilu_schedule_build(int n, const int *lev, int n_levels, int upper, int *keys, int *rows, int *keys_alt,
+                         int *rows_alt, int *sort_tmp, int *level_ptr, int *slot_ptr, int *order, void *stream);
+
+/* ---- sparse.py:228-249 `_lower_solve` / :252-272 `_upper_solve`.
+ * *err must hold INT_MAX on entry; on a zero/missing diagonal it receives the
+ * smallest failing row (the reference raises ZeroDivisionError for that row). */
+int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
+                 const double *b, double *x, int upper, int unit_diag, int *err, void *stream);
+
+/* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
+int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,
+                      double *rownorm, void *stream);
+/* ---- factor.py:219-246 `_split_fill` */
+int ddilu_split_fill(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, const int *p_rp,
+                     int *p_ci, double *p_v, const int *k_rp, int *k_ci, double *k_v, void *stream);
+/* ---- factor.py:397-432 `_factor_split`: ILU(0) / MILU(0) / partial ILU(0) on the
+ * split pattern, rows visited in the level order `order` of the pivot pattern. */
+int ddilu_ilu0_numeric(int n, int n_slots, const int *order, const int *p_rp, const int *p_ci, double *p_v,
+                       const int *k_rp, const int *k_ci, double *k_v, int n_elim, int milu, const double *target,
+                       const double *wvec, double delta, const double *rownorm, int *done, void *stream);
+/* ---- factor.py:482-656 `_ilut_factor` + :465-479 `_select_largest`.  Rows are
+ * written to fixed-capacity slabs: caps_h = {lcap, ucap, scap} from ddilu_ilut_caps;
+ * L row i at i*lcap; U row i at i*ucap (i < n_elim, diagonal first) or
+ * n_elim*ucap + (i-n_elim)*scap (Schur rows).  *status != 0: row_cap too small. */
+long long ddilu_ilut_smem_bytes(int row_cap);
+int ddilu_ilut_caps(int maxfill, int row_cap, int *caps_h);
+int ddilu_ilut_factor(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, double tau, int maxfill,
+                      double tau_s, double delta, int row_cap, int *l_cnt, int *l_ci, double *l_v, int *u_cnt,
+                      int *u_ci, double *u_v, int *done, int *status, void *stream);
+/* slab rows (cap_a for rows < n_split, cap_b after) -> CSR with the given row_ptr */
+int ddilu_compact_rows(int n, int n_split, int cap_a, int cap_b, const int *cnt, const int *ci, const double *v,
+                       const int *out_rp, int *out_ci, double *out_v, void *stream);
+
+/* ---- factor.py:756-803 `_col_split_*` / sparse.py:456-471 `extract_block` on
+ * contiguous index ranges: rows [r0,r1) x cols [c0,c1), columns shifted by -c0 */
+int ddilu_csr_block_count(const int *rp, const int *ci, int r0, int r1, int c0, int c1, int *counts, void *stream);
+int ddilu_csr_block_fill(const int *rp, const int *ci, const double *v, int r0, int r1, int c0, int c1,
+                         const int *out_rp, int *out_ci, double *out_v, void *stream);
+
+/* ---- Krylov vector kernels: sparse.py:275-280 `_vdot`, :526-528 `vnorm2`,
+ * krylov.py:74-77 `_axpy`, and the numpy expressions of krylov.py:122,156,160-167 */
+long long ddilu_reduce_ws_bytes(void);
+int ddilu_dot(long long n, const double *x, const double *y, double *out, void *ws, void *stream);
+/* w += (alpha_dev ? alpha_host * *alpha_dev : alpha_host) * v; if u: *out = dot(u, w) */
+int ddilu_axpy_dot(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
+                   const double *u, double *out, void *ws, void *stream);
+/* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
+int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
+                double *y, void *stream);
+/* x (+)= sum_i coef[i] * basis[i*ld + :] in increasing i */
+int ddilu_multi_axpy(long long n, int k, const double *basis, long long ld, const double *coef, double *x,
+                     int overwrite, void *stream);
+/* z = a + b (0), a - b (1), -a (2) */
+int ddilu_ewise(long long n, const double *a, const double *b, int op, double *z, void *stream);
+/* dst[i] = src[idx[i]] / dst[idx[i]] = src[i]  (precond.py:190, 369, 384 fancy indexing) */
+int ddilu_gather(long long n, const int *idx, const double *src, double *dst, void *stream);
+int ddilu_scatter(long long n, const int *idx, const double *src, double *dst, void *stream);
+
+/* ---- ordering.py:88-94 `_mark_exterior` on the symmetrised pattern (:32-81) */
+int ddilu_mark_exterior(int n, const int *rp, const int *ci, const int *owner, int *exterior, void *stream);
+/* keys = exterior * p + owner, vals = iota: sorting them gives DomainLayout.global_perm (ordering.py:273-293) */
+int ddilu_layout_keys(int n, const int *owner, const int *exterior, int p, int *keys, int *vals, void *stream);
+int ddilu_lower_bounds(const int *sorted, int n, int nkeys, int *out, void *stream);
+/* ordering.py:171-187: structured box partition */
+int ddilu_box_owner(int n, int nd, const int *dims_h, const int *factors_h, int *owner, void *stream);
+
+/* ---- sparse.py:303-330 `_gather_rows_count/_fill` (take_submatrix / extract_block),
+ * precond.py:154-170 `_keep_cross_block` folded in as a filter:
+ * filter & 3: 0 all, 1 same-domain entries only, 2 cross-domain only; filter & 4: drop diagonal */
+int ddilu_build_map(int n_nodes, const int *nodes, int offset, int *map, void *stream);
+int ddilu_gather_rows_count(int n_sel, const int *rows, const int *rp, const int *ci, const int *colmap,
+                            const int *dom, int filter, int *counts, void *stream);
+int ddilu_gather_rows_fill(int n_sel, const int *rows, const int *rp, const int *ci, const double *v,
+                           const int *colmap, const int *dom, int filter, const int *out_rp, int *out_ci,
+                           double *out_v, int resort, void *stream);
+
+/* ---- halo planning for the one-subdomain-block-per-GPU mapping (no reference
+ * equivalent: the reference loops over domains in one process, precond.py:189-190).
+ * flags[j] = 1 for every column of the selected rows with colmap[j] < 0;
+ * flags[rank * n_ext + extmap[j]] = 1 when a row of another rank touches my exterior j. */
+int ddilu_mark_foreign_cols(int n_sel, const int *rows, const int *rp, const int *ci, const int *colmap, int *flags,
+                            void *stream);
+int ddilu_mark_sends(int n, const int *rp, const int *ci, const int *owner, int doms_per_rank, int my_rank,
+                     const int *extmap, int n_ext, int *flags, void *stream);
+
+/* ---- ordering.py:32-81 `_sym_adjacency` (neighbour sets; order inside a row is unspecified) */
+int ddilu_sym_adj_count(int n, const int *rp, const int *ci, int *counts, void *stream);
+int ddilu_sym_adj_fill(int n, const int *rp, const int *ci, const int *out_rp, int *cursor, int *out_ci, void *stream);
+int ddilu_row_lengths(int n, const int *rp, int *out, void *stream);
+
+/* ---- ordering.py:304-397 `_bfs_ecc` + `_rcm_order`: Cuthill-McKee order (not reversed) */
+long long ddilu_cm_work_elems(int n);
+int ddilu_cm_order(int n, const int *adj_rp, const int *adj_ci, int *order, int *work, void *stream);
+/* ordering.py:416 reversal, per domain segment */
+int ddilu_reverse_segments(int n, const int *cm, int n_seg, const int *seg_ptr, int *out, void *stream);
+
+/* ---- int64 <-> int32 index conversion at the API boundary (sparse.py:95-96 uses int64) */
+int ddilu_narrow_i64(long long n, const long long *in, int *out, void *stream);
+int ddilu_widen_i32(long long n, const int *in, long long *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDILU_B200_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of libddilu_b200.so (the C ABI declared in include/ddilu_b200.h).
+
+There is no CPU fallback: if the library is missing the import of any compute
+entry point raises, and every call checks the library's status code.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libddilu_b200.so")
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_longlong
+_D = ctypes.c_double
+_S = ctypes.c_char_p
+
+# name -> (restype, argtypes); must stay in sync with include/ddilu_b200.h
+SIGNATURES = {
+    "ddilu_set_tuning": (_I, [_S, _I]),
+    "ddilu_scan_tmp_elems": (_L, [_L]),
+    "ddilu_exclusive_scan_i32": (_I, [_P, _P, _L, _P, _P]),
+    "ddilu_sort_tmp_elems": (_L, [_L]),
+    "ddilu_sort_pairs_i32": (_I, [_P, _P, _P, _P, _L, _I, _P, _P]),
+    "ddilu_spmv_csr_f64": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P]),
+    "ddilu_levels": (_I, [_I, _P, _P, _I, _P, _P, _P]),
+    "ddilu_schedule_build": (_I, [_I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),
+    "ddilu_ilut_smem_bytes": (_L, [_I]),
+    "ddilu_ilut_caps": (_I, [_I, _I, _P]),
+    "ddilu_ilut_factor": (_I, [_I, _P, _P, _P, _I, _D, _I, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_compact_rows": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_csr_block_count": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "ddilu_csr_block_fill": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "ddilu_reduce_ws_bytes": (_L, []),
+    "ddilu_dot": (_I, [_L, _P, _P, _P, _P, _P]),
+    "ddilu_axpy_dot": (_I, [_L, _P, _D, _P, _P, _P, _P, _P, _P]),
+    "ddilu_scale": (_I, [_L, _P, _P, _D, _I, _I, _P, _P]),
+    "ddilu_multi_axpy": (_I, [_L, _I, _P, _L, _P, _P, _I, _P]),
+    "ddilu_ewise": (_I, [_L, _P, _P, _I, _P, _P]),
+    "ddilu_gather": (_I, [_L, _P, _P, _P, _P]),
+    "ddilu_scatter": (_I, [_L, _P, _P, _P, _P]),
+    "ddilu_mark_exterior": (_I, [_I, _P, _P, _P, _P, _P]),
+    "ddilu_layout_keys": (_I, [_I, _P, _P, _I, _P, _P, _P]),
+    "ddilu_lower_bounds": (_I, [_P, _I, _I, _P, _P]),
+    "ddilu_box_owner": (_I, [_I, _I, _P, _P, _P, _P]),
+    "ddilu_build_map": (_I, [_I, _P, _I, _P, _P]),
+    "ddilu_gather_rows_count": (_I, [_I, _P, _P, _P, _P, _P, _I, _P, _P]),
+    "ddilu_gather_rows_fill": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P]),
+    "ddilu_mark_foreign_cols": (_I, [_I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_mark_sends": (_I, [_I, _P, _P, _P, _I, _I, _P, _I, _P, _P]),
+    "ddilu_sym_adj_count": (_I, [_I, _P, _P, _P, _P]),
+    "ddilu_sym_adj_fill": (_I, [_I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_row_lengths": (_I, [_I, _P, _P, _P]),
+    "ddilu_cm_work_elems": (_L, [_I]),
+    "ddilu_cm_order": (_I, [_I, _P, _P, _P, _P, _P]),
+    "ddilu_reverse_segments": (_I, [_I, _P, _I, _P, _P, _P]),
+    "ddilu_narrow_i64": (_I, [_L, _P, _P, _P]),
+    "ddilu_widen_i32": (_I, [_L, _P, _P, _P]),
+}
+
+_lib = None
+launches = 0  # kernels-launching C-ABI calls made so far (bench.py reports the delta)
+
+
+class DdiluError(RuntimeError):
+    pass
+
+
+def load() -> ctypes.CDLL:
+    """Load the shared library (no device needed); raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DdiluError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2303_08881_b200.build` "
+                "(there is no CPU fallback for the DD-ILU path)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise DdiluError("the DD-ILU path runs on a CUDA device only (sm_100a); no CPU fallback exists")
+
+
+def _arg(a):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.data_ptr()
+    return a
+
+
+def stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def call(name: str, *args):
+    """Call a status-returning entry point with torch tensors / scalars; the
+    current torch stream is appended as the last argument."""
+    global launches
+    fn = getattr(load(), name)
+    rc = fn(*[_arg(a) for a in args], stream_ptr())
+    launches += 1
+    if rc != 0:
+        raise DdiluError(f"{name} failed with status {rc}")
+
+
+def query(name: str, *args):
+    """Call a size-query entry point (no stream, returns a number)."""
+    return getattr(load(), name)(*args)

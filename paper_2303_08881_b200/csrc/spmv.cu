@@ -1,0 +1,73 @@
+// CSR SpMV, fp64 values / int32 indices (replaces sparse.py:219-225 `_spmv`).
+//
+// "CSR-stream": a CTA owns ROWS consecutive rows; their entries are one
+// contiguous slice of (col_idx, values), read with fully coalesced loads, the
+// products val*x[col] are staged in shared memory, then one thread per row adds
+// its products strictly left to right.  Each product is rounded before it is
+// added (-fmad=false), so the result is bit-identical to the serial reference.
+// x may carry a halo tail (columns >= n_local hold interface values received
+// from other ranks); interior rows never touch it, so the caller launches the
+// interior row range while the halo is still in flight.
+//
+// Algorithmic bytes: 12*nnz + 4*(rows+1) + 8*cols_touched + 8*rows (+8*rows for b).
+#include "common.cuh"
+#include "ddilu_b200.h"
+
+namespace ddilu {
+
+constexpr int SPMV_ROWS = 256;       // rows (= threads) per CTA
+constexpr int SPMV_STAGE = 4096;     // products staged per CTA (32 KB)
+
+// mode 0: y = A x      mode 1: y = b - A x      mode 2: y = b + A x
+template <int MODE>
+__global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const int *__restrict__ rp,
+                                                         const int *__restrict__ ci, const double *__restrict__ val,
+                                                         const double *__restrict__ x, const double *__restrict__ b,
+                                                         double *__restrict__ y) {
+    __shared__ double prod[SPMV_STAGE];
+    __shared__ int srp[SPMV_ROWS + 1];
+    const int row0 = r0 + blockIdx.x * SPMV_ROWS;
+    const int nrows = min(SPMV_ROWS, r1 - row0);
+    if (threadIdx.x <= nrows) srp[threadIdx.x] = rp[row0 + threadIdx.x];
+    __syncthreads();
+    const int e0 = srp[0], e1 = srp[nrows];
+    const int row = row0 + threadIdx.x;
+    if (e1 - e0 <= SPMV_STAGE) {
+        for (int e = e0 + threadIdx.x; e < e1; e += SPMV_ROWS) prod[e - e0] = val[e] * x[ci[e]];
+        __syncthreads();
+        if (threadIdx.x < nrows) {
+            double s = 0.0;
+            for (int k = srp[threadIdx.x] - e0, ke = srp[threadIdx.x + 1] - e0; k < ke; ++k) s += prod[k];
+            if (MODE == 1) s = b[row] - s;
+            if (MODE == 2) s = b[row] + s;
+            y[row] = s;
+        }
+    } else if (threadIdx.x < nrows) {  // long rows: plain row loop, same summation order
+        double s = 0.0;
+        for (int k = srp[threadIdx.x], ke = srp[threadIdx.x + 1]; k < ke; ++k) s += val[k] * x[ci[k]];
+        if (MODE == 1) s = b[row] - s;
+        if (MODE == 2) s = b[row] + s;
+        y[row] = s;
+    }
+}
+
+}  // namespace ddilu
+
+using namespace ddilu;
+
+extern "C" int ddilu_spmv_csr_f64(int row_begin, int row_end, const int *row_ptr, const int *col_idx,
+                                  const double *values, const double *x, const double *b, double *y, int mode,
+                                  void *stream) {
+    if (row_end <= row_begin) return DDILU_OK;
+    if ((mode != 0 && !b) || mode < 0 || mode > 2) return DDILU_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    int grid = div_up(row_end - row_begin, SPMV_ROWS);
+    if (mode == 0)
+        spmv_stream<0><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
+    else if (mode == 1)
+        spmv_stream<1><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
+    else
+        spmv_stream<2><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}

@@ -1,0 +1,302 @@
+"""Device-side building blocks: CSR matrices in HBM and thin wrappers that
+launch the library's kernels on them.  torch is used for allocation, streams
+and host<->device copies only.
+
+HBM layout: row_ptr int32[n+1], col_idx int32[nnz] (strictly increasing per
+row), values float64[nnz]; vectors float64.  int32 halves the index traffic of
+the reference's int64 arrays (sparse.py:95-96); nnz < 2^31 is enforced here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, query
+
+I32 = torch.int32
+F64 = torch.float64
+INT_MAX = 2**31 - 1
+
+
+def dev():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def empty_i32(n):
+    return torch.empty(int(n), dtype=I32, device=dev())
+
+
+def zeros_i32(n):
+    return torch.zeros(int(n), dtype=I32, device=dev())
+
+
+def empty_f64(n):
+    return torch.empty(int(n), dtype=F64, device=dev())
+
+
+def zeros_f64(n):
+    return torch.zeros(int(n), dtype=F64, device=dev())
+
+
+def to_device_i32(a) -> torch.Tensor:
+    """Host int array (any int dtype) -> device int32 (values must fit)."""
+    a = np.ascontiguousarray(a)
+    if a.size and (int(a.max()) > INT_MAX or int(a.min()) < -INT_MAX - 1):
+        raise ValueError("index does not fit the device int32 layout")
+    if a.dtype == np.int64 and a.size > (1 << 16):
+        # narrow on the device: one pinned int64 copy, no host pass
+        wide = torch.from_numpy(a).to(dev(), non_blocking=False)
+        out = empty_i32(a.size)
+        call("ddilu_narrow_i64", a.size, wide, out)
+        return out
+    return torch.from_numpy(a.astype(np.int32, copy=False)).to(dev())
+
+
+def to_device_f64(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev())
+
+
+def to_host_i64(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().astype(np.int64)
+
+
+def exclusive_scan_(buf: torch.Tensor, n: int) -> torch.Tensor:
+    """In-place exclusive scan of buf[0:n]; buf has n+1 entries, buf[n] = total."""
+    tmp = empty_i32(query("ddilu_scan_tmp_elems", n))
+    call("ddilu_exclusive_scan_i32", buf, buf, n, tmp)
+    return buf
+
+
+def sort_pairs_(keys: torch.Tensor, vals: torch.Tensor, bits: int):
+    n = keys.numel()
+    if n <= 1:
+        return
+    ka, va = torch.empty_like(keys), torch.empty_like(vals)
+    tmp = empty_i32(query("ddilu_sort_tmp_elems", n))
+    call("ddilu_sort_pairs_i32", keys, vals, ka, va, n, int(bits), tmp)
+
+
+@dataclass
+class DeviceCsr:
+    n_rows: int
+    n_cols: int
+    rp: torch.Tensor
+    ci: torch.Tensor
+    val: torch.Tensor | None
+    _nnz: int = -1
+
+    @property
+    def nnz(self) -> int:
+        if self._nnz < 0:
+            self._nnz = int(self.rp[-1].item()) if self.n_rows else 0
+        return self._nnz
+
+    @staticmethod
+    def from_host(n_rows, n_cols, row_ptr, col_idx, values) -> "DeviceCsr":
+        nnz = int(row_ptr[-1]) if len(row_ptr) else 0
+        if nnz > INT_MAX or max(n_rows, n_cols) > INT_MAX:
+            raise ValueError("matrix too large for the int32 device layout")
+        return DeviceCsr(int(n_rows), int(n_cols), to_device_i32(row_ptr), to_device_i32(col_idx),
+                         to_device_f64(values), nnz)
+
+    def to_host(self):
+        vals = self.val.cpu().numpy() if self.val is not None else np.zeros(self.nnz)
+        return to_host_i64(self.rp), to_host_i64(self.ci), vals
+
+
+# ---------------------------------------------------------------------------
+# kernels
+
+
+def spmv(a: DeviceCsr, x: torch.Tensor, out: torch.Tensor, b: torch.Tensor | None = None, mode: int = 0,
+         r0: int = 0, r1: int | None = None):
+    """out[r0:r1] = A x | b - A x | b + A x  (rows r0..r1)."""
+    r1 = a.n_rows if r1 is None else r1
+    call("ddilu_spmv_csr_f64", int(r0), int(r1), a.rp, a.ci, a.val, x, b, out, int(mode))
+    return out
+
+
+@dataclass
+class Schedule:
+    """Level schedule of a triangular factor (SURVEY.md 8c definition)."""
+
+    n: int
+    n_levels: int
+    n_slots: int
+    order: torch.Tensor        # padded schedule, -1 = empty slot
+    level_ptr: torch.Tensor    # n_levels + 1
+    level_rows: torch.Tensor   # rows sorted by (level, index); index descending for U
+    lev: torch.Tensor
+
+
+def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
+    n = t.n_rows
+    lev = empty_i32(max(n, 1))
+    mx = zeros_i32(1)
+    call("ddilu_levels", n, t.rp, t.ci, int(upper), lev, mx)
+    n_levels = int(mx.item()) + 1 if n else 0
+    if n == 0:
+        z = zeros_i32(1)
+        return Schedule(0, 0, 0, z, z, z, z)
+    keys, rows = empty_i32(n), empty_i32(n)
+    ka, ra = empty_i32(n), empty_i32(n)
+    tmp = empty_i32(query("ddilu_sort_tmp_elems", n))
+    level_ptr, slot_ptr = empty_i32(n_levels + 1), empty_i32(n_levels + 1)
+    order = empty_i32(n + 32 * n_levels)
+    call("ddilu_schedule_build", n, lev, n_levels, int(upper), keys, rows, ka, ra, tmp, level_ptr, slot_ptr, order)
+    n_slots = int(slot_ptr[-1].item())
+    return Schedule(n, n_levels, n_slots, order[:n_slots], level_ptr, rows, lev)
+
+
+class TriSolveError(ZeroDivisionError):
+    pass
+
+
+_err_flag = None
+
+
+def _err():
+    global _err_flag
+    if _err_flag is None or _err_flag.device != dev():
+        _err_flag = torch.full((1,), INT_MAX, dtype=I32, device=dev())
+    return _err_flag
+
+
+def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, upper: bool, unit_diag: bool,
+           check: bool = False):
+    """out = T^-1 b with the sync-free kernel; `check` reads the error flag back
+    (a host sync) and raises like the reference does (sparse.py:414-415)."""
+    call("ddilu_sptrsv", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
+         int(unit_diag), _err())
+    if check:
+        bad = int(_err().item())
+        if bad != INT_MAX:
+            _err().fill_(INT_MAX)
+            raise TriSolveError(f"zero or missing diagonal at row {bad}")
+    return out
+
+
+def csr_block(a: DeviceCsr, r0: int, r1: int, c0: int, c1: int) -> DeviceCsr:
+    """Rows [r0, r1) x columns [c0, c1) with columns shifted to start at 0
+    (factor.py:784-803 `_csr_rows_colsplit`, sparse.py:456-471 on ranges)."""
+    nr = r1 - r0
+    rp = zeros_i32(nr + 1)
+    call("ddilu_csr_block_count", a.rp, a.ci, r0, r1, c0, c1, rp)
+    exclusive_scan_(rp, nr)
+    nnz = int(rp[-1].item())
+    ci, val = empty_i32(nnz), empty_f64(nnz)
+    call("ddilu_csr_block_fill", a.rp, a.ci, a.val, r0, r1, c0, c1, rp, ci, val)
+    return DeviceCsr(nr, c1 - c0, rp, ci, val, nnz)
+
+
+def gather_rows(a: DeviceCsr, rows: torch.Tensor | None, n_sel: int, colmap: torch.Tensor, n_cols_out: int,
+                dom: torch.Tensor | None = None, filt: int = 0, resort: bool = True,
+                with_values: bool = True) -> DeviceCsr:
+    """Row gather with column remap (sparse.py:445-453 `_gather`)."""
+    rp = zeros_i32(n_sel + 1)
+    call("ddilu_gather_rows_count", n_sel, rows, a.rp, a.ci, colmap, dom, filt, rp)
+    exclusive_scan_(rp, n_sel)
+    nnz = int(rp[-1].item())
+    ci = empty_i32(nnz)
+    val = empty_f64(nnz) if with_values else None
+    call("ddilu_gather_rows_fill", n_sel, rows, a.rp, a.ci, a.val if with_values else None, colmap, dom, filt, rp,
+         ci, val, int(resort))
+    return DeviceCsr(n_sel, n_cols_out, rp, ci, val, nnz)
+
+
+def index_map(n_total: int, nodes: torch.Tensor, offset: int = 0, base: torch.Tensor | None = None) -> torch.Tensor:
+    """map[nodes[k]] = offset + k, -1 elsewhere (sparse.py:469-470 colmap)."""
+    m = base if base is not None else torch.full((int(n_total),), -1, dtype=I32, device=dev())
+    call("ddilu_build_map", nodes.numel(), nodes, int(offset), m)
+    return m
+
+
+def sym_adjacency(pattern: DeviceCsr) -> DeviceCsr:
+    """Symmetrised pattern without the diagonal (ordering.py:72-81); neighbour
+    order inside a row is unspecified (only sets and degrees are used)."""
+    n = pattern.n_rows
+    rp = zeros_i32(n + 1)
+    call("ddilu_sym_adj_count", n, pattern.rp, pattern.ci, rp)
+    exclusive_scan_(rp, n)
+    nnz = int(rp[-1].item())
+    ci = empty_i32(nnz)
+    cursor = empty_i32(max(n, 1))
+    call("ddilu_sym_adj_fill", n, pattern.rp, pattern.ci, rp, cursor, ci)
+    return DeviceCsr(n, n, rp, ci, None, nnz)
+
+
+def cm_order(adj: DeviceCsr) -> torch.Tensor:
+    """Cuthill-McKee order (not reversed) of a symmetric adjacency."""
+    n = adj.n_rows
+    order = empty_i32(max(n, 1))
+    work = empty_i32(query("ddilu_cm_work_elems", n))
+    call("ddilu_cm_order", n, adj.rp, adj.ci, order, work)
+    return order[:n]
+
+
+def reverse_segments(cm: torch.Tensor, seg_ptr: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(cm)
+    call("ddilu_reverse_segments", cm.numel(), cm, seg_ptr.numel() - 1, seg_ptr, out)
+    return out
+
+
+def gather_i32(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """src[idx] for int32 tensors (index plumbing; torch indexing kernel)."""
+    return src[idx.long()]
+
+
+# ---------------------------------------------------------------------------
+# vector kernels
+
+
+class Reducer:
+    """Workspace of the deterministic two-stage reductions (one per stream of use)."""
+
+    def __init__(self):
+        nbytes = query("ddilu_reduce_ws_bytes")
+        self.ws = torch.zeros(nbytes // 8 + 1, dtype=F64, device=dev())
+
+    def dot(self, n, x, y, out):
+        call("ddilu_dot", int(n), x, y, out, self.ws)
+
+    def axpy_dot(self, n, alpha_dev, alpha_host, v, w, u, out):
+        call("ddilu_axpy_dot", int(n), alpha_dev, float(alpha_host), v, w, u, out, self.ws)
+
+
+def axpy(n, alpha, v, w, alpha_dev=None):
+    call("ddilu_axpy_dot", int(n), alpha_dev, float(alpha), v, w, None, None, None)
+
+
+def scale(n, x, y, alpha_dev=None, alpha_host=1.0, take_sqrt=False, multiply=False):
+    call("ddilu_scale", int(n), x, alpha_dev, float(alpha_host), int(take_sqrt), int(multiply), y)
+
+
+def multi_axpy(n, k, basis, ld, coef, x, overwrite=False):
+    call("ddilu_multi_axpy", int(n), int(k), basis, int(ld), coef, x, int(overwrite))
+
+
+def ewise(n, a, b, op, z):
+    call("ddilu_ewise", int(n), a, b, int(op), z)
+
+
+def gather(n, idx, src, dst):
+    call("ddilu_gather", int(n), idx, src, dst)
+
+
+def scatter(n, idx, src, dst):
+    call("ddilu_scatter", int(n), idx, src, dst)
+
+
+def box_owner(n, dims, factors) -> torch.Tensor:
+    nd = len(dims)
+    arr = ctypes.c_int * nd
+    owner = empty_i32(n)
+    d, f = arr(*[int(v) for v in dims]), arr(*[int(v) for v in factors])
+    call("ddilu_box_owner", int(n), nd, ctypes.addressof(d), ctypes.addressof(f), owner)
+    return owner

@@ -1,0 +1,180 @@
+"""GPU parity, pipeline level: partition -> classify -> setup -> apply -> FGMRES
+through the reference-shaped Python API, against the reference fixtures.
+
+Tolerances (BASELINE.json north_star): permutations, layouts, level schedules
+and sparsity patterns bit-exact; L/U values bit-exact (<= 1e-10 required);
+iteration counts within +-1 at the same final relative residual level; applies
+that contain reductions (inner GMRES) to 1e-9 relative."""
+
+import numpy as np
+import pytest
+
+from _golden import iterations, same_csr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2303_08881_b200 as pkg
+    return pkg
+
+
+def _csr(P):
+    return lambda nr, nc, rp, ci, v: P.CsrMatrix(nr, nc, rp.copy(), ci.copy(), v.copy())
+
+
+def _setup(P, g, tag):
+    pname, ptag, part, pc, fill = tag.split("|")
+    p = int(ptag[1:])
+    a = g.csr(f"p.{pname}.a", _csr(P))
+    hint = tuple(int(v) for v in g[f"p.{pname}.hint"])
+    owner = P.row_block_owner(a.n_rows, p) if part == "rows" else P.partition(a, p, hint)
+    layout = P.classify_and_order(a, owner, p)
+    m = P.make_preconditioner(pc, a, layout, P.FillRule.parse(fill), inner_iters=3)
+    return pname, p, pc, a, owner, layout, m
+
+
+def _rel(x, ref):
+    return float(np.max(np.abs(x - ref)) / max(1e-300, np.max(np.abs(ref))))
+
+
+def test_generators_match_reference(P, golden_pipeline):
+    g = golden_pipeline
+    built = {
+        "aniso2d_16": P.aniso2d(16, 16, (1.0, 0.01)),
+        "aniso3d_10": P.aniso3d(10, 10, 10, (1.0, 1.0, 0.01)),
+        "poisson3d_9x8x7": P.poisson3d(9, 8, 7),
+        "convdiff3d_8": P.convdiff3d(8, 8, 8, (20.0, -10.0, 5.0)),
+        "cd27_8": P.convdiff27(8, 8, 8, (10.0, 10.0, 10.0)),
+    }
+    for name, a in built.items():
+        same_csr(a, g, f"p.{name}.a")
+        assert np.array_equal(P.default_rhs(a), g[f"p.{name}.b"])
+
+
+def test_layout_and_factors_bit_exact(P, golden_pipeline):
+    g = golden_pipeline
+    for tag in g.names("pipeline.cases"):
+        pname, p, pc, a, owner, layout, m = _setup(P, g, tag)
+        k = "c." + tag
+        assert np.array_equal(np.asarray(owner), g[k + ".owner"]), tag
+        assert np.array_equal(layout.interior_starts, g[k + ".interior_starts"])
+        assert np.array_equal(layout.exterior_starts, g[k + ".exterior_starts"])
+        assert np.array_equal(layout.global_perm.forward, g[k + ".global_perm_forward"])
+        for d, dom in enumerate(m.domains):
+            assert np.array_equal(dom.interior_nodes, g[f"{k}.dom{d}.interior_nodes"]), (tag, d)
+            assert np.array_equal(dom.exterior_nodes, g[f"{k}.dom{d}.exterior_nodes"]), (tag, d)
+        if pc == "bj":
+            for d, f in enumerate(m.factors):
+                same_csr(f.lower, g, f"{k}.dom{d}.factors.lower")
+                same_csr(f.upper, g, f"{k}.dom{d}.factors.upper")
+        elif pc == "schur":
+            for d, pf in enumerate(m.partial):
+                same_csr(pf.interior.lower, g, f"{k}.dom{d}.interior.lower")
+                same_csr(pf.interior.upper, g, f"{k}.dom{d}.interior.upper")
+                same_csr(pf.w_block, g, f"{k}.dom{d}.w")
+                same_csr(pf.z_block, g, f"{k}.dom{d}.z")
+                same_csr(pf.s_tilde, g, f"{k}.dom{d}.s")
+                same_csr(pf.schur.lower, g, f"{k}.dom{d}.schur.lower")
+                same_csr(pf.schur.upper, g, f"{k}.dom{d}.schur.upper")
+            same_csr(m.coupling, g, f"{k}.coupling")
+        else:
+            for d, (f, blk) in enumerate(zip(m.smoother, m.blocks)):
+                same_csr(f.lower, g, f"{k}.dom{d}.smoother.lower")
+                same_csr(f.upper, g, f"{k}.dom{d}.smoother.upper")
+                same_csr(blk.interior.lower, g, f"{k}.dom{d}.interior.lower")
+                same_csr(blk.interior.upper, g, f"{k}.dom{d}.interior.upper")
+                same_csr(blk.w_tilde, g, f"{k}.dom{d}.w")
+                same_csr(blk.z_tilde, g, f"{k}.dom{d}.z")
+                same_csr(blk.schur.lower, g, f"{k}.dom{d}.schur.lower")
+                same_csr(blk.schur.upper, g, f"{k}.dom{d}.schur.upper")
+            same_csr(m.a_perm, g, f"{k}.a_perm")
+            assert np.array_equal(m.perm.forward, g[f"{k}.perm_forward"])
+
+
+def test_apply_and_solve_match_reference(P, golden_pipeline):
+    g = golden_pipeline
+    for tag in g.names("pipeline.cases"):
+        pname, p, pc, a, owner, layout, m = _setup(P, g, tag)
+        k = "c." + tag
+        r = g[f"p.{pname}.r"]
+        z = m.apply(r)
+        if pc == "bj" or p == 1:
+            assert np.array_equal(z, g[k + ".apply_r"]), tag       # no reductions on this path
+        else:
+            assert _rel(z, g[k + ".apply_r"]) < 1e-9, (tag, _rel(z, g[k + ".apply_r"]))
+        if (k + ".reduced_matvec") in g:
+            assert _rel(m.reduced_matvec(g[k + ".y"]), g[k + ".reduced_matvec"]) < 1e-13
+        if (k + ".coarse_matvec") in g:
+            y = g[k + ".y"]
+            assert _rel(m.coarse_matvec(y), g[k + ".coarse_matvec"]) < 1e-13
+            assert np.array_equal(m.interpolate(y), g[k + ".interpolate"])
+            assert np.array_equal(m.restrict(r[m.perm.inverse]), g[k + ".restrict"])
+        x, rep = P.fgmres(a, g[f"p.{pname}.b"], m=m.apply,
+                          cfg=P.KrylovConfig(restart=20, rtol=1e-8, max_iters=400))
+        assert abs(rep.iterations - int(g[k + ".its"])) <= 1, (tag, rep.iterations, int(g[k + ".its"]))
+        assert rep.converged == bool(g[k + ".converged"])
+        assert rep.final_relres <= 1e-8
+        assert _rel(x, g[k + ".x"]) < 1e-6, tag
+        hist = g[k + ".history"]
+        m_ = min(len(hist), len(rep.residual_history)) - 1
+        assert np.allclose(rep.residual_history[:m_], hist[:m_], rtol=1e-5, atol=1e-12), tag
+
+
+def test_p1_collapse_bitwise(P):
+    """tests/test_precond.py:108-114,198-205,356-364."""
+    a = P.aniso3d(6, 5, 4)
+    layout = P.classify_and_order(a, P.partition(a, 1))
+    r = np.random.default_rng(1).standard_normal(a.n_rows)
+    outs = [P.make_preconditioner(pc, a, layout).apply(r) for pc in ("bj", "schur", "rap", "rap-milu")]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_krylov_variants(P, golden_pipeline):
+    g = golden_pipeline
+    a = g.csr("p.convdiff3d_8.a", _csr(P))
+    b = g["p.convdiff3d_8.b"]
+    x, rep = P.gmres(a, b, cfg=P.KrylovConfig(restart=15, rtol=1e-9, max_iters=300))
+    assert abs(rep.iterations - int(g["g.gmres_none.its"])) <= 1
+    assert _rel(x, g["g.gmres_none.x"]) < 1e-7
+    f0 = P.ilu0(a)
+    x, rep = P.gmres(a, b, m=f0.solve, cfg=P.KrylovConfig(restart=10, rtol=1e-9, max_iters=300))
+    assert abs(rep.iterations - int(g["g.gmres_ilu0.its"])) <= 1
+    assert _rel(x, g["g.gmres_ilu0.x"]) < 1e-7
+    assert _rel(P.fixed_gmres(lambda v: P.spmv(a, v), b, 5), g["g.fixed_gmres5"]) < 1e-10
+    assert _rel(P.fixed_gmres(lambda v: P.spmv(a, v), b, 4, apply_m=f0.solve), g["g.fixed_gmres4_m"]) < 1e-10
+    # b = 0 -> zero iterations, converged (tests/test_krylov.py:65-70)
+    x, rep = P.fgmres(a, np.zeros(a.n_rows))
+    assert rep.iterations == 0 and rep.converged and not x.any()
+
+
+def test_iteration_counts_baseline_shapes(P):
+    """tests/golden/iterations.json: BASELINE-shaped inputs (restart 50, rtol 1e-8, inner 3)."""
+    for rec in iterations():
+        dims = tuple(rec["dims"])
+        kind = rec["kind"]
+        spec = P.ProblemSpec(kind, dims, velocity=tuple(rec["param"]) if kind == "convdiff27" else (0.0, 0.0, 0.0),
+                             eps=tuple(rec["param"]) if kind != "convdiff27" else ())
+        cfg = P.RunConfig(spec, domains=rec["p"], precond=rec["precond"], fill=P.FillRule.parse(rec["fill"]))
+        out, rep = P.run(cfg)
+        assert abs(rep.iterations - rec["its"]) <= 1, (rec, rep.iterations)
+        assert rep.converged and rep.final_relres <= 1e-8
+
+
+def test_roundtrip_properties_at_scale(P):
+    """Size-independent checks at a size the oracle is not run at: the ILU(0)
+    residual vanishes on the pattern ((LU - A) 1 restricted ... via MILU identity),
+    and the solve really solves."""
+    a = P.aniso3d(96, 96, 96)
+    ones = np.ones(a.n_rows)
+    f = P.milu0(a)
+    assert np.max(np.abs(f.lu_matvec(ones) - P.spmv(a, ones))) < 1e-10     # (LU) 1 = A 1 (tests/test_acceptance.py:73-87)
+    b = P.default_rhs(a)
+    layout = P.classify_and_order(a, P.partition(a, 8, (96, 96, 96)), 8)
+    m = P.make_preconditioner("schur", a, layout)
+    x, rep = P.fgmres(a, b, m=m.apply)
+    assert rep.converged
+    assert np.max(np.abs(x - 1.0)) < 1e-5
+    assert np.linalg.norm(P.spmv(a, x) - b) / np.linalg.norm(b) <= 1.0001e-8
