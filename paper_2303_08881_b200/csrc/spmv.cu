@@ -28,7 +28,8 @@ __global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const i
     __shared__ int srp[SPMV_ROWS + 1];
     const int row0 = r0 + blockIdx.x * SPMV_ROWS;
     const int nrows = min(SPMV_ROWS, r1 - row0);
-    if (threadIdx.x <= nrows) srp[threadIdx.x] = rp[row0 + threadIdx.x];
+    if (threadIdx.x < nrows) srp[threadIdx.x] = rp[row0 + threadIdx.x];
+    if (threadIdx.x == 0) srp[nrows] = rp[row0 + nrows];
     __syncthreads();
     const int e0 = srp[0], e1 = srp[nrows];
     const int row = row0 + threadIdx.x;

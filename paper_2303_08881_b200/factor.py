@@ -146,7 +146,7 @@ def d_factor_level0(a: D.DeviceCsr, n_elim: int, milu: bool = False, target: tor
 
 def d_ilut(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float,
            safeguard: float = DIAG_SAFEGUARD) -> DevFactors:
-    from .ilut import d_ilut_factor
+    from ._ilut import d_ilut_factor
     return d_ilut_factor(a, n_elim, tau, maxfill, tau_s, safeguard)
 
 
