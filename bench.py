@@ -1,0 +1,335 @@
+"""bench.py -- DD-ILU preconditioner + FGMRES hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: launched by torchrun, one rank per GPU)
+
+Workload (BASELINE.json metric): 3D anisotropic 7-point diffusion 256^3,
+eps = (1, 1, 0.01), b = A*1; two-level ILU(0) with the implicit Schur-complement
+inner GMRES ("schur", 3 inner steps); FGMRES(50) to 1e-8; p = 8 subdomains
+dealt to the N GPUs in blocks of 8/N (so iteration counts do not depend on N:
+strong scaling).  One step = one complete setup + solve.
+
+JSON line: metric / value = seconds per step (setup + solve, inputs already in
+HBM); e2e = the same through the host API with host buffers (H2D of the CSR
+arrays and b, D2H of x inside the timed region); roofline = the dominant kernel
+(sync-free SpTRSV of the interior factor) from CUDA events inside the timed
+region; cpu_baseline = the CPU oracle (port of the reference, 1 core) on a
+bounded sample of the same workload, scaled to the full job.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+EPS = (1.0, 1.0, 0.01)
+P_DOMAINS = 8
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def algorithmic_bytes_sptrsv(nnz, n):
+    """12 B per stored entry (fp64 value + int32 column), 4 B row
+    pointer, 8 B right-hand side, 8 B solution per row."""
+    return 12 * nnz + 4 * (n + 1) + 16 * n
+
+
+def run_ours(args):
+    import torch
+    import paper_2303_08881_b200 as P
+    from paper_2303_08881_b200 import _lib, dist
+    from paper_2303_08881_b200 import device as D
+
+    comm = dist.init_from_env()
+    rank, world = comm.rank, comm.size
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    n1 = args.n
+    dims = (n1, n1, n1)
+    a = P.aniso3d(*dims, EPS)                     # host CSR (int64 / fp64), untimed like the reference's run()
+    rule = P.FillRule.parse(args.fill)
+    cfg = P.RunConfig(P.ProblemSpec("aniso3d", dims, eps=EPS), domains=args.domains, precond=args.precond, fill=rule)
+    kcfg = P.KrylovConfig(restart=cfg.restart, rtol=cfg.rtol, max_iters=cfg.max_iters)
+    # pinned host copies for the end-to-end arm
+    host = [torch.from_numpy(x).pin_memory() for x in (a.row_ptr, a.col_idx, a.values)]
+    ad = a.device()
+    ones = torch.ones(a.n_cols, dtype=torch.float64, device="cuda")
+    b_dev = torch.empty(a.n_rows, dtype=torch.float64, device="cuda")
+    D.spmv(ad, ones, b_dev)
+    b_host = b_dev.cpu().pin_memory()
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB > 126 MB L2
+
+    def step(resident: bool):
+        """setup + solve; returns (record fields, x).  resident: A and b already in HBM."""
+        flush.fill_(0.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if resident:
+            mat, rhs = a, b_dev
+        else:
+            mat = P.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)   # fresh object: uploads again
+            rp, ci, v = (h.to("cuda", non_blocking=True) for h in host)
+            ci32, rp32 = D.empty_i32(ci.numel()), D.empty_i32(rp.numel())
+            D.call("ddilu_narrow_i64", ci.numel(), ci, ci32)
+            D.call("ddilu_narrow_i64", rp.numel(), rp, rp32)
+            mat._dev = D.DeviceCsr(a.n_rows, a.n_cols, rp32, ci32, v, a.nnz)
+            rhs = b_host.to("cuda", non_blocking=True)
+        owner = P.partition(mat, args.domains, grid_hint=dims)
+        layout = P.classify_and_order(mat, owner, args.domains)
+        m = P.make_preconditioner(args.precond, mat, layout, rule, inner_iters=cfg.inner_iters)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        x, rep = P.fgmres(mat, rhs, m=m.apply, cfg=kcfg)
+        if not resident:
+            x = x.cpu()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        return {"setup_s": t1 - t0, "solve_s": t2 - t1, "its": rep.iterations, "relres": rep.final_relres,
+                "converged": rep.converged}, x, m
+
+    def timed(resident: bool, steps: int):
+        comm.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _lib.launches
+        e0.record()
+        recs = []
+        m = None
+        for _ in range(steps):
+            rec, x, m = step(resident)
+            recs.append(rec)
+        e1.record()
+        torch.cuda.synchronize()
+        comm.barrier()
+        total = e0.elapsed_time(e1) * 1e-3
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        if comm.active:
+            import torch.distributed as tdist
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item()), recs, _lib.launches - l0, m
+
+    for _ in range(args.warmup):
+        step(True)
+    # --- timed region 1: inputs resident in HBM, kernels watched with CUDA events
+    watch = ("ddilu_sptrsv_sell", "ddilu_spmv_csr_f64", "ddilu_axpy_dot", "ddilu_dot")
+    _lib.profile = {k: [] for k in watch}
+    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    total, recs, launches, m = timed(True, args.steps)
+    clocks = sampler.stop() if sampler else None
+    prof, _lib.profile = _lib.profile, None
+    kern = {}
+    for name, evs in prof.items():
+        if evs:
+            ms = np.array([e0.elapsed_time(e1) for e0, e1, _ in evs])
+            kern[name] = {"launches": len(ms), "total_s": float(ms.sum() * 1e-3), "avg_us": float(ms.mean() * 1e3)}
+    # --- timed region 2: end to end through the host API (H2D + D2H inside)
+    e2e_steps = max(1, min(args.steps, 2))
+    step(False)
+    e2e_total, e2e_recs, _, _ = timed(False, e2e_steps)
+    h2d = int(sum(h.numel() * h.element_size() for h in host) + b_host.numel() * 8)
+    d2h = int(a.n_rows * 8)
+
+    if rank != 0:
+        return
+    peak, peak_src = measured_peak()
+    # dominant kernel: the interior lower solve (largest SpTRSV of the apply)
+    s = m.system
+    fac = m._p.interior if args.precond == "schur" else (m._f if args.precond == "bj" else m._interior)
+    nL, nU, nrows = fac.lower.nnz, fac.upper.nnz, fac.n
+    # split the watched sptrsv launches by size: interior-factor solves are the long ones
+    ev = [(e0.elapsed_time(e1) * 1e-3) for e0, e1, _ in prof["ddilu_sptrsv_sell"]]
+    big = sorted(ev)[len(ev) // 2:] if ev else []
+    # bytes per launch: average of the L and U interior solves (they alternate 1:1)
+    alg = 0.5 * (algorithmic_bytes_sptrsv(nL, nrows) + algorithmic_bytes_sptrsv(nU, nrows))
+    dur = float(np.mean(big)) if big else float("nan")
+    achieved = alg / dur / 1e9 if big else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"sptrsv_sell_{args.n}_{args.precond}")
+        except Exception:
+            traffic = None
+    step_s = total / args.steps
+    rec = recs[-1]
+    line = {
+        "metric": "setup+solve seconds, FGMRES(50) rtol 1e-8, two-level DD-ILU on 3D anisotropic 7-pt diffusion",
+        "value": step_s, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"aniso3d {n1}^3 eps=(1,1,0.01), b=A*1, {args.precond}/{args.fill}, "
+                               f"p={args.domains} subdomains ({args.domains // world} per GPU), FGMRES(50), inner 3",
+                   "n": a.n_rows, "nnz": a.nnz, "cache": "256 MB L2 flush before every step; working set >> L2"},
+        "its": rec["its"], "converged": rec["converged"], "final_relres": rec["relres"],
+        "setup_s": float(np.mean([r["setup_s"] for r in recs])), "solve_s": float(np.mean([r["solve_s"] for r in recs])),
+        "e2e": {"value": e2e_total / e2e_steps, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "setup_s": float(np.mean([r["setup_s"] for r in e2e_recs])),
+                "solve_s": float(np.mean([r["solve_s"] for r in e2e_recs]))},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "kernel": "sptrsv_sell (interior L_B / U_B solves)", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg, "avg_launch_us": dur * 1e6,
+                     "levels": fac.sched_l.n_levels,
+                     "latency_bound_us": fac.sched_l.n_levels * 0.38,
+                     "note": "dependency-latency bound = levels x 0.38 us (measured L2 store->poll hop)"},
+        "kernels": kern,
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, full_its=rec["its"])
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the oracle port of the reference, one core
+
+
+def cpu_sample(args, n_sample):
+    """One run of the reference pipeline (oracle port) on the n_sample^3 version
+    of the workload; returns the record."""
+    from oracle import ddilu_oracle as orc
+    dims = (n_sample,) * 3
+    a = orc.aniso(dims, EPS)
+    rec, rep, _ = orc.run(a, dims, args.domains, args.precond, orc.Rule.parse(args.fill))
+    rec["n_sample"] = n_sample
+    return rec
+
+
+def scale_to_full(rec, args, full_its=None):
+    """Scale a sample to the full job: setup ~ rows; solve ~ rows x iterations."""
+    ratio = (args.n / rec["n_sample"]) ** 3
+    its_full = full_its if full_its else rec["its"] * (args.n / rec["n_sample"])   # its grow ~ linearly with n
+    return rec["setup_s"] * ratio + rec["solve_s"] / max(1, rec["its"]) * its_full * ratio
+
+
+def cpu_baseline(args, full_its=None):
+    ns = args.cpu_sample
+    t0 = time.perf_counter()
+    rec = cpu_sample(args, ns)
+    return {"value": scale_to_full(rec, args, full_its), "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"oracle (C port of the reference, 1 of {os.cpu_count()} cores) on aniso3d {ns}^3, same "
+                      f"preconditioner/partition: setup {rec['setup_s']:.2f} s + solve {rec['solve_s']:.2f} s, "
+                      f"{rec['its']} its; scaled by rows ({args.n}^3/{ns}^3) and by the iteration count of the full job",
+            "sample_seconds": time.perf_counter() - t0, "sample_its": rec["its"]}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ddilu_oracle as orc
+    orc.build()
+    ns = args.cpu_sample
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample(args, max(16, ns // 2))
+    t0 = time.perf_counter()
+    recs = [cpu_sample(args, ns) for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    vals = [scale_to_full(r, args) for r in recs]
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference",
+        "metric": "setup+solve seconds, FGMRES(50) rtol 1e-8, two-level DD-ILU on 3D anisotropic 7-pt diffusion",
+        "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"aniso3d {args.n}^3 eps=(1,1,0.01), b=A*1, {args.precond}/{args.fill}, "
+                               f"p={args.domains} subdomains, FGMRES(50), inner 3",
+                   "sample": f"each step = the {ns}^3 version of the workload on 1 CPU core, scaled to {args.n}^3"},
+        "its": recs[-1]["its"],
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
+                         "sample": f"oracle port, aniso3d {ns}^3 per step ({wall / args.steps:.1f} s of CPU per step), "
+                                   f"scaled by rows and iterations (its ~ n)"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--n", type=int, default=256, help="grid points per axis")
+    ap.add_argument("--precond", default="schur", choices=("bj", "schur", "rap", "rap-milu"))
+    ap.add_argument("--fill", default="ilu0")
+    ap.add_argument("--domains", type=int, default=P_DOMAINS)
+    ap.add_argument("--cpu-sample", type=int, default=64, help="grid size of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -23,7 +23,8 @@
 extern "C" {
 #endif
 
-/* ---- tuning knobs (no reference equivalent): "trsv_blocks_per_sm", "trsv_sleep_ns" */
+/* ---- tuning knobs (no reference equivalent): "trsv_blocks_per_sm", "trsv_depth",
+ * "trsv_pipe", "trsv_pipe_warps_per_sm", "trsv_sleep_ns" */
 int ddilu_set_tuning(const char *key, int value);
 
 /* ---- primitives used by the count -> scan -> fill setup passes (the reference
@@ -56,6 +57,21 @@ int ddilu_schedule_build(int n, const int *lev, int n_levels, int upper, int *ke
  * smallest failing row (the reference raises ZeroDivisionError for that row). */
 int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
                  const double *b, double *x, int upper, int unit_diag, int *err, void *stream);
+
+/* Schedule-ordered sliced-ELL form of a factor (group = 32 schedule slots = one
+ * warp): gw32[g] = 32 * (longest dependency list in group g) -> scan -> goff;
+ * entry k of lane l at goff[g] + 32*k + l (col -1 = padding); sdiag[slot] = pivot.
+ * goff == NULL selects the uniform layout: every group has `uniform_width` entries
+ * per lane at g * 32 * uniform_width (no descriptor load on the dependency chain).
+ * ddilu_sptrsv_sell is the production solve (same semantics as ddilu_sptrsv;
+ * sdiag == NULL means unit diagonal). */
+int ddilu_sell_width(int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
+                     int upper, int unit_diag, int *gw32, double *sdiag, int *bad_row, void *stream);
+int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
+                    int upper, const int *goff, int uniform_width, int *scol, double *sval, void *stream);
+int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff, int uniform_width,
+                      const int *scol, const double *sval, const double *sdiag, const double *b, double *x,
+                      void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,

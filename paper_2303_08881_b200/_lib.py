@@ -31,6 +31,9 @@ SIGNATURES = {
     "ddilu_levels": (_I, [_I, _P, _P, _I, _P, _P, _P]),
     "ddilu_schedule_build": (_I, [_I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "ddilu_sell_width": (_I, [_I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "ddilu_sell_fill": (_I, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
+    "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),
@@ -69,6 +72,11 @@ SIGNATURES = {
 
 _lib = None
 launches = 0  # kernels-launching C-ABI calls made so far (bench.py reports the delta)
+
+# Optional per-entry timing with CUDA events on the launching stream (bench.py):
+# profile = {"name": [(start_event, end_event, tag), ...]} for the watched entries.
+profile = None
+profile_tag = None
 
 
 class DdiluError(RuntimeError):
@@ -114,7 +122,14 @@ def call(name: str, *args):
     current torch stream is appended as the last argument."""
     global launches
     fn = getattr(load(), name)
-    rc = fn(*[_arg(a) for a in args], stream_ptr())
+    if profile is not None and name in profile:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rc = fn(*[_arg(a) for a in args], stream_ptr())
+        e1.record()
+        profile[name].append((e0, e1, profile_tag))
+    else:
+        rc = fn(*[_arg(a) for a in args], stream_ptr())
     launches += 1
     if rc != 0:
         raise DdiluError(f"{name} failed with status {rc}")

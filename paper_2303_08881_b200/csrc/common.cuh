@@ -64,6 +64,15 @@ __device__ __forceinline__ double ld_l2(const double *p) {
 __device__ __forceinline__ void st_l2(double *p, double v) {
     asm volatile("st.volatile.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+// gpu-scope relaxed (coherent at L2, no system-scope semantics)
+__device__ __forceinline__ double ld_gpu(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_gpu(double *p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 __device__ __forceinline__ int ld_l2(const int *p) {
     int v;
     asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

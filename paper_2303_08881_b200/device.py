@@ -133,6 +133,17 @@ class Schedule:
     level_ptr: torch.Tensor    # n_levels + 1
     level_rows: torch.Tensor   # rows sorted by (level, index); index descending for U
     lev: torch.Tensor
+    sell: dict = None          # unit_diag -> Sell (schedule-ordered sliced-ELL copy of the factor)
+
+
+@dataclass
+class Sell:
+    goff: torch.Tensor | None  # n_groups + 1 offsets into scol / sval; None = uniform width
+    width: int                 # entries per lane in the uniform layout
+    scol: torch.Tensor
+    sval: torch.Tensor
+    sdiag: torch.Tensor | None
+    bad_row: int               # first row with a zero / missing diagonal, or INT_MAX
 
 
 def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
@@ -158,6 +169,40 @@ class TriSolveError(ZeroDivisionError):
     pass
 
 
+USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)
+UNIFORM_SELL = True
+
+
+def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> Sell:
+    n_groups = sched.n_slots // 32
+    gw = zeros_i32(n_groups + 1)
+    sdiag = None if unit_diag else empty_f64(max(1, sched.n_slots))
+    bad = torch.full((1,), INT_MAX, dtype=I32, device=dev())
+    call("ddilu_sell_width", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), int(unit_diag), gw, sdiag,
+         bad)
+    wmax = int(gw[:n_groups].max().item()) // 32 if n_groups else 0
+    exclusive_scan_(gw, n_groups)
+    total = int(gw[-1].item())
+    uniform = wmax * 32 * n_groups
+    if UNIFORM_SELL and uniform <= 1.25 * total + 1024:
+        # short, regular rows (stencils): pad every group to the widest one and drop the descriptor array
+        scol, sval = empty_i32(max(1, uniform)), empty_f64(max(1, uniform))
+        call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), None, wmax, scol, sval)
+        return Sell(None, wmax, scol, sval, sdiag, int(bad.item()))
+    scol, sval = empty_i32(max(1, total)), empty_f64(max(1, total))
+    call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), gw, 0, scol, sval)
+    return Sell(gw, 0, scol, sval, sdiag, int(bad.item()))
+
+
+def get_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> Sell:
+    if sched.sell is None:
+        sched.sell = {}
+    key = bool(unit_diag)
+    if key not in sched.sell:
+        sched.sell[key] = build_sell(t, sched, upper, unit_diag)
+    return sched.sell[key]
+
+
 _err_flag = None
 
 
@@ -172,6 +217,15 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
            check: bool = False):
     """out = T^-1 b with the sync-free kernel; `check` reads the error flag back
     (a host sync) and raises like the reference does (sparse.py:414-415)."""
+    if t.n_rows == 0:
+        return out
+    if USE_SELL:
+        sell = get_sell(t, sched, upper, unit_diag)
+        if check and sell.bad_row != INT_MAX:
+            raise TriSolveError(f"zero or missing diagonal at row {sell.bad_row}")
+        call("ddilu_sptrsv_sell", t.n_rows, sched.n_slots, sched.n_levels, sched.order, sell.goff, sell.width,
+             sell.scol, sell.sval, sell.sdiag, b, out)
+        return out
     call("ddilu_sptrsv", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
          int(unit_diag), _err())
     if check:

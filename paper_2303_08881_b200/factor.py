@@ -99,7 +99,9 @@ class DevFactors:
         return self._su
 
     def prepare(self):
-        self.sched_l, self.sched_u  # noqa: B018  (build both schedules now, inside setup)
+        # build both schedules and their solve layouts now, inside setup
+        D.get_sell(self.lower, self.sched_l, False, True)
+        D.get_sell(self.upper, self.sched_u, True, False)
         if self._tmp is None:
             self._tmp = D.empty_f64(max(self.n, 1))
         return self

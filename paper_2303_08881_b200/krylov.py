@@ -294,7 +294,9 @@ def _device_operator(op, n: int) -> DevOp:
 
 def _solve(a, b, m, x0, cfg: KrylovConfig | None, flexible: bool):
     cfg = cfg or KrylovConfig()
-    b = np.asarray(b, dtype=np.float64)
+    on_device = isinstance(b, torch.Tensor)   # device-resident fast path: CUDA tensor in -> CUDA tensor out
+    if not on_device:
+        b = np.asarray(b, dtype=np.float64)
     t0 = time.perf_counter()
     owner = getattr(m, "__self__", None)
     fast = getattr(owner, "_solve_local", None)
@@ -304,10 +306,12 @@ def _solve(a, b, m, x0, cfg: KrylovConfig | None, flexible: bool):
         n = len(b)
         apply_a = _device_operator(a, n)
         apply_m = _device_operator(m, n) if m is not None else None
-        bd = D.to_device_f64(b)
-        x0d = D.to_device_f64(np.asarray(x0, dtype=np.float64)) if x0 is not None else None
+        bd = b if on_device else D.to_device_f64(b)
+        x0d = None
+        if x0 is not None:
+            x0d = x0 if isinstance(x0, torch.Tensor) else D.to_device_f64(np.asarray(x0, dtype=np.float64))
         xd, report = restarted_device(n, apply_a, apply_m, bd, x0d, cfg, flexible, Comm())
-        x = xd.cpu().numpy()
+        x = xd.clone() if on_device else xd.cpu().numpy()
     torch.cuda.synchronize()
     report.solve_seconds = time.perf_counter() - t0
     return x, report

@@ -257,19 +257,21 @@ class _DDPrecond:
         iteration, halo exchange inside the matvec, allreduced dots."""
         s = self.system
         n = self.layout.n
-        bd = D.to_device_f64(b)
+        on_device = isinstance(b, torch.Tensor)
+        bd = b if on_device else D.to_device_f64(b)
         b_loc = D.empty_f64(max(1, s.n_loc))
         D.gather(s.n_loc, s.nodes, bd, b_loc)
         x0_loc = None
         if x0 is not None:
             x0_loc = D.empty_f64(max(1, s.n_loc))
-            D.gather(s.n_loc, s.nodes, D.to_device_f64(np.asarray(x0, dtype=np.float64)), x0_loc)
+            x0d = x0 if isinstance(x0, torch.Tensor) else D.to_device_f64(np.asarray(x0, dtype=np.float64))
+            D.gather(s.n_loc, s.nodes, x0d, x0_loc)
         x_loc, report = restarted_device(s.n_loc, s.spmv, self.apply_local, b_loc, x0_loc, cfg, flexible, s.comm,
                                          pad=s.n_halo)
         x = torch.zeros(n, dtype=D.F64, device=D.dev()) if s.comm.active else D.empty_f64(n)
         D.scatter(s.n_loc, s.nodes, x_loc, x)
         s.comm.allreduce_sum_(x)
-        return x.cpu().numpy(), report
+        return (x if on_device else x.cpu().numpy()), report
 
 
 class BjIluPrecond(_DDPrecond):

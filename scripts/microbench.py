@@ -78,20 +78,37 @@ def main():
     ubytes = 12 * nu + 4 * (n + 1) + 16 * n
     emit(what="factors", rows=n, nnz_l=nl, nnz_u=nu, levels_l=f.sched_l.n_levels, levels_u=f.sched_u.n_levels,
          slots_l=f.sched_l.n_slots)
-    configs = [(4, 0)]
+    configs = [(3, 0, True, 0)]
     if args.sweep:
-        configs = [(b, sl) for b in (1, 2, 3, 4, 6, 8) for sl in (0, 20, 100)]
-    for bps, sleep in configs:
-        query("ddilu_set_tuning", b"trsv_blocks_per_sm", bps)
-        query("ddilu_set_tuning", b"trsv_sleep_ns", sleep)
+        configs = [(b, 0, True, 0) for b in (2, 3, 4)]
+    for bps, sleep, use_sell, pipe in configs:
+        D.USE_SELL = use_sell
+        query("ddilu_set_tuning", b"trsv_pipe", pipe)
+        query("ddilu_set_tuning", b"trsv_pipe_warps_per_sm" if pipe else b"trsv_blocks_per_sm", bps)
         tl, tlmin = timed(lambda: f.lower_solve(r, t), flush=flush)
         tu, tumin = timed(lambda: f.upper_solve(t, z), flush=flush)
-        emit(what="sptrsv", blocks_per_sm=bps, sleep_ns=sleep, lower_s=tl, upper_s=tu, lower_min_s=tlmin,
+        emit(what="sptrsv", kernel=("pipe" if pipe else "sell") if use_sell else "csr", blocks_per_sm=bps, sleep_ns=sleep, lower_s=tl, upper_s=tu, lower_min_s=tlmin,
              upper_min_s=tumin, lower_gbs=lbytes / tl / 1e9, upper_gbs=ubytes / tu / 1e9,
              lower_frac=lbytes / tl / 1e9 / PEAK, upper_frac=ubytes / tu / 1e9 / PEAK,
              hop_us_lower=tl / f.sched_l.n_levels * 1e6, hop_us_upper=tu / f.sched_u.n_levels * 1e6)
-    query("ddilu_set_tuning", b"trsv_blocks_per_sm", 4)
-    query("ddilu_set_tuning", b"trsv_sleep_ns", 0)
+    query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
+    query("ddilu_set_tuning", b"trsv_pipe", 0)
+    D.USE_SELL = True
+    if args.p > 1:   # the small, deep interface solves of the two-level preconditioners
+        ms = P.schur_setup(a, layout)
+        sf = ms._p.schur
+        ne = sf.n
+        rs, ts_ = torch.randn(ne, dtype=torch.float64, device="cuda"), torch.empty(ne, dtype=torch.float64, device="cuda")
+        query("ddilu_set_tuning", b"trsv_pipe", 0)
+        query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
+        for w in ((0, 4, 8, 16, 24, 32, 64) if args.sweep else (24,)):
+            query("ddilu_set_tuning", b"trsv_depth", w)
+            tl, _ = timed(lambda: sf.lower_solve(rs, ts_), flush=flush)
+            emit(what="schur_lower", warps_per_sm=w, rows=ne, levels=sf.sched_l.n_levels, s=tl,
+                 hop_us=tl / sf.sched_l.n_levels * 1e6)
+        del ms
+    query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
+    query("ddilu_set_tuning", b"trsv_depth", 24)
     # SpMV
     al = s.a_loc
     x = torch.randn(al.n_cols, dtype=torch.float64, device="cuda")
