@@ -73,6 +73,21 @@ int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const 
                       const int *scol, const double *sval, const double *sdiag, const double *b, double *x,
                       void *stream);
 
+/* Block-local variant for small, deep, block-diagonal factors (interface factors L_S/U_S:
+ * precond.py:239-245 `_schur_solve`, :361-366 `_coarse_precond`): one CTA per independent row
+ * block seg_ptr[d]..seg_ptr[d+1], levels separated by a CTA barrier.  start/cnt[d*n_levels+l]
+ * = first position / number of rows of block d in level l inside level_rows. */
+int ddilu_blocklocal_table(int n, int n_blocks, const int *seg_ptr, int n_levels, const int *lev,
+                           const int *level_rows, int *start, int *cnt, void *stream);
+int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *start, const int *cnt, const int *level_rows,
+                            const int *row_ptr, const int *col_idx, const double *values, const double *b, double *x,
+                            int upper, int unit_diag, int *err, void *stream);
+
+/* same sweep on the SELL arrays; sstart[d*n_levels+l] = first SCHEDULE SLOT of block d in level l */
+int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *order,
+                                 const int *goff, int uniform_width, const int *scol, const double *sval,
+                                 const double *sdiag, const double *b, double *x, void *stream);
+
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,
                       double *rownorm, void *stream);

@@ -406,6 +406,221 @@ __global__ void __launch_bounds__(128) sptrsv_sell_pipe(int n_groups, const int 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Block-local solve for SMALL, DEEP factors that are block diagonal (the
+// interface factors L_S / U_S of the two-level preconditioners: one independent
+// block per subdomain, ~100-400 rows per level).  One CTA owns one block and
+// walks its levels with __syncthreads() in between: a level costs one L2 load of
+// the dependencies + a CTA barrier (deterministic, no polling, no cooperative
+// launch); the row data of the next level is prefetched into registers before
+// the current level is finished.  Row sums in storage order: bit-identical.
+constexpr int BL_THREADS = 1024;
+constexpr int BL_PRE = 6;  // entries of a row kept in registers
+
+__global__ void blocklocal_table(int n, int n_blocks, const int *__restrict__ seg_ptr, int n_levels,
+                                 const int *__restrict__ lev, const int *__restrict__ level_rows,
+                                 int *start, int *cnt) {
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+        const int row = level_rows[q];
+        int lo = 0, hi = n_blocks;  // largest d with seg_ptr[d] <= row
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (seg_ptr[mid] <= row) lo = mid; else hi = mid;
+        }
+        const long long slot = (long long)lo * n_levels + lev[row];
+        atomicMin(start + slot, (int)q);
+        atomicAdd(cnt + slot, 1);
+    }
+}
+
+struct BlRow {
+    int row, k, ke;
+    int c[BL_PRE];
+    double a[BL_PRE];
+    double rhs;
+};
+
+__device__ __forceinline__ void bl_load(BlRow &r, bool active, int q, const int *__restrict__ level_rows,
+                                        const int *__restrict__ rp, const int *__restrict__ ci,
+                                        const double *__restrict__ val, const double *__restrict__ b) {
+    r.row = -1;
+    r.k = r.ke = 0;
+    r.rhs = 0.0;
+    if (active) {
+        r.row = level_rows[q];
+        r.k = rp[r.row];
+        r.ke = rp[r.row + 1];
+        r.rhs = b[r.row];
+    }
+#pragma unroll
+    for (int u = 0; u < BL_PRE; ++u) {
+        const bool in = r.k + u < r.ke;
+        r.c[u] = in ? ci[r.k + u] : -1;
+        r.a[u] = in ? val[r.k + u] : 0.0;
+    }
+}
+
+template <bool UPPER>
+__device__ __forceinline__ void bl_finish(const BlRow &r, const int *__restrict__ ci, const double *__restrict__ val,
+                                          double *x, int unit_diag, int *err) {
+    if (r.row < 0) return;
+    double s = r.rhs, diag = 1.0;
+    bool seen = false;
+#pragma unroll
+    for (int u = 0; u < BL_PRE; ++u) {
+        const int j = r.c[u];
+        if (j < 0) continue;
+        if (UPPER ? j > r.row : j < r.row) s -= r.a[u] * x[j];
+        else if (j == r.row) {
+            diag = r.a[u];
+            seen = true;
+        }
+    }
+    for (int k = r.k + BL_PRE; k < r.ke; ++k) {  // long rows
+        const int j = ci[k];
+        if (UPPER ? j > r.row : j < r.row) s -= val[k] * x[j];
+        else if (j == r.row) {
+            diag = val[k];
+            seen = true;
+        }
+    }
+    if (!unit_diag) {
+        if (!seen || fabs(diag) < 1e-300) {
+            atomicMin(err, r.row);
+            s = __longlong_as_double(0x7FF8000000000000LL);
+        } else {
+            s = s / diag;
+        }
+    }
+    x[r.row] = s;
+}
+
+template <bool UPPER>
+__global__ void __launch_bounds__(BL_THREADS) sptrsv_blocklocal(int n_levels, const int *__restrict__ start,
+                                                                const int *__restrict__ cnt,
+                                                                const int *__restrict__ level_rows,
+                                                                const int *__restrict__ rp, const int *__restrict__ ci,
+                                                                const double *__restrict__ val,
+                                                                const double *__restrict__ b, double *x, int unit_diag,
+                                                                int *err) {
+    const int *st = start + (long long)blockIdx.x * n_levels;
+    const int *ct = cnt + (long long)blockIdx.x * n_levels;
+    BlRow cur, nxt;
+    int c0 = n_levels > 0 ? ct[0] : 0;
+    bl_load(nxt, (int)threadIdx.x < c0, n_levels > 0 ? st[0] + (int)threadIdx.x : 0, level_rows, rp, ci, val, b);
+    for (int l = 0; l < n_levels; ++l) {
+        cur = nxt;
+        const int c = c0, s0 = st[l];
+        if (l + 1 < n_levels) {
+            c0 = ct[l + 1];
+            bl_load(nxt, (int)threadIdx.x < c0, st[l + 1] + (int)threadIdx.x, level_rows, rp, ci, val, b);
+        }
+        bl_finish<UPPER>(cur, ci, val, x, unit_diag, err);
+        for (int t = threadIdx.x + BL_THREADS; t < c; t += BL_THREADS) {  // levels wider than the CTA
+            BlRow extra;
+            bl_load(extra, true, s0 + t, level_rows, rp, ci, val, b);
+            bl_finish<UPPER>(extra, ci, val, x, unit_diag, err);
+        }
+        __syncthreads();
+    }
+}
+
+
+// Block-local sweep on the schedule-ordered SELL arrays: the address of every
+// operand of slot s is computable from s, so the register prefetch is one load
+// deep (row id two levels ahead; entries, pivot and right-hand side one level ahead).
+struct BsRow {
+    int row;
+    int c[SELL_CHUNK];
+    double a[SELL_CHUNK];
+    double rhs, piv;
+    long long off;
+    int w, lane;
+};
+
+template <bool HAS_DIAG>
+__device__ __forceinline__ void bs_load(BsRow &r, int row, bool active, int slot, const int *__restrict__ goff, int uw,
+                                        const int *__restrict__ scol, const double *__restrict__ sval,
+                                        const double *__restrict__ sdiag, const double *__restrict__ b) {
+    r.row = active ? row : -1;
+    r.w = 0;
+    r.off = 0;
+    r.lane = slot & 31;
+    r.rhs = 0.0;
+    r.piv = 1.0;
+    if (active) {
+        const long long g = slot >> 5;
+        r.off = goff ? goff[g] : g * 32LL * uw;
+        r.w = goff ? (goff[g + 1] - (int)r.off) >> 5 : uw;
+        if (r.row >= 0) r.rhs = b[r.row];
+        if (HAS_DIAG) r.piv = sdiag[slot];
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_CHUNK; ++u) {
+        const bool in = u < r.w;
+        r.c[u] = in ? scol[r.off + 32 * u + r.lane] : -1;
+        r.a[u] = in ? sval[r.off + 32 * u + r.lane] : 0.0;
+    }
+}
+
+template <bool HAS_DIAG>
+__device__ __forceinline__ void bs_finish(const BsRow &r, const int *__restrict__ scol, const double *__restrict__ sval,
+                                          double *x) {
+    if (r.row < 0) return;
+    double s = r.rhs;
+#pragma unroll
+    for (int u = 0; u < SELL_CHUNK; ++u)
+        if (r.c[u] >= 0) s -= r.a[u] * x[r.c[u]];
+    for (int k = SELL_CHUNK; k < r.w; ++k) {
+        const int j = scol[r.off + 32 * k + r.lane];
+        if (j >= 0) s -= sval[r.off + 32 * k + r.lane] * x[j];
+    }
+    x[r.row] = HAS_DIAG ? s / r.piv : s;
+}
+
+template <bool HAS_DIAG>
+__global__ void __launch_bounds__(BL_THREADS) sptrsv_blocklocal_sell(int n_levels, const int *__restrict__ sstart,
+                                                                     const int *__restrict__ cnt,
+                                                                     const int *__restrict__ order,
+                                                                     const int *__restrict__ goff, int uw,
+                                                                     const int *__restrict__ scol,
+                                                                     const double *__restrict__ sval,
+                                                                     const double *__restrict__ sdiag,
+                                                                     const double *__restrict__ b, double *x) {
+    const int *st = sstart + (long long)blockIdx.x * n_levels;
+    const int *ct = cnt + (long long)blockIdx.x * n_levels;
+    const int tid = threadIdx.x;
+    // prologue: row ids of levels 0 and 1, operands of level 0
+    int c_cur = n_levels > 0 ? ct[0] : 0, c_n = n_levels > 1 ? ct[1] : 0;
+    int s_cur = n_levels > 0 ? st[0] : 0, s_n = n_levels > 1 ? st[1] : 0;
+    int row0 = tid < c_cur ? order[s_cur + tid] : -1;
+    int row_n = tid < c_n ? order[s_n + tid] : -1;
+    BsRow cur, nxt;
+    bs_load<HAS_DIAG>(nxt, row0, tid < c_cur, s_cur + tid, goff, uw, scol, sval, sdiag, b);
+    for (int l = 0; l < n_levels; ++l) {
+        cur = nxt;
+        const int c = c_cur, s0 = s_cur;
+        // stage A: row ids of level l+2;  stage B: operands of level l+1
+        int c_nn = 0, s_nn = 0, row_nn = -1;
+        if (l + 2 < n_levels) {
+            c_nn = ct[l + 2];
+            s_nn = st[l + 2];
+            if (tid < c_nn) row_nn = order[s_nn + tid];
+        }
+        if (l + 1 < n_levels) bs_load<HAS_DIAG>(nxt, row_n, tid < c_n, s_n + tid, goff, uw, scol, sval, sdiag, b);
+        bs_finish<HAS_DIAG>(cur, scol, sval, x);
+        for (int t = tid + BL_THREADS; t < c; t += BL_THREADS) {  // levels wider than the CTA
+            BsRow extra;
+            bs_load<HAS_DIAG>(extra, order[s0 + t], true, s0 + t, goff, uw, scol, sval, sdiag, b);
+            bs_finish<HAS_DIAG>(extra, scol, sval, x);
+        }
+        __syncthreads();
+        c_cur = c_n; s_cur = s_n;
+        c_n = c_nn; s_n = s_nn; row_n = row_nn;
+    }
+}
+
 template <typename K>
 static int coop_grid(K kernel, int threads, int blocks_per_sm_cap, long long work_items) {
     int occ = 0;
@@ -547,5 +762,51 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
     }
     if (sdiag) DDILU_CHECK(cudaLaunchCooperativeKernel((void *)sptrsv_sell<true>, grid, SELL_THREADS, args, 0, st));
     else DDILU_CHECK(cudaLaunchCooperativeKernel((void *)sptrsv_sell<false>, grid, SELL_THREADS, args, 0, st));
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_blocklocal_table(int n, int n_blocks, const int *seg_ptr, int n_levels, const int *lev,
+                                      const int *level_rows, int *start, int *cnt, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0 || n_blocks <= 0 || n_levels <= 0) return DDILU_OK;
+    size_t slots = (size_t)n_blocks * n_levels;
+    DDILU_CHECK(cudaMemsetAsync(start, 0x7F, sizeof(int) * slots, st));
+    DDILU_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * slots, st));
+    blocklocal_table<<<stream_grid(n, 256), 256, 0, st>>>(n, n_blocks, seg_ptr, n_levels, lev, level_rows, start, cnt);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *start, const int *cnt,
+                                       const int *level_rows, const int *row_ptr, const int *col_idx,
+                                       const double *values, const double *b, double *x, int upper, int unit_diag,
+                                       int *err, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_blocks <= 0 || n_levels <= 0) return DDILU_OK;
+    if (x == b) return DDILU_ERR_ARG;
+    if (upper)
+        sptrsv_blocklocal<true><<<n_blocks, BL_THREADS, 0, st>>>(n_levels, start, cnt, level_rows, row_ptr, col_idx,
+                                                                values, b, x, unit_diag, err);
+    else
+        sptrsv_blocklocal<false><<<n_blocks, BL_THREADS, 0, st>>>(n_levels, start, cnt, level_rows, row_ptr, col_idx,
+                                                                 values, b, x, unit_diag, err);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt,
+                                            const int *order, const int *goff, int uniform_width, const int *scol,
+                                            const double *sval, const double *sdiag, const double *b, double *x,
+                                            void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_blocks <= 0 || n_levels <= 0) return DDILU_OK;
+    if (x == b) return DDILU_ERR_ARG;
+    if (sdiag)
+        sptrsv_blocklocal_sell<true><<<n_blocks, BL_THREADS, 0, st>>>(n_levels, sstart, cnt, order, goff, uniform_width,
+                                                                     scol, sval, sdiag, b, x);
+    else
+        sptrsv_blocklocal_sell<false><<<n_blocks, BL_THREADS, 0, st>>>(n_levels, sstart, cnt, order, goff,
+                                                                      uniform_width, scol, sval, sdiag, b, x);
+    DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -133,7 +133,17 @@ class Schedule:
     level_ptr: torch.Tensor    # n_levels + 1
     level_rows: torch.Tensor   # rows sorted by (level, index); index descending for U
     lev: torch.Tensor
+    slot_ptr: torch.Tensor = None   # n_levels + 1 padded level starts
     sell: dict = None          # unit_diag -> Sell (schedule-ordered sliced-ELL copy of the factor)
+    blocks: "BlockLocal" = None  # set for small, deep, block-diagonal factors
+
+
+@dataclass
+class BlockLocal:
+    n_blocks: int
+    start: torch.Tensor        # [n_blocks * n_levels] first position of block d / level l in level_rows
+    cnt: torch.Tensor
+    sstart: torch.Tensor       # the same as schedule slots (levels padded to 32)
 
 
 @dataclass
@@ -162,7 +172,7 @@ def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
     order = empty_i32(n + 32 * n_levels)
     call("ddilu_schedule_build", n, lev, n_levels, int(upper), keys, rows, ka, ra, tmp, level_ptr, slot_ptr, order)
     n_slots = int(slot_ptr[-1].item())
-    return Schedule(n, n_levels, n_slots, order[:n_slots], level_ptr, rows, lev)
+    return Schedule(n, n_levels, n_slots, order[:n_slots], level_ptr, rows, lev, slot_ptr)
 
 
 class TriSolveError(ZeroDivisionError):
@@ -171,6 +181,7 @@ class TriSolveError(ZeroDivisionError):
 
 USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)
 UNIFORM_SELL = True
+USE_BLOCK_LOCAL = False   # "sell" | "csr": CTA-per-block sweeps (measured slower: 0.77 us/level floor)
 
 
 def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> Sell:
@@ -192,6 +203,26 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
     scol, sval = empty_i32(max(1, total)), empty_f64(max(1, total))
     call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), gw, 0, scol, sval)
     return Sell(gw, 0, scol, sval, sdiag, int(bad.item()))
+
+
+BLOCK_LOCAL_MAX_WIDTH = 1024   # average rows per level per block up to which the CTA-per-block sweep is used
+
+
+def enable_block_local(sched: Schedule, seg_ptr) -> bool:
+    """Use the CTA-per-block sweep for this factor if its independent row blocks
+    (seg_ptr, host ints) have narrow levels; returns whether it was enabled."""
+    nb = len(seg_ptr) - 1
+    if sched.n == 0 or nb < 1 or sched.n_levels == 0:
+        return False
+    if sched.n / (nb * sched.n_levels) > BLOCK_LOCAL_MAX_WIDTH:
+        return False
+    seg = torch.tensor([int(v) for v in seg_ptr], dtype=I32, device=dev())
+    start, cnt = empty_i32(nb * sched.n_levels), empty_i32(nb * sched.n_levels)
+    call("ddilu_blocklocal_table", sched.n, nb, seg, sched.n_levels, sched.lev, sched.level_rows, start, cnt)
+    L = sched.n_levels
+    sstart = (start.view(nb, L) - sched.level_ptr[:L].view(1, L) + sched.slot_ptr[:L].view(1, L)).contiguous().view(-1)
+    sched.blocks = BlockLocal(nb, start, cnt, sstart)
+    return True
 
 
 def get_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> Sell:
@@ -218,6 +249,24 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
     """out = T^-1 b with the sync-free kernel; `check` reads the error flag back
     (a host sync) and raises like the reference does (sparse.py:414-415)."""
     if t.n_rows == 0:
+        return out
+    if sched.blocks is not None and USE_BLOCK_LOCAL == "sell":
+        bl = sched.blocks
+        sell = get_sell(t, sched, upper, unit_diag)
+        if check and sell.bad_row != INT_MAX:
+            raise TriSolveError(f"zero or missing diagonal at row {sell.bad_row}")
+        call("ddilu_sptrsv_blocklocal_sell", bl.n_blocks, sched.n_levels, bl.sstart, bl.cnt, sched.order, sell.goff,
+             sell.width, sell.scol, sell.sval, sell.sdiag, b, out)
+        return out
+    if sched.blocks is not None and USE_BLOCK_LOCAL == "csr":
+        bl = sched.blocks
+        call("ddilu_sptrsv_blocklocal", bl.n_blocks, sched.n_levels, bl.start, bl.cnt, sched.level_rows, t.rp, t.ci,
+             t.val, b, out, int(upper), int(unit_diag), _err())
+        if check:
+            bad = int(_err().item())
+            if bad != INT_MAX:
+                _err().fill_(INT_MAX)
+                raise TriSolveError(f"zero or missing diagonal at row {bad}")
         return out
     if USE_SELL:
         sell = get_sell(t, sched, upper, unit_diag)

@@ -98,8 +98,12 @@ class DevFactors:
             self._su = D.build_schedule(self.upper, True)
         return self._su
 
-    def prepare(self):
-        # build both schedules and their solve layouts now, inside setup
+    def prepare(self, seg_ptr=None):
+        """Build both schedules and their solve layouts now (inside setup).  seg_ptr:
+        row ranges of independent diagonal blocks (one per subdomain), if known."""
+        local = False
+        if seg_ptr is not None:
+            local = D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
         D.get_sell(self.lower, self.sched_l, False, True)
         D.get_sell(self.upper, self.sched_u, True, False)
         if self._tmp is None:

@@ -309,7 +309,7 @@ class SchurIluPrecond(_DDPrecond):
         self.rule, self.inner_iters = rule, inner_iters
         self._p = d_partial_ilu(s.a_dom, s.n_int, rule, schur_drop_tol=schur_drop_tol, factor_schur=True)
         self._p.interior.prepare()
-        self._p.schur.prepare()
+        self._p.schur.prepare(seg_ptr=s.ext_ptr)       # interface factors: one independent block per subdomain
         self._coupling = s.coupling()
         ne, nh = s.n_ext, s.n_halo
         self._inner = InnerGmres(ne, inner_iters, s.comm, pad=nh)
@@ -418,7 +418,7 @@ class RapIluPrecond(_DDPrecond):
         l_b, u_b, w, z, l_s, u_s = d_carve(coarse, s.n_int)
         self._interior = DevFactors(l_b, u_b).prepare()
         self._w, self._zt = w, z
-        self._schur = DevFactors(l_s, u_s).prepare()
+        self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr)
         self._coarse_kind = coarse
         ni, ne, nh = s.n_int, s.n_ext, s.n_halo
         self._inner = InnerGmres(ne, inner_iters, s.comm)

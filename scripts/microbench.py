@@ -101,11 +101,16 @@ def main():
         rs, ts_ = torch.randn(ne, dtype=torch.float64, device="cuda"), torch.empty(ne, dtype=torch.float64, device="cuda")
         query("ddilu_set_tuning", b"trsv_pipe", 0)
         query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
-        for w in ((0, 4, 8, 16, 24, 32, 64) if args.sweep else (24,)):
-            query("ddilu_set_tuning", b"trsv_depth", w)
+        for mode in ("sell", "csr", "syncfree"):
+            D.USE_BLOCK_LOCAL = mode if mode != "syncfree" else False
             tl, _ = timed(lambda: sf.lower_solve(rs, ts_), flush=flush)
-            emit(what="schur_lower", warps_per_sm=w, rows=ne, levels=sf.sched_l.n_levels, s=tl,
-                 hop_us=tl / sf.sched_l.n_levels * 1e6)
+            tu, _ = timed(lambda: sf.upper_solve(rs, ts_), flush=flush)
+            tlw, _ = timed(lambda: sf.lower_solve(rs, ts_), flush=None)
+            tuw, _ = timed(lambda: sf.upper_solve(rs, ts_), flush=None)
+            emit(what="schur_solve", mode=mode, rows=ne, levels=sf.sched_l.n_levels, lower_s=tl, upper_s=tu,
+                 hop_us_lower=tl / sf.sched_l.n_levels * 1e6, hop_us_upper=tu / sf.sched_u.n_levels * 1e6,
+                 warm_hop_us_lower=tlw / sf.sched_l.n_levels * 1e6, warm_hop_us_upper=tuw / sf.sched_u.n_levels * 1e6)
+        D.USE_BLOCK_LOCAL = False
         del ms
     query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
     query("ddilu_set_tuning", b"trsv_depth", 24)

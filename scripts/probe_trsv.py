@@ -45,10 +45,17 @@ for name, n, offs in cases:
     b = torch.rand(n, dtype=torch.float64, device="cuda")
     out = torch.empty_like(b)
     res = {}
-    for label, use_sell, pipe, w in (("sell3", True, 0, 3), ("sell1", True, 0, 1), ("pipe8", True, 1, 8), ("pipe32", True, 1, 32)):
-        D.USE_SELL = use_sell
-        query("ddilu_set_tuning", b"trsv_pipe", pipe)
-        query("ddilu_set_tuning", b"trsv_pipe_warps_per_sm" if pipe else b"trsv_blocks_per_sm", w)
+    D.USE_BLOCK_LOCAL = False
+    for label, depth in (("syncfree", 24), ("syncfree_d0", 0)):
+        query("ddilu_set_tuning", b"trsv_depth", depth)
         t = timed(lambda: D.sptrsv(ld, sched, b, out, False, True))
         res[label] = round(t / sched.n_levels * 1e6, 3)
+    query("ddilu_set_tuning", b"trsv_depth", 24)
+    if sched.n / sched.n_levels <= 1024:
+        D.enable_block_local(sched, [0, n])
+        for mode in ("sell", "csr"):
+            D.USE_BLOCK_LOCAL = mode
+            t = timed(lambda: D.sptrsv(ld, sched, b, out, False, True))
+            res["block_" + mode] = round(t / sched.n_levels * 1e6, 3)
+        sched.blocks = None
     print(json.dumps({"case": name, "n": n, "levels": sched.n_levels, "us_per_level": res}))
