@@ -63,15 +63,18 @@ int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row_ptr, const
  * entry k of lane l at goff[g] + 32*k + l (col -1 = padding); sdiag[slot] = pivot.
  * goff == NULL selects the uniform layout: every group has `uniform_width` entries
  * per lane at g * 32 * uniform_width (no descriptor load on the dependency chain).
+ * gwait[g] (optional; pos_work = n scratch ints) = the dependency of group g that is latest
+ * in the schedule: the warp spins on that one address before checking the others.
  * ddilu_sptrsv_sell is the production solve (same semantics as ddilu_sptrsv;
  * sdiag == NULL means unit diagonal). */
 int ddilu_sell_width(int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
-                     int upper, int unit_diag, int *gw32, double *sdiag, int *bad_row, void *stream);
+                     int upper, int unit_diag, int *gw32, double *sdiag, int *bad_row, int *pos_work, int *gwait,
+                     void *stream);
 int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
                     int upper, const int *goff, int uniform_width, int *scol, double *sval, void *stream);
 int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff, int uniform_width,
-                      const int *scol, const double *sval, const double *sdiag, const double *b, double *x,
-                      void *stream);
+                      const int *scol, const double *sval, const double *sdiag, const int *gwait, const double *b,
+                      double *x, void *stream);
 
 /* Block-local variant for small, deep, block-diagonal factors (interface factors L_S/U_S:
  * precond.py:239-245 `_schur_solve`, :361-366 `_coarse_precond`): one CTA per independent row

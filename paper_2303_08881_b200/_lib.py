@@ -31,9 +31,9 @@ SIGNATURES = {
     "ddilu_levels": (_I, [_I, _P, _P, _I, _P, _P, _P]),
     "ddilu_schedule_build": (_I, [_I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
-    "ddilu_sell_width": (_I, [_I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "ddilu_sell_width": (_I, [_I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sell_fill": (_I, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
-    "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),

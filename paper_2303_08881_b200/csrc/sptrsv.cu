@@ -199,9 +199,18 @@ __global__ void sched_place(int n, const int *__restrict__ keys, const int *__re
 // longest row of the group; the diagonal (U, or a non-unit L) is kept per slot.
 // Every load of the solve is then a coalesced 128/256-byte access and the chain
 // of dependent loads is descriptor -> (cols, vals, row id) -> x.
+__global__ void sched_positions(int n_slots, const int *__restrict__ order, int *__restrict__ pos) {
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots; s += (long long)gridDim.x * blockDim.x)
+        if (order[s] >= 0) pos[order[s]] = (int)s;
+}
+
+// gwait[g] = the dependency of group g that sits LATEST in the schedule (-1 if the
+// group has none): the warp spins on that single address before it checks the rest,
+// so a waiting warp costs one 32-byte L2 sector per poll instead of ~30.
 __global__ void sell_width(int n_groups, const int *__restrict__ order, const int *__restrict__ rp,
                            const int *__restrict__ ci, const double *__restrict__ val, int upper, int unit_diag,
-                           int *__restrict__ gw32, double *__restrict__ sdiag, int *bad_row) {
+                           int *__restrict__ gw32, double *__restrict__ sdiag, int *bad_row,
+                           const int *__restrict__ pos, int *__restrict__ gwait) {
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -210,11 +219,17 @@ __global__ void sell_width(int n_groups, const int *__restrict__ order, const in
         int deps = 0;
         double d = 1.0;
         bool seen = false;
+        long long last = -1;  // (schedule position << 32) | column of the latest dependency
         if (row >= 0) {
             for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
                 const int j = ci[k];
-                if (upper ? j > row : j < row) ++deps;
-                else if (j == row) {
+                if (upper ? j > row : j < row) {
+                    ++deps;
+                    if (pos) {
+                        const long long key = ((long long)pos[j] << 32) | (unsigned)j;
+                        last = key > last ? key : last;
+                    }
+                } else if (j == row) {
                     d = val[k];
                     seen = true;
                 }
@@ -224,6 +239,13 @@ __global__ void sell_width(int n_groups, const int *__restrict__ order, const in
         if (sdiag) sdiag[g * 32 + lane] = unit_diag ? 1.0 : d;
         const int w = __reduce_max_sync(0xffffffffu, deps);
         if (lane == 0) gw32[g] = w * 32;
+        if (gwait) {
+            for (int o = 16; o > 0; o >>= 1) {
+                const long long other = __shfl_xor_sync(0xffffffffu, last, o);
+                last = other > last ? other : last;
+            }
+            if (lane == 0) gwait[g] = last < 0 ? -1 : (int)(last & 0xffffffffLL);
+        }
     }
 }
 
@@ -284,6 +306,7 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
                                                             const int *__restrict__ scol,
                                                             const double *__restrict__ sval,
                                                             const double *__restrict__ sdiag,
+                                                            const int *__restrict__ gwait,
                                                             const double *__restrict__ b, double *x) {
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -293,8 +316,13 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
         const long long off = goff ? goff[g] : g * 32LL * uw;
         const int w = goff ? (goff[g + 1] - (int)off) >> 5 : uw;
         const int row = order[g * 32 + lane];
+        const int wait_col = gwait ? gwait[g] : -1;
         double s = row >= 0 ? b[row] : 0.0;
         const double d = HAS_DIAG ? sdiag[g * 32 + lane] : 1.0;
+        // spin on the group's latest dependency only: one sector per poll for the whole warp
+        if (wait_col >= 0)
+            while (is_sentinel(ld_l2(x + wait_col))) {
+            }
         for (int k0 = 0; k0 < w; k0 += SELL_CHUNK) {
             int c[SELL_CHUNK];
             double a[SELL_CHUNK], xv[SELL_CHUNK];
@@ -705,12 +733,16 @@ extern "C" int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row
 
 extern "C" int ddilu_sell_width(int n_slots, const int *order, const int *row_ptr, const int *col_idx,
                                 const double *values, int upper, int unit_diag, int *gw32, double *sdiag,
-                                int *bad_row, void *stream) {
+                                int *bad_row, int *pos_work, int *gwait, void *stream) {
     if (n_slots <= 0) return DDILU_OK;
     if (n_slots & 31) return DDILU_ERR_ARG;
+    if (gwait && !pos_work) return DDILU_ERR_ARG;
     const int n_groups = n_slots >> 5;
+    if (gwait)
+        sched_positions<<<stream_grid(n_slots, 256), 256, 0, (cudaStream_t)stream>>>(n_slots, order, pos_work);
     sell_width<<<stream_grid((long long)n_groups * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        n_groups, order, row_ptr, col_idx, values, upper, unit_diag, gw32, sdiag, bad_row);
+        n_groups, order, row_ptr, col_idx, values, upper, unit_diag, gw32, sdiag, bad_row, gwait ? pos_work : nullptr,
+        gwait);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
@@ -728,14 +760,15 @@ extern "C" int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr
 
 extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff,
                                  int uniform_width, const int *scol, const double *sval, const double *sdiag,
-                                 const double *b, double *x, void *stream) {
+                                 const int *gwait, const double *b, double *x, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) return DDILU_OK;
     if (x == b || (n_slots & 31)) return DDILU_ERR_ARG;
     DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
     int n_groups = n_slots >> 5;
-    void *args[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &b, &x};
+    void *args[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &gwait, &b, &x};
     if (g_trsv.pipe) {
+        void *pargs[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &b, &x};
         // few resident warps: pipe_warps_per_sm warps on every SM, 4 warps per CTA
         int ctas_per_sm = (g_trsv.pipe_warps_per_sm + 3) / 4;
         if (ctas_per_sm < 1) ctas_per_sm = 1;
@@ -748,7 +781,7 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
         long long grid = (long long)ctas_per_sm * device_info().sm_count;
         long long need = ((long long)n_groups + 3) / 4;
         if (grid > need) grid = need;
-        DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, 128, args, 0, st));
+        DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, 128, pargs, 0, st));
         return DDILU_OK;
     }
     int grid = sdiag ? coop_grid(sptrsv_sell<true>, SELL_THREADS, g_trsv.blocks_per_sm, n_slots)

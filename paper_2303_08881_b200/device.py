@@ -154,6 +154,7 @@ class Sell:
     sval: torch.Tensor
     sdiag: torch.Tensor | None
     bad_row: int               # first row with a zero / missing diagonal, or INT_MAX
+    gwait: torch.Tensor | None = None   # per group: the dependency that is latest in the schedule
 
 
 def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
@@ -181,6 +182,7 @@ class TriSolveError(ZeroDivisionError):
 
 USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)
 UNIFORM_SELL = True
+USE_GWAIT = True
 USE_BLOCK_LOCAL = False   # "sell" | "csr": CTA-per-block sweeps (measured slower: 0.77 us/level floor)
 
 
@@ -189,8 +191,10 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
     gw = zeros_i32(n_groups + 1)
     sdiag = None if unit_diag else empty_f64(max(1, sched.n_slots))
     bad = torch.full((1,), INT_MAX, dtype=I32, device=dev())
+    gwait = empty_i32(max(1, n_groups)) if USE_GWAIT else None
+    pos = empty_i32(max(1, t.n_rows)) if USE_GWAIT else None
     call("ddilu_sell_width", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), int(unit_diag), gw, sdiag,
-         bad)
+         bad, pos, gwait)
     wmax = int(gw[:n_groups].max().item()) // 32 if n_groups else 0
     exclusive_scan_(gw, n_groups)
     total = int(gw[-1].item())
@@ -199,10 +203,10 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
         # short, regular rows (stencils): pad every group to the widest one and drop the descriptor array
         scol, sval = empty_i32(max(1, uniform)), empty_f64(max(1, uniform))
         call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), None, wmax, scol, sval)
-        return Sell(None, wmax, scol, sval, sdiag, int(bad.item()))
+        return Sell(None, wmax, scol, sval, sdiag, int(bad.item()), gwait)
     scol, sval = empty_i32(max(1, total)), empty_f64(max(1, total))
     call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), gw, 0, scol, sval)
-    return Sell(gw, 0, scol, sval, sdiag, int(bad.item()))
+    return Sell(gw, 0, scol, sval, sdiag, int(bad.item()), gwait)
 
 
 BLOCK_LOCAL_MAX_WIDTH = 1024   # average rows per level per block up to which the CTA-per-block sweep is used
@@ -273,7 +277,7 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
         if check and sell.bad_row != INT_MAX:
             raise TriSolveError(f"zero or missing diagonal at row {sell.bad_row}")
         call("ddilu_sptrsv_sell", t.n_rows, sched.n_slots, sched.n_levels, sched.order, sell.goff, sell.width,
-             sell.scol, sell.sval, sell.sdiag, b, out)
+             sell.scol, sell.sval, sell.sdiag, sell.gwait if USE_GWAIT else None, b, out)
         return out
     call("ddilu_sptrsv", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
          int(unit_diag), _err())

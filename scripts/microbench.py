@@ -78,22 +78,24 @@ def main():
     ubytes = 12 * nu + 4 * (n + 1) + 16 * n
     emit(what="factors", rows=n, nnz_l=nl, nnz_u=nu, levels_l=f.sched_l.n_levels, levels_u=f.sched_u.n_levels,
          slots_l=f.sched_l.n_slots)
-    configs = [(3, 0, True, 0)]
+    configs = [(3, 0, True, 0, True)]
     if args.sweep:
-        configs = [(b, 0, True, 0) for b in (2, 3, 4)]
-    for bps, sleep, use_sell, pipe in configs:
+        configs = [(b, 0, True, 0, True) for b in (2, 3, 4, 5, 8)] + [(3, 0, True, 0, False)]
+    for bps, sleep, use_sell, pipe, gwait in configs:
         D.USE_SELL = use_sell
+        D.USE_GWAIT = gwait
         query("ddilu_set_tuning", b"trsv_pipe", pipe)
         query("ddilu_set_tuning", b"trsv_pipe_warps_per_sm" if pipe else b"trsv_blocks_per_sm", bps)
         tl, tlmin = timed(lambda: f.lower_solve(r, t), flush=flush)
         tu, tumin = timed(lambda: f.upper_solve(t, z), flush=flush)
-        emit(what="sptrsv", kernel=("pipe" if pipe else "sell") if use_sell else "csr", blocks_per_sm=bps, sleep_ns=sleep, lower_s=tl, upper_s=tu, lower_min_s=tlmin,
+        emit(what="sptrsv", kernel=("pipe" if pipe else ("sellw" if gwait else "sell")) if use_sell else "csr", blocks_per_sm=bps, sleep_ns=sleep, lower_s=tl, upper_s=tu, lower_min_s=tlmin,
              upper_min_s=tumin, lower_gbs=lbytes / tl / 1e9, upper_gbs=ubytes / tu / 1e9,
              lower_frac=lbytes / tl / 1e9 / PEAK, upper_frac=ubytes / tu / 1e9 / PEAK,
              hop_us_lower=tl / f.sched_l.n_levels * 1e6, hop_us_upper=tu / f.sched_u.n_levels * 1e6)
     query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
     query("ddilu_set_tuning", b"trsv_pipe", 0)
     D.USE_SELL = True
+    D.USE_GWAIT = True
     if args.p > 1:   # the small, deep interface solves of the two-level preconditioners
         ms = P.schur_setup(a, layout)
         sf = ms._p.schur

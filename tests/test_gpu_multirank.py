@@ -1,0 +1,85 @@
+"""Two ranks sharing one GPU (gloo, tensors staged through the host): the whole
+multi-rank path -- subdomain blocks per rank, halo plan, halo exchange inside
+SpMV and the interface matvec, allreduced dots -- must reproduce the
+single-rank solve (same p, so the same preconditioner: strong-scaling invariant)."""
+
+import json
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("bj", 4), ("schur", 8), ("rap", 4), ("rap-milu", 8)]
+DIMS = (20, 18, 16)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _solve_all(P):
+    out = {}
+    a = P.aniso3d(*DIMS)
+    b = P.default_rhs(a) if False else None
+    for pc, p in CASES:
+        a = P.aniso3d(*DIMS)
+        layout = P.classify_and_order(a, P.partition(a, p, DIMS), p)
+        m = P.make_preconditioner(pc, a, layout)
+        import torch
+        from paper_2303_08881_b200 import device as D
+        ones = torch.ones(a.n_cols, dtype=torch.float64, device="cuda")
+        bd = torch.empty(a.n_rows, dtype=torch.float64, device="cuda")
+        D.spmv(a.device(), ones, bd)
+        rhs = bd.cpu().numpy()
+        x, rep = P.fgmres(a, rhs, m=m.apply)
+        r = np.random.default_rng(3).standard_normal(a.n_rows)
+        z = m.apply(r)
+        out[f"{pc}|{p}"] = {"its": rep.iterations, "relres": rep.final_relres, "x": x.tolist(), "z": z.tolist(),
+                            "n_halo": int(m.system.n_halo), "n_loc": int(m.system.n_loc)}
+    return out
+
+
+def _worker(rank, world, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK="0")
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_2303_08881_b200 as P
+    from paper_2303_08881_b200 import dist
+    comm = dist.init_from_env(backend="gloo")
+    assert comm.size == world and comm.rank == rank
+    res = _solve_all(P)
+    with open(f"{path}.{rank}", "w") as fh:
+        json.dump(res, fh)
+    import torch.distributed as tdist
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_two_ranks_match_single_rank(tmp_path):
+    import paper_2303_08881_b200 as P
+    single = _solve_all(P)
+    world, port, path = 2, _free_port(), str(tmp_path / "res")
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, path)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    for rank in range(world):
+        multi = json.load(open(f"{path}.{rank}"))
+        for key, ref in single.items():
+            got = multi[key]
+            assert got["n_halo"] > 0 and got["n_loc"] < ref["n_loc"], key      # really distributed
+            assert abs(got["its"] - ref["its"]) <= 1, (key, got["its"], ref["its"])
+            assert got["relres"] <= 1e-8
+            assert np.max(np.abs(np.array(got["x"]) - np.array(ref["x"]))) < 1e-6, key
+            scale = np.max(np.abs(ref["z"]))
+            assert np.max(np.abs(np.array(got["z"]) - np.array(ref["z"]))) < 1e-9 * scale, key
