@@ -24,7 +24,7 @@ extern "C" {
 #endif
 
 /* ---- tuning knobs (no reference equivalent): "trsv_blocks_per_sm", "trsv_depth",
- * "trsv_pipe", "trsv_pipe_warps_per_sm", "trsv_sleep_ns" */
+ * "trsv_stage_mask", "trsv_far_sleep_ns", "trsv_pipe", "trsv_pipe_warps_per_sm", "trsv_sleep_ns" */
 int ddilu_set_tuning(const char *key, int value);
 
 /* ---- primitives used by the count -> scan -> fill setup passes (the reference
@@ -72,9 +72,13 @@ int ddilu_sell_width(int n_slots, const int *order, const int *row_ptr, const in
                      void *stream);
 int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
                     int upper, const int *goff, int uniform_width, int *scol, double *sval, void *stream);
+/* out[g] = gwait[group of prev[g]]: the same kind of indicator one level further back */
+int ddilu_compose_wait(int n_groups, const int *gwait, const int *pos, const int *prev, int *out, void *stream);
+/* gwait / gfar1 / gfar2 (each optional): single addresses 1 / 2 / 3 levels back a warp waits on before
+ * it polls its own dependencies ("trsv_stage_mask" selects which are used) */
 int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff, int uniform_width,
-                      const int *scol, const double *sval, const double *sdiag, const int *gwait, const double *b,
-                      double *x, void *stream);
+                      const int *scol, const double *sval, const double *sdiag, const int *gwait, const int *gfar1,
+                      const int *gfar2, const double *b, double *x, void *stream);
 
 /* Block-local variant for small, deep, block-diagonal factors (interface factors L_S/U_S:
  * precond.py:239-245 `_schur_solve`, :361-366 `_coarse_precond`): one CTA per independent row
@@ -90,6 +94,12 @@ int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *start, const 
 int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *order,
                                  const int *goff, int uniform_width, const int *scol, const double *sval,
                                  const double *sdiag, const double *b, double *x, void *stream);
+
+/* diagnostics: same solve with per-group timestamps (8 int64 per group: start, spin done, deps
+ * loaded, stored [globaltimer ns], SM id, spin count, re-poll rounds, warp id) */
+int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *order, const int *goff,
+                            int uniform_width, const int *scol, const double *sval, const double *sdiag,
+                            const int *gwait, const double *b, double *x, long long *stamps, void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,

@@ -34,6 +34,10 @@ struct TrsvTuning {
     unsigned sleep_ns = 0;
     int pipe = 0;            // 1: software-pipelined SELL kernel, 0: plain SELL kernel
     int pipe_warps_per_sm = 8;
+    int stage_mask = -1;     // -1: by level width (measured: narrow levels -> 3, wide levels -> 4)
+                             // bit0: far stage (sleep-poll 3 levels back), bit1: mid stage (spin 2 levels
+                             // back), bit2: near stage (spin on the group's own latest dependency)
+    int far_sleep_ns = 400;
     int depth = 24;          // resident warps ~ depth x (groups per level): enough lookahead to hide the
                              // startup loads of a group, few enough pollers not to slow the producers
 };
@@ -204,6 +208,15 @@ __global__ void sched_positions(int n_slots, const int *__restrict__ order, int 
         if (order[s] >= 0) pos[order[s]] = (int)s;
 }
 
+// out[g] = gwait of the group that produces gwait[g]: an indicator one level further back
+__global__ void compose_wait(int n_groups, const int *__restrict__ gwait, const int *__restrict__ pos,
+                             const int *__restrict__ prev, int *__restrict__ out) {
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n_groups; g += (long long)gridDim.x * blockDim.x) {
+        const int c = prev[g];
+        out[g] = c >= 0 ? gwait[pos[c] >> 5] : -1;
+    }
+}
+
 // gwait[g] = the dependency of group g that sits LATEST in the schedule (-1 if the
 // group has none): the warp spins on that single address before it checks the rest,
 // so a waiting warp costs one 32-byte L2 sector per poll instead of ~30.
@@ -307,6 +320,8 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
                                                             const double *__restrict__ sval,
                                                             const double *__restrict__ sdiag,
                                                             const int *__restrict__ gwait,
+                                                            const int *__restrict__ gfar1,
+                                                            const int *__restrict__ gfar2, unsigned far_sleep_ns,
                                                             const double *__restrict__ b, double *x) {
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -317,9 +332,19 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
         const int w = goff ? (goff[g + 1] - (int)off) >> 5 : uw;
         const int row = order[g * 32 + lane];
         const int wait_col = gwait ? gwait[g] : -1;
+        const int far1 = gfar1 ? gfar1[g] : -1, far2 = gfar2 ? gfar2[g] : -1;
         double s = row >= 0 ? b[row] : 0.0;
         const double d = HAS_DIAG ? sdiag[g * 32 + lane] : 1.0;
-        // spin on the group's latest dependency only: one sector per poll for the whole warp
+        // staged waiting: every stage polls ONE address (one 32-byte sector for the whole warp)
+        //   far  (an indicator 3 levels back not yet written): sleep between polls, latency is irrelevant here
+        //   mid  (2 levels back): tight single-sector spin
+        //   near (optional, the group's own latest dependency): tight single-sector spin
+        // afterwards the real dependencies are polled directly.
+        if (far2 >= 0)
+            while (is_sentinel(ld_l2(x + far2))) __nanosleep(far_sleep_ns);
+        if (far1 >= 0)
+            while (is_sentinel(ld_l2(x + far1))) {
+            }
         if (wait_col >= 0)
             while (is_sentinel(ld_l2(x + wait_col))) {
             }
@@ -671,6 +696,8 @@ extern "C" int ddilu_set_tuning(const char *key, int value) {
     else if (!strcmp(key, "trsv_sleep_ns")) g_trsv.sleep_ns = (unsigned)value;
     else if (!strcmp(key, "trsv_pipe")) g_trsv.pipe = value;
     else if (!strcmp(key, "trsv_depth")) g_trsv.depth = value;
+    else if (!strcmp(key, "trsv_stage_mask")) g_trsv.stage_mask = value;
+    else if (!strcmp(key, "trsv_far_sleep_ns")) g_trsv.far_sleep_ns = value;
     else if (!strcmp(key, "trsv_pipe_warps_per_sm")) g_trsv.pipe_warps_per_sm = value;
     else return DDILU_ERR_ARG;
     return DDILU_OK;
@@ -758,15 +785,30 @@ extern "C" int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr
     return DDILU_OK;
 }
 
+extern "C" int ddilu_compose_wait(int n_groups, const int *gwait, const int *pos, const int *prev, int *out,
+                                  void *stream) {
+    if (n_groups <= 0) return DDILU_OK;
+    compose_wait<<<stream_grid(n_groups, 256), 256, 0, (cudaStream_t)stream>>>(n_groups, gwait, pos, prev, out);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
 extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff,
                                  int uniform_width, const int *scol, const double *sval, const double *sdiag,
-                                 const int *gwait, const double *b, double *x, void *stream) {
+                                 const int *gwait, const int *gfar1, const int *gfar2, const double *b, double *x,
+                                 void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) return DDILU_OK;
     if (x == b || (n_slots & 31)) return DDILU_ERR_ARG;
     DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
     int n_groups = n_slots >> 5;
-    void *args[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &gwait, &b, &x};
+    int mask = g_trsv.stage_mask;
+    if (mask < 0) mask = (n_levels > 0 && n_groups / n_levels >= 256) ? 4 : 3;
+    const int *w0 = (mask & 4) ? gwait : nullptr;
+    const int *w1 = (mask & 2) ? gfar1 : nullptr;
+    const int *w2 = (mask & 1) ? gfar2 : nullptr;
+    unsigned far_sleep = (unsigned)g_trsv.far_sleep_ns;
+    void *args[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &w0, &w1, &w2, &far_sleep, &b, &x};
     if (g_trsv.pipe) {
         void *pargs[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &b, &x};
         // few resident warps: pipe_warps_per_sm warps on every SM, 4 warps per CTA

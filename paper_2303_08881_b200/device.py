@@ -155,6 +155,8 @@ class Sell:
     sdiag: torch.Tensor | None
     bad_row: int               # first row with a zero / missing diagonal, or INT_MAX
     gwait: torch.Tensor | None = None   # per group: the dependency that is latest in the schedule
+    gfar1: torch.Tensor | None = None   # the same indicator one level further back (gwait of gwait's group)
+    gfar2: torch.Tensor | None = None   # two levels further back
 
 
 def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
@@ -195,6 +197,11 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
     pos = empty_i32(max(1, t.n_rows)) if USE_GWAIT else None
     call("ddilu_sell_width", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), int(unit_diag), gw, sdiag,
          bad, pos, gwait)
+    gfar1 = gfar2 = None
+    if USE_GWAIT and n_groups:
+        gfar1, gfar2 = empty_i32(n_groups), empty_i32(n_groups)
+        call("ddilu_compose_wait", n_groups, gwait, pos, gwait, gfar1)
+        call("ddilu_compose_wait", n_groups, gwait, pos, gfar1, gfar2)
     wmax = int(gw[:n_groups].max().item()) // 32 if n_groups else 0
     exclusive_scan_(gw, n_groups)
     total = int(gw[-1].item())
@@ -203,10 +210,10 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
         # short, regular rows (stencils): pad every group to the widest one and drop the descriptor array
         scol, sval = empty_i32(max(1, uniform)), empty_f64(max(1, uniform))
         call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), None, wmax, scol, sval)
-        return Sell(None, wmax, scol, sval, sdiag, int(bad.item()), gwait)
+        return Sell(None, wmax, scol, sval, sdiag, int(bad.item()), gwait, gfar1, gfar2)
     scol, sval = empty_i32(max(1, total)), empty_f64(max(1, total))
     call("ddilu_sell_fill", sched.n_slots, sched.order, t.rp, t.ci, t.val, int(upper), gw, 0, scol, sval)
-    return Sell(gw, 0, scol, sval, sdiag, int(bad.item()), gwait)
+    return Sell(gw, 0, scol, sval, sdiag, int(bad.item()), gwait, gfar1, gfar2)
 
 
 BLOCK_LOCAL_MAX_WIDTH = 1024   # average rows per level per block up to which the CTA-per-block sweep is used
@@ -277,7 +284,8 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
         if check and sell.bad_row != INT_MAX:
             raise TriSolveError(f"zero or missing diagonal at row {sell.bad_row}")
         call("ddilu_sptrsv_sell", t.n_rows, sched.n_slots, sched.n_levels, sched.order, sell.goff, sell.width,
-             sell.scol, sell.sval, sell.sdiag, sell.gwait if USE_GWAIT else None, b, out)
+             sell.scol, sell.sval, sell.sdiag, sell.gwait if USE_GWAIT else None,
+             sell.gfar1 if USE_GWAIT else None, sell.gfar2 if USE_GWAIT else None, b, out)
         return out
     call("ddilu_sptrsv", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
          int(unit_diag), _err())

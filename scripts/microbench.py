@@ -78,12 +78,15 @@ def main():
     ubytes = 12 * nu + 4 * (n + 1) + 16 * n
     emit(what="factors", rows=n, nnz_l=nl, nnz_u=nu, levels_l=f.sched_l.n_levels, levels_u=f.sched_u.n_levels,
          slots_l=f.sched_l.n_slots)
-    configs = [(3, 0, True, 0, True)]
+    configs = [(3, -1, True, 0, True)]
     if args.sweep:
-        configs = [(b, 0, True, 0, True) for b in (2, 3, 4, 5, 8)] + [(3, 0, True, 0, False)]
+        configs = [(3, mk, True, 0, True) for mk in (4, 2, 3, 6, 7, 0)] + [(6, 3, True, 0, True), (3, 1003, True, 0, True)]
     for bps, sleep, use_sell, pipe, gwait in configs:
         D.USE_SELL = use_sell
         D.USE_GWAIT = gwait
+        if sleep >= 0:
+            query("ddilu_set_tuning", b"trsv_stage_mask", sleep % 1000)
+            query("ddilu_set_tuning", b"trsv_far_sleep_ns", 1000 if sleep >= 1000 else 400)
         query("ddilu_set_tuning", b"trsv_pipe", pipe)
         query("ddilu_set_tuning", b"trsv_pipe_warps_per_sm" if pipe else b"trsv_blocks_per_sm", bps)
         tl, tlmin = timed(lambda: f.lower_solve(r, t), flush=flush)
@@ -94,6 +97,8 @@ def main():
              hop_us_lower=tl / f.sched_l.n_levels * 1e6, hop_us_upper=tu / f.sched_u.n_levels * 1e6)
     query("ddilu_set_tuning", b"trsv_blocks_per_sm", 3)
     query("ddilu_set_tuning", b"trsv_pipe", 0)
+    query("ddilu_set_tuning", b"trsv_stage_mask", -1)
+    query("ddilu_set_tuning", b"trsv_far_sleep_ns", 400)
     D.USE_SELL = True
     D.USE_GWAIT = True
     if args.p > 1:   # the small, deep interface solves of the two-level preconditioners
