@@ -322,7 +322,7 @@ def main():
     ap.add_argument("--precond", default="schur", choices=("bj", "schur", "rap", "rap-milu"))
     ap.add_argument("--fill", default="ilu0")
     ap.add_argument("--domains", type=int, default=P_DOMAINS)
-    ap.add_argument("--cpu-sample", type=int, default=64, help="grid size of the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=96, help="grid size of the CPU baseline sample (~10 s of CPU)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -182,6 +182,21 @@ int ddilu_sym_adj_count(int n, const int *rp, const int *ci, int *counts, void *
 int ddilu_sym_adj_fill(int n, const int *rp, const int *ci, const int *out_rp, int *cursor, int *out_ci, void *stream);
 int ddilu_row_lengths(int n, const int *rp, int *out, void *stream);
 
+int ddilu_sort_rows_i32(int n, const int *rp, int *ci, void *stream);
+/* ---- ordering.py:97-127 `_grow_regions` (serial greedy BFS growth; work = 2n ints) */
+int ddilu_grow_regions(int n, const int *adj_rp, const int *adj_ci, int n_dom, const int *sizes, int *owner,
+                       int *work, void *stream);
+/* ---- precond.py:84-125 `_l1_row_shifts`, `_add_to_diagonal` (l1 block Jacobi) */
+int ddilu_l1_row_shifts(int n_sel, const int *rows, const int *rp, const int *ci, const double *v, const int *owner,
+                        double *out, void *stream);
+int ddilu_add_to_diagonal(int n, const int *rp, const int *ci, double *v, const double *shifts, int *missing,
+                          void *stream);
+/* ---- factor.py:806-822 `_drop_small_rows` (schur_drop_tol thinning) */
+int ddilu_drop_small_count(int n, const int *rp, const int *ci, const double *v, double tol, int *counts,
+                           void *stream);
+int ddilu_drop_small_fill(int n, const int *rp, const int *ci, const double *v, double tol, const int *out_rp,
+                          int *out_ci, double *out_v, void *stream);
+
 /* ---- ordering.py:304-397 `_bfs_ecc` + `_rcm_order`: Cuthill-McKee order (not reversed) */
 long long ddilu_cm_work_elems(int n);
 int ddilu_cm_order(int n, const int *adj_rp, const int *adj_ci, int *order, int *work, void *stream);

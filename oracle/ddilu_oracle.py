@@ -742,13 +742,35 @@ def strip_diagonal_blocks(m: Csr, block_of):
     return Csr(m.n_rows, m.n_cols, rp, m.col_idx[keep], m.values[keep])
 
 
+def add_to_diagonal(m: Csr, shifts):
+    """precond.py:105-125 (diagonal present, or nothing to add where it is missing)."""
+    rows = np.repeat(np.arange(m.n_rows), np.diff(m.row_ptr))
+    slots = np.full(m.n_rows, -1, dtype=np.int64)
+    on_diag = np.where(rows == m.col_idx)[0]
+    slots[rows[on_diag]] = on_diag
+    if np.any((slots < 0) & (shifts != 0.0)):
+        raise NotImplementedError("oracle: l1 shift on a structurally missing diagonal")
+    vals = m.values.copy()
+    have = slots >= 0
+    vals[slots[have]] += shifts[have]
+    return Csr(m.n_rows, m.n_cols, m.row_ptr, m.col_idx, vals)
+
+
 class BjPrecond:
     """precond.py:177-214."""
 
-    def __init__(self, a, layout, rule=Rule("ilu0"), use_rcm=True):
+    def __init__(self, a, layout, rule=Rule("ilu0"), use_rcm=True, l1=False):
         self.layout, self.rule = layout, rule
         self.domains = domain_orderings(a, layout, use_rcm)
-        self.factors = [factorize(take_submatrix(a, d.nodes, d.nodes), rule) for d in self.domains]
+        self.factors = []
+        for d, dom in enumerate(self.domains):
+            local = take_submatrix(a, dom.nodes, dom.nodes)
+            if l1:  # precond.py:207-212
+                shifts = np.empty(len(dom.nodes))
+                lib().orc_l1_row_shifts(_p(a.row_ptr), _p(a.col_idx), _p(a.values), _p(layout.owner),
+                                        _I(len(dom.nodes)), _p(_i64(dom.nodes)), _I(d), _p(shifts))
+                local = add_to_diagonal(local, shifts)
+            self.factors.append(factorize(local, rule))
 
     def apply(self, r):
         z = np.empty_like(r)
@@ -869,11 +891,13 @@ class RapPrecond:
 
 
 def make_preconditioner(name, a, layout, rule=Rule("ilu0"), inner_iters=3):
-    """precond.py:450-474 (l1bj is outside the hot path)."""
+    """precond.py:450-474."""
     if name == "none":
         return None
     if name == "bj":
         return BjPrecond(a, layout, rule)
+    if name == "l1bj":
+        return BjPrecond(a, layout, rule, l1=True)
     if name == "schur":
         return SchurPrecond(a, layout, rule, inner_iters=inner_iters)
     if name == "rap":

@@ -67,6 +67,12 @@ SIGNATURES = {
     "ddilu_mark_sends": (_I, [_I, _P, _P, _P, _I, _I, _P, _I, _P, _P]),
     "ddilu_sym_adj_count": (_I, [_I, _P, _P, _P, _P]),
     "ddilu_sym_adj_fill": (_I, [_I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sort_rows_i32": (_I, [_I, _P, _P, _P]),
+    "ddilu_grow_regions": (_I, [_I, _P, _P, _I, _P, _P, _P, _P]),
+    "ddilu_l1_row_shifts": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_add_to_diagonal": (_I, [_I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_drop_small_count": (_I, [_I, _P, _P, _P, _D, _P, _P]),
+    "ddilu_drop_small_fill": (_I, [_I, _P, _P, _P, _D, _P, _P, _P, _P]),
     "ddilu_row_lengths": (_I, [_I, _P, _P, _P]),
     "ddilu_cm_work_elems": (_L, [_I]),
     "ddilu_cm_order": (_I, [_I, _P, _P, _P, _P, _P]),

@@ -4,6 +4,9 @@ factorisation; solve_s is measured inside fgmres."""
 
 from __future__ import annotations
 
+import csv
+import io
+import json
 import time
 from dataclasses import dataclass, field
 
@@ -15,7 +18,7 @@ from .ordering import classify_and_order, partition, row_block_owner
 from .precond import PRECONDITIONER_NAMES, make_preconditioner
 from .problems import ProblemSpec, default_rhs
 
-__all__ = ["RunConfig", "run", "solve_prepared", "COLUMNS"]
+__all__ = ["RunConfig", "run", "sweep", "to_json", "to_csv", "solve_prepared", "COLUMNS", "REPORT_SCHEMA"]
 
 COLUMNS = ("problem", "n", "p", "precond", "fill", "its", "converged", "setup_s", "solve_s", "final_relres", "error")
 
@@ -78,3 +81,58 @@ def run(cfg: RunConfig) -> tuple[dict, SolveReport]:
     b = default_rhs(a)
     record, report, _, _ = solve_prepared(cfg, a, hint, b)
     return record, report
+
+
+# ---------------------------------------------------------------------------
+# sweep + serialisation (bench.py:36-69, 143-195 of the reference): plain host code
+
+_RUN_FIELDS = {
+    "problem": {"type": "string"}, "n": {"type": ["integer", "null"]}, "p": {"type": "integer", "minimum": 1},
+    "precond": {"enum": list(PRECONDITIONER_NAMES)}, "fill": {"type": "string"},
+    "its": {"type": ["integer", "null"]}, "converged": {"type": ["boolean", "null"]},
+    "setup_s": {"type": ["number", "null"]}, "solve_s": {"type": ["number", "null"]},
+    "final_relres": {"type": ["number", "null"]}, "error": {"type": ["string", "null"]},
+    "history": {"type": "array", "items": {"type": "number"}},
+}
+REPORT_SCHEMA = json.dumps({
+    "$schema": "https://json-schema.org/draft/2020-12/schema", "title": "benchmark report", "type": "object",
+    "required": ["runs"],
+    "properties": {"runs": {"type": "array", "items": {
+        "type": "object", "required": list(COLUMNS), "properties": _RUN_FIELDS, "additionalProperties": True}}},
+}, indent=2) + "\n"
+
+
+def sweep(cfgs) -> list[dict]:
+    """Run every configuration in order; a failing run becomes an error row and the sweep goes on."""
+    if not cfgs:
+        raise ValueError("sweep needs at least one configuration")
+    rows = []
+    for cfg in cfgs:
+        try:
+            rows.append(run(cfg)[0])
+        except Exception as exc:
+            row = dict.fromkeys(COLUMNS)
+            row.update(problem=cfg.problem.label() if cfg.problem is not None else "", p=cfg.domains,
+                       precond=cfg.precond, fill=str(cfg.fill), error=f"{type(exc).__name__}: {exc}")
+            rows.append(row)
+    return rows
+
+
+def to_json(records) -> str:
+    return json.dumps({"runs": records}, indent=2) + "\n"
+
+
+def to_csv(records) -> str:
+    """Fixed columns; booleans as true/false, floats with repr, missing values empty."""
+    def cell(v):
+        if v is None:
+            return ""
+        if isinstance(v, bool):
+            return "true" if v else "false"
+        return repr(v) if isinstance(v, float) else str(v)
+
+    out = io.StringIO()
+    w = csv.writer(out, lineterminator="\n")
+    w.writerow(COLUMNS)
+    w.writerows([cell(rec.get(col)) for col in COLUMNS] for rec in records)
+    return out.getvalue()

@@ -174,6 +174,120 @@ __global__ void mark_sends(int n, const int *__restrict__ rp, const int *__restr
     }
 }
 
+// sort the column indices of every row (used after the symmetrisation appended mirrored entries)
+__global__ void sort_rows(int n, const int *__restrict__ rp, int *ci) {
+    GRID_STRIDE(i, n) {
+        const int p0 = rp[i], len = rp[i + 1] - p0;
+        for (int gap = len >> 1; gap > 0; gap >>= 1)
+            for (int a = gap; a < len; ++a) {
+                const int cc = ci[p0 + a];
+                int b = a - gap;
+                while (b >= 0 && ci[p0 + b] > cc) {
+                    ci[p0 + b + gap] = ci[p0 + b];
+                    b -= gap;
+                }
+                ci[p0 + b + gap] = cc;
+            }
+    }
+}
+
+// ordering.py:97-127 `_grow_regions`: greedy breadth-first growth of the domains, one after the
+// other, seeded at the lowest unassigned index.  The sweep is inherently serial (every step depends
+// on the queue state left by the previous one), so it runs as ONE thread; it is the rarely used
+// fallback of `partition` for unstructured matrices.  owner / queued preset to -1.
+__global__ void grow_regions(int n, const int *__restrict__ rp, const int *__restrict__ ci, int n_dom,
+                             const int *__restrict__ sizes, int *owner, int *queue, int *queued) {
+    if (blockIdx.x || threadIdx.x) return;
+    int scan = 0;
+    for (int d = 0; d < n_dom; ++d) {
+        const int need = sizes[d];
+        int count = 0, head = 0, tail = 0;
+        while (count < need) {
+            if (head == tail) {
+                while (owner[scan] >= 0) ++scan;
+                queue[tail++] = scan;
+                queued[scan] = d;
+            }
+            const int u = queue[head++];
+            if (owner[u] >= 0) continue;
+            owner[u] = d;
+            if (++count == need) break;
+            for (int k = rp[u], ke = rp[u + 1]; k < ke; ++k) {
+                const int w = ci[k];
+                if (owner[w] < 0 && queued[w] != d) {
+                    queued[w] = d;
+                    queue[tail++] = w;
+                }
+            }
+        }
+    }
+}
+
+// precond.py:84-92 `_l1_row_shifts`: off-domain absolute row sums of the selected rows
+__global__ void l1_shifts(int n_sel, const int *__restrict__ rows, const int *__restrict__ rp,
+                          const int *__restrict__ ci, const double *__restrict__ v, const int *__restrict__ owner,
+                          double *__restrict__ out) {
+    GRID_STRIDE(r, n_sel) {
+        const int i = rows[r], d = owner[i];
+        double s = 0.0;
+        for (int k = rp[i], ke = rp[i + 1]; k < ke; ++k)
+            if (owner[ci[k]] != d) s += fabs(v[k]);
+        out[r] = s;
+    }
+}
+
+// precond.py:105-115 `_add_to_diagonal` (diagonal present); *missing counts rows that would need an insertion
+__global__ void add_to_diag(int n, const int *__restrict__ rp, const int *__restrict__ ci, double *v,
+                            const double *__restrict__ shifts, int *missing) {
+    GRID_STRIDE(i, n) {
+        int lo = rp[i], hi = rp[i + 1];
+        bool found = false;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ci[mid] == (int)i) {
+                v[mid] += shifts[i];
+                found = true;
+                break;
+            }
+            if (ci[mid] < (int)i) lo = mid + 1; else hi = mid;
+        }
+        if (!found && shifts[i] != 0.0) atomicAdd(missing, 1);
+    }
+}
+
+// factor.py:806-822 `_drop_small_rows`: keep the diagonal and entries with |v| >= tol * ||row||_2
+__device__ __forceinline__ double row_norm2(const double *v, int k0, int k1) {
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s += v[k] * v[k];
+    return sqrt(s);
+}
+
+__global__ void drop_small_count(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                 const double *__restrict__ v, double tol, int *__restrict__ counts) {
+    GRID_STRIDE(i, n) {
+        const int k0 = rp[i], k1 = rp[i + 1];
+        const double thr = tol * row_norm2(v, k0, k1);
+        int c = 0;
+        for (int k = k0; k < k1; ++k) c += !(fabs(v[k]) < thr && ci[k] != (int)i);
+        counts[i] = c;
+    }
+}
+
+__global__ void drop_small_fill(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                const double *__restrict__ v, double tol, const int *__restrict__ out_rp,
+                                int *__restrict__ out_ci, double *__restrict__ out_v) {
+    GRID_STRIDE(i, n) {
+        const int k0 = rp[i], k1 = rp[i + 1];
+        const double thr = tol * row_norm2(v, k0, k1);
+        int p = out_rp[i];
+        for (int k = k0; k < k1; ++k)
+            if (!(fabs(v[k]) < thr && ci[k] != (int)i)) {
+                out_ci[p] = ci[k];
+                out_v[p++] = v[k];
+            }
+    }
+}
+
 __global__ void diff_kernel(int n, const int *__restrict__ rp, int *__restrict__ out) {
     GRID_STRIDE(i, n) out[i] = rp[i + 1] - rp[i];
 }
@@ -289,6 +403,56 @@ extern "C" int ddilu_mark_sends(int n, const int *rp, const int *ci, const int *
                                 const int *extmap, int n_ext, int *flags, void *stream) {
     if (n <= 0 || n_ext <= 0) return DDILU_OK;
     mark_sends<<<G1(n), ST(stream)>>>(n, rp, ci, owner, doms_per_rank, my_rank, extmap, n_ext, flags);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_sort_rows_i32(int n, const int *rp, int *ci, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    sort_rows<<<G1(n), ST(stream)>>>(n, rp, ci);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_grow_regions(int n, const int *adj_rp, const int *adj_ci, int n_dom, const int *sizes,
+                                  int *owner, int *work, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    DDILU_CHECK(cudaMemsetAsync(owner, 0xFF, sizeof(int) * (size_t)n, ST(stream)));
+    DDILU_CHECK(cudaMemsetAsync(work + n, 0xFF, sizeof(int) * (size_t)n, ST(stream)));
+    grow_regions<<<1, 1, 0, ST(stream)>>>(n, adj_rp, adj_ci, n_dom, sizes, owner, work, work + n);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_l1_row_shifts(int n_sel, const int *rows, const int *rp, const int *ci, const double *v,
+                                   const int *owner, double *out, void *stream) {
+    if (n_sel <= 0) return DDILU_OK;
+    l1_shifts<<<G1(n_sel), ST(stream)>>>(n_sel, rows, rp, ci, v, owner, out);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_add_to_diagonal(int n, const int *rp, const int *ci, double *v, const double *shifts,
+                                     int *missing, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    DDILU_CHECK(cudaMemsetAsync(missing, 0, sizeof(int), ST(stream)));
+    add_to_diag<<<G1(n), ST(stream)>>>(n, rp, ci, v, shifts, missing);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_drop_small_count(int n, const int *rp, const int *ci, const double *v, double tol, int *counts,
+                                      void *stream) {
+    if (n <= 0) return DDILU_OK;
+    drop_small_count<<<G1(n), ST(stream)>>>(n, rp, ci, v, tol, counts);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_drop_small_fill(int n, const int *rp, const int *ci, const double *v, double tol,
+                                     const int *out_rp, int *out_ci, double *out_v, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    drop_small_fill<<<G1(n), ST(stream)>>>(n, rp, ci, v, tol, out_rp, out_ci, out_v);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -332,9 +332,9 @@ def index_map(n_total: int, nodes: torch.Tensor, offset: int = 0, base: torch.Te
     return m
 
 
-def sym_adjacency(pattern: DeviceCsr) -> DeviceCsr:
+def sym_adjacency(pattern: DeviceCsr, sort: bool = False) -> DeviceCsr:
     """Symmetrised pattern without the diagonal (ordering.py:72-81); neighbour
-    order inside a row is unspecified (only sets and degrees are used)."""
+    order inside a row is unspecified unless `sort` (RCM only uses sets and degrees)."""
     n = pattern.n_rows
     rp = zeros_i32(n + 1)
     call("ddilu_sym_adj_count", n, pattern.rp, pattern.ci, rp)
@@ -343,6 +343,8 @@ def sym_adjacency(pattern: DeviceCsr) -> DeviceCsr:
     ci = empty_i32(nnz)
     cursor = empty_i32(max(n, 1))
     call("ddilu_sym_adj_fill", n, pattern.rp, pattern.ci, rp, cursor, ci)
+    if sort:
+        call("ddilu_sort_rows_i32", n, rp, ci)
     return DeviceCsr(n, n, rp, ci, None, nnz)
 
 

@@ -48,9 +48,12 @@ class Comm:
             tdist.all_reduce(t, group=self.group)
         return t
 
-    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor, recv_counts, send_counts):
+    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor, recv_counts, send_counts, async_op: bool = False):
+        """Variable-size exchange.  With async_op (NCCL) a work handle is returned:
+        the transfer runs on NCCL's stream and `handle.wait()` makes the current
+        stream wait for it, so kernels launched in between overlap the exchange."""
         if not self.active:
-            return
+            return None
         if self._staged():
             sh = send.cpu()
             rh = torch.empty(recv.shape, dtype=recv.dtype)
@@ -69,8 +72,9 @@ class Comm:
             for r in reqs:
                 r.wait()
             recv.copy_(rh)
-        else:
-            tdist.all_to_all_single(recv, send, list(recv_counts), list(send_counts), group=self.group)
+            return None
+        return tdist.all_to_all_single(recv, send, list(recv_counts), list(send_counts), group=self.group,
+                                       async_op=async_op)
 
     def barrier(self):
         if self.active:

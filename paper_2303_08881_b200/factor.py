@@ -185,10 +185,17 @@ def d_carve(f: DevFactors, n1: int):
 
 
 def d_drop_small_rows(m: D.DeviceCsr, tol: float) -> D.DeviceCsr:
-    """factor.py:806-822 (`schur_drop_tol` thinning) is a 'next' row."""
+    """factor.py:806-822 (`schur_drop_tol` thinning, diagonal kept)."""
     if tol <= 0.0 or m.nnz == 0:
         return m
-    raise NotImplementedError("schur_drop_tol > 0 with a level-0 rule is outside the built hot path")
+    n = m.n_rows
+    rp = D.zeros_i32(n + 1)
+    D.call("ddilu_drop_small_count", n, m.rp, m.ci, m.val, float(tol), rp)
+    D.exclusive_scan_(rp, n)
+    nnz = int(rp[-1].item())
+    ci, val = D.empty_i32(nnz), D.empty_f64(nnz)
+    D.call("ddilu_drop_small_fill", n, m.rp, m.ci, m.val, float(tol), rp, ci, val)
+    return D.DeviceCsr(n, m.n_cols, rp, ci, val, nnz)
 
 
 def d_partial_ilu(a: D.DeviceCsr, n_interior: int, rule: FillRule, schur_drop_tol: float = 0.0,

@@ -67,9 +67,9 @@ def _owner_device(owner) -> torch.Tensor:
 
 
 def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
-    """ordering.py:148-198.  Structured boxes on the device; the unstructured
-    breadth-first fallback (`_grow_regions`, a strictly serial greedy sweep) is
-    a "next" row of SURVEY.md 8f and not built yet."""
+    """ordering.py:148-198.  Structured boxes as one kernel; the unstructured
+    breadth-first fallback (`_grow_regions`) is a strictly serial greedy sweep
+    and runs as a single device thread."""
     n = a.n_rows
     if a.n_rows != a.n_cols:
         raise ValueError("partition requires a square matrix")
@@ -92,9 +92,15 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
             if np.max(np.abs(sizes - n / p)) <= max(1.0, 0.1 * n / p):
                 owner_d = D.box_owner(n, dims, factors)
                 return _wrap_owner(D.to_host_i64(owner_d), owner_d)
-    raise NotImplementedError(
-        "unstructured breadth-first partition (ordering.py:97-127,192-198) is outside the built hot path; "
-        "pass grid_hint for a box split or use row_block_owner")
+    # unstructured fallback (ordering.py:192-198): greedy breadth-first growth over the symmetrised pattern
+    base, rem = divmod(n, p)
+    sizes = np.full(p, base, dtype=np.int32)
+    sizes[:rem] += 1
+    adj = D.sym_adjacency(a.device(), sort=True)
+    owner_d = D.empty_i32(n)
+    work = D.empty_i32(2 * n)
+    D.call("ddilu_grow_regions", n, adj.rp, adj.ci, p, torch.from_numpy(sizes).to(D.dev()), owner_d, work)
+    return _wrap_owner(D.to_host_i64(owner_d), owner_d)
 
 
 class DomainLayout:

@@ -115,14 +115,16 @@ class LocalSystem:
         self.send_idx = torch.nonzero(sf)[:, 1].to(D.I32).contiguous()
         return D.index_map(n, halo_nodes, offset=self.n_loc, base=colmap)
 
-    def exchange_halo(self, src_ext: torch.Tensor, halo_out: torch.Tensor):
+    def exchange_halo(self, src_ext: torch.Tensor, halo_out: torch.Tensor, async_op: bool = False):
         """halo_out[:n_halo] <- exterior values of the other ranks; src_ext is
-        this rank's exterior section (n_ext entries)."""
+        this rank's exterior section (n_ext entries).  Returns a work handle when
+        the exchange was started asynchronously (caller must .wait())."""
         if not self.comm.active:
-            return
+            return None
         ns = sum(self.send_counts)
         D.gather(ns, self.send_idx, src_ext, self._sendbuf)
-        self.comm.all_to_all(halo_out[: self.n_halo], self._sendbuf[:ns], self.recv_counts, self.send_counts)
+        return self.comm.all_to_all(halo_out[: self.n_halo], self._sendbuf[:ns], self.recv_counts, self.send_counts,
+                                    async_op=async_op)
 
     # ----------------------------------------------------------------- matvec
     def spmv(self, x: torch.Tensor, out: torch.Tensor, b: torch.Tensor | None = None, mode: int = 0):
@@ -134,8 +136,11 @@ class LocalSystem:
             self._xbuf[: self.n_loc].copy_(x[: self.n_loc])
             x = self._xbuf
         if self.comm.active:
+            # start the halo exchange, run the interior rows while it is in flight, then the interface rows
+            work = self.exchange_halo(x[self.n_int:self.n_loc], x[self.n_loc:], async_op=True)
             D.spmv(self.a_loc, x, out, b, mode, 0, self.n_int)
-            self.exchange_halo(x[self.n_int:self.n_loc], x[self.n_loc:])
+            if work is not None:
+                work.wait()
             D.spmv(self.a_loc, x, out, b, mode, self.n_int, self.n_loc)
         else:
             D.spmv(self.a_loc, x, out, b, mode)
@@ -279,10 +284,21 @@ class BjIluPrecond(_DDPrecond):
 
     def __init__(self, a, layout, rule: FillRule, l1: bool, use_rcm: bool = True):
         super().__init__(a, layout, use_rcm)
-        if l1:
-            raise NotImplementedError("l1bj (precond.py:84-125) is a 'next' row of the hot-path scope (SURVEY.md 8f)")
         self.rule, self.l1 = rule, l1
-        self._f = d_factorize(self.system.a_dom, rule).prepare()
+        mat = self.system.a_dom
+        if l1:
+            # precond.py:207-212: add each row's off-domain absolute sum to the diagonal before factorising
+            s = self.system
+            ad = a.device()
+            shifts = D.empty_f64(max(1, s.n_loc))
+            D.call("ddilu_l1_row_shifts", s.n_loc, s.nodes, ad.rp, ad.ci, ad.val, layout._owner_d, shifts)
+            vals = mat.val.clone()
+            missing = D.zeros_i32(1)
+            D.call("ddilu_add_to_diagonal", s.n_loc, mat.rp, mat.ci, vals, shifts, missing)
+            if int(missing.item()):
+                raise NotImplementedError("l1bj on a matrix with structurally missing diagonal entries")
+            mat = D.DeviceCsr(mat.n_rows, mat.n_cols, mat.rp, mat.ci, vals, mat.nnz)
+        self._f = d_factorize(mat, rule).prepare()
         self._factors = None
 
     @property

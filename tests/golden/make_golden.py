@@ -264,6 +264,9 @@ def pipeline():
     cases += [("cd27_8", 8, "grid", "schur", "ilut:0.001,20"), ("cd27_8", 8, "grid", "bj", "ilut:0.001,20"),
               ("cd27_8", 1, "grid", "bj", "ilut:0.001,20"), ("cd27_8", 8, "grid", "schur", "ilu0"),
               ("cd27_8", 2, "grid", "bj", "ilu0"), ("aniso3d_10", 8, "grid", "schur", "ilut:0.01,5")]
+    # appended later (keeps the random draws of the cases above unchanged)
+    cases += [("aniso3d_10", 8, "grid", "l1bj", "ilu0"), ("convdiff3d_8", 8, "grid", "l1bj", "ilu0"),
+              ("poisson3d_9x8x7", 3, "rows", "l1bj", "ilu0")]
     put("pipeline.problems", np.array(sorted(problems)))
     for pname, (a, hint) in sorted(problems.items()):
         put_csr(f"p.{pname}.a", a)
@@ -285,7 +288,7 @@ def pipeline():
         put(k + ".global_perm_forward", layout.global_perm.forward)
         rule = rfac.FillRule.parse(fill)
         m = rpre.make_preconditioner(pc, a, layout, rule, inner_iters=3)
-        put_precond(k, pc if pc in ("bj", "schur") else "rap", m)
+        put_precond(k, "bj" if pc in ("bj", "l1bj") else ("schur" if pc == "schur" else "rap"), m)
         r = OUT[f"p.{pname}.r"]
         put(k + ".apply_r", m.apply(r))
         if pc == "schur" and layout.n_exterior:

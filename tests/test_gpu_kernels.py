@@ -79,6 +79,22 @@ def test_rcm_bit_exact(P, golden_kernels):
         assert np.array_equal(perm.inverse, g[k + ".rcm_inverse"]), name
 
 
+def test_partitions_bit_exact(P, golden_kernels):
+    """Structured boxes, their breadth-first fallback (uneven grids) and the
+    unstructured breadth-first partition (ordering.py:97-127, 148-198)."""
+    import json
+    g = golden_kernels
+    for case in g.names("partition.cases"):
+        dims, p = json.loads(case)
+        a = P.poisson2d(*dims) if len(dims) == 2 else P.poisson3d(*dims)
+        got = P.partition(a, p, grid_hint=tuple(dims))
+        assert np.array_equal(np.asarray(got), g[f"partition.{'x'.join(map(str, dims))}.p{p}"]), case
+    for name in g.names("kernels.names"):
+        a = g.csr("k." + name + ".a", _csr(P))
+        for p in (2, 3):
+            assert np.array_equal(np.asarray(P.partition(a, p)), g[f"k.{name}.grow_owner_p{p}"]), (name, p)
+
+
 def test_rcm_larger_grids(P, orc):
     for a in (P.aniso3d(17, 13, 11), P.poisson2d(64, 37), P.convdiff27(9, 10, 11)):
         fwd, inv = orc.rcm(_to_orc(orc, a))
@@ -106,15 +122,16 @@ def test_factorisations_against_reference(P, golden_kernels):
         same_csr(fv.lower, g, k + ".milu0_vecs.lower")
         same_csr(fv.upper, g, k + ".milu0_vecs.upper")
         n1 = int(g[k + ".n_interior"])
-        pf = P.partial_ilu(a, n1, P.FillRule("ilu0"))
-        kk = k + ".partial_ilu0"
-        same_csr(pf.interior.lower, g, kk + ".interior.lower")
-        same_csr(pf.interior.upper, g, kk + ".interior.upper")
-        same_csr(pf.w_block, g, kk + ".w")
-        same_csr(pf.z_block, g, kk + ".z")
-        same_csr(pf.s_tilde, g, kk + ".s")
-        same_csr(pf.schur.lower, g, kk + ".schur.lower")
-        same_csr(pf.schur.upper, g, kk + ".schur.upper")
+        for tag, drop in (("ilu0", 0.0), ("ilu0_drop", 0.05)):       # the second exercises schur_drop_tol thinning
+            pf = P.partial_ilu(a, n1, P.FillRule("ilu0"), schur_drop_tol=drop)
+            kk = k + ".partial_" + tag
+            same_csr(pf.interior.lower, g, kk + ".interior.lower")
+            same_csr(pf.interior.upper, g, kk + ".interior.upper")
+            same_csr(pf.w_block, g, kk + ".w")
+            same_csr(pf.z_block, g, kk + ".z")
+            same_csr(pf.s_tilde, g, kk + ".s")
+            same_csr(pf.schur.lower, g, kk + ".schur.lower")
+            same_csr(pf.schur.upper, g, kk + ".schur.upper")
         tl = P.extract_two_level_blocks(f0, n1)
         same_csr(tl.interior.lower, g, k + ".twolevel.interior.lower")
         same_csr(tl.interior.upper, g, k + ".twolevel.interior.upper")

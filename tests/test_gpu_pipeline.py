@@ -65,7 +65,7 @@ def test_layout_and_factors_bit_exact(P, golden_pipeline):
         for d, dom in enumerate(m.domains):
             assert np.array_equal(dom.interior_nodes, g[f"{k}.dom{d}.interior_nodes"]), (tag, d)
             assert np.array_equal(dom.exterior_nodes, g[f"{k}.dom{d}.exterior_nodes"]), (tag, d)
-        if pc == "bj":
+        if pc in ("bj", "l1bj"):
             for d, f in enumerate(m.factors):
                 same_csr(f.lower, g, f"{k}.dom{d}.factors.lower")
                 same_csr(f.upper, g, f"{k}.dom{d}.factors.upper")
@@ -100,7 +100,7 @@ def test_apply_and_solve_match_reference(P, golden_pipeline):
         k = "c." + tag
         r = g[f"p.{pname}.r"]
         z = m.apply(r)
-        if pc == "bj" or p == 1:
+        if pc in ("bj", "l1bj") or p == 1:
             assert np.array_equal(z, g[k + ".apply_r"]), tag       # no reductions on this path
         else:
             assert _rel(z, g[k + ".apply_r"]) < 1e-9, (tag, _rel(z, g[k + ".apply_r"]))

@@ -109,7 +109,7 @@ def _check_precond(g, k, pc, m):
     for d, dom in enumerate(m.domains):
         assert np.array_equal(dom.interior_nodes, g[f"{k}.dom{d}.interior_nodes"])
         assert np.array_equal(dom.exterior_nodes, g[f"{k}.dom{d}.exterior_nodes"])
-    if pc == "bj":
+    if pc in ("bj", "l1bj"):
         for d, f in enumerate(m.factors):
             same_csr(f.lower, g, f"{k}.dom{d}.factors.lower")
             same_csr(f.upper, g, f"{k}.dom{d}.factors.upper")
