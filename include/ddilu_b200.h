@@ -101,6 +101,41 @@ int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *or
                             int uniform_width, const int *scol, const double *sval, const double *sdiag,
                             const int *gwait, const double *b, double *x, long long *stamps, void *stream);
 
+/* ---- tiled triangular solve (csrc/tiled.cu): sparse.py:228-272 again, for factors whose
+ * rows cluster into tiles (<= 1024 rows) with an ACYCLIC tile dependency graph.  A CTA
+ * walks a tile's levels with the tile's x in shared memory; boundary dependencies go
+ * through L2.  Setup passes (all device pointers unless *_h):
+ *   tile_box_keys : key of row i = box of grid node nodes[i] (x fastest, like ordering.py:171-190),
+ *                   + owner[node] * n_boxes when owner != NULL; *n_keys_h = boxes per owner
+ *   tile_heads / tile_assign : from (key, row) pairs sorted by key: compact tile ids,
+ *                   tile_of[row], tpos[row] (position in the sorted list), tile_ptr[n_tiles+1]
+ *   tile_edges_*  : (producer tile, consumer tile) pairs of the cross-tile dependencies
+ *   tile_relax    : `passes` sweeps of tlev[c] = max(tlev[c], tlev[p]+1); flags[0] = last sweep
+ *                   changed something, flags[1] = cycle (a level reached n_tiles)
+ *   tile_build    : fill = 0: size of every tile's static block (16-byte units) -> blk16[q],
+ *                   stats[0..2] = max rows, max externals, max bytes; fill = 1: blk16 holds the
+ *                   scanned offsets, blocks are written to blob, stats[3] = first bad pivot row
+ *   sptrsv_tiled  : x = T^-1 b; one cooperative launch */
+int ddilu_tiled_set_tuning(const char *key, int value);
+int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *owner,
+                        int *keys, long long *n_keys_h, void *stream);
+int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream);
+int ddilu_tile_assign(int n, const int *sorted_keys, const int *head_scan, const int *sorted_rows, int *tile_of,
+                      int *tpos, int *tile_ptr, void *stream);
+int ddilu_tile_edges_count(int n, const int *row_ptr, const int *col_idx, int upper, const int *tile_of, int *cnt,
+                           void *stream);
+int ddilu_tile_edges_fill(int n, const int *row_ptr, const int *col_idx, int upper, const int *tile_of,
+                          const int *off, int *edges, void *stream);
+int ddilu_tile_relax(long long n_edges, const int *edges, int n_tiles, int *tlev, int *flags, int passes,
+                     void *stream);
+int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_ptr, const int *trows,
+                     const int *tile_of, const int *tpos, const int *row_ptr, const int *col_idx,
+                     const double *values, const int *glev, int upper, int has_diag, int *blk16, int *stats,
+                     unsigned char *blob, void *stream);
+long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax);
+int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
+                       int emax, int has_diag, const double *b, double *x, void *stream);
+
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,
                       double *rownorm, void *stream);

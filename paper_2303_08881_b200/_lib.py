@@ -39,6 +39,16 @@ SIGNATURES = {
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_sell_trace": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_tiled_set_tuning": (_I, [_S, _I]),
+    "ddilu_tile_box_keys": (_I, [_I, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_tile_heads": (_I, [_I, _P, _P, _P]),
+    "ddilu_tile_assign": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_tile_edges_count": (_I, [_I, _P, _P, _I, _P, _P, _P]),
+    "ddilu_tile_edges_fill": (_I, [_I, _P, _P, _I, _P, _P, _P, _P]),
+    "ddilu_tile_relax": (_I, [_L, _P, _I, _P, _P, _I, _P]),
+    "ddilu_tile_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "ddilu_tiled_smem_bytes": (_L, [_I, _I, _I]),
+    "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),

@@ -1,0 +1,667 @@
+// Tiled sparse triangular solve: the production path for factors whose rows can
+// be clustered into tiles with a one-way (acyclic) tile dependency graph
+// (structured problems: box tiles of the grid; checked, not assumed).
+//
+// Replaces sparse.py:228-272 (`_lower_solve`, `_upper_solve`) like sptrsv.cu.
+// Why a second kernel: the sync-free solve pays one L2 round trip (0.4-1.9 us)
+// per LEVEL because consecutive levels live in different warps / SMs.  Here a
+// CTA owns a tile of <= 1024 rows and walks the tile's levels with the tile's
+// part of x in SHARED memory (one named barrier per level, ~0.1 us); only the
+// dependencies that cross a tile boundary travel through L2, and those are
+// fetched by a dedicated polling warp ahead of the compute warps.  The tile's
+// matrix data (one contiguous "static block": level table, row ids, external
+// columns, pivots, values, 16-bit local column codes) arrives by one
+// cp.async.bulk (TMA) per tile into a 3-deep shared-memory ring, signalled
+// through an mbarrier; a feeder warp gathers the tile's right-hand side one
+// tile ahead.  Row sums keep the storage order of the reference: bit-exact.
+//
+// Deadlock freedom: tiles are listed in a topological order of the tile graph,
+// CTA c takes tiles c, c+G, c+2G, ... in that order and the launch is
+// cooperative (all CTAs co-resident); the lowest unfinished tile of the list is
+// always the current tile of its CTA and all its producers are finished.
+//
+// Algorithmic bytes: 12*nnz + 4*(n+1) + 16n; this layout moves
+// 10*nnz + 4n (row ids) + 16n (+ 4 per boundary dependency).
+#include <stdint.h>
+
+#include "common.cuh"
+#include "ddilu_b200.h"
+
+namespace ddilu {
+
+constexpr int TILE_MAX_ROWS = 1024;
+constexpr int TILE_HDR_BYTES = 64;
+constexpr int TILE_PAD = 0xFFFF;
+constexpr int TILE_NBUF = 3;
+constexpr int TILE_HELPERS = 64;   // warp 0: TMA + right-hand side, warp 1: external dependencies
+
+// header ints of a static block
+enum { H_T = 0, H_NLEV, H_NEXT, H_NENT, H_OFF_ROWS, H_OFF_EXT, H_OFF_PIV, H_OFF_VAL, H_OFF_CODE, H_BYTES };
+
+struct TiledTuning {
+    int compute_threads = 128;
+    int ctas_per_sm = 0;  // 0: as many as fit
+    int store_mode = 0;   // how a finished row is published to L2: 0 st.volatile, 1 st.relaxed.gpu, 2 plain st
+};
+static TiledTuning g_tiled;
+
+#define GRID_STRIDE_Q(i, n) \
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (long long)gridDim.x * blockDim.x)
+
+__global__ void tile_box_keys(int n, const int *__restrict__ nodes, int d0, int d1, int t0, int t1, int t2, int nb0,
+                              int nb1, int nboxes, const int *__restrict__ owner, int *__restrict__ keys) {
+    GRID_STRIDE_Q(i, n) {
+        const int g = nodes ? nodes[i] : (int)i;
+        const int c0 = g % d0, c1 = (g / d0) % d1, c2 = g / (d0 * d1);
+        int key = ((c2 / t2) * nb1 + (c1 / t1)) * nb0 + (c0 / t0);
+        if (owner) key += owner[g] * nboxes;
+        keys[i] = key;
+    }
+}
+
+__global__ void tile_heads(int n, const int *__restrict__ skeys, int *__restrict__ flags) {
+    GRID_STRIDE_Q(q, n) flags[q] = (q == 0 || skeys[q] != skeys[q - 1]) ? 1 : 0;
+}
+
+__global__ void tile_assign(int n, const int *__restrict__ skeys, const int *__restrict__ scan,
+                            const int *__restrict__ srows, int *__restrict__ tile_of, int *__restrict__ tpos,
+                            int *__restrict__ tile_ptr) {
+    GRID_STRIDE_Q(q, n) {
+        const bool head = q == 0 || skeys[q] != skeys[q - 1];
+        const int tid = scan[q] + (head ? 0 : -1);
+        const int row = srows[q];
+        tile_of[row] = tid;
+        tpos[row] = (int)q;
+        if (head) tile_ptr[tid] = (int)q;
+        if (q == n - 1) tile_ptr[tid + 1] = n;
+    }
+}
+
+// cross-tile dependencies as (producer tile, consumer tile) pairs
+template <bool FILL>
+__global__ void tile_edges(int n, const int *__restrict__ rp, const int *__restrict__ ci, int upper,
+                           const int *__restrict__ tile_of, int *__restrict__ cnt, const int *__restrict__ off,
+                           int2 *__restrict__ edges) {
+    GRID_STRIDE_Q(i, n) {
+        const int row = (int)i, t = tile_of[row];
+        int c = 0, last = -1;
+        long long o = FILL ? off[row] : 0;
+        for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
+            const int j = ci[k];
+            if (upper ? j > row : j < row) {
+                const int tj = tile_of[j];
+                if (tj != t && tj != last) {   // runs of the same producer tile collapse
+                    if (FILL) edges[o + c] = make_int2(tj, t);
+                    ++c;
+                    last = tj;
+                }
+            }
+        }
+        if (!FILL) cnt[row] = c;
+    }
+}
+
+// one relaxation sweep of tlev[consumer] = max(tlev[consumer], tlev[producer] + 1)
+__global__ void tile_relax(long long n_edges, const int2 *__restrict__ edges, int n_tiles, int *tlev, int *flags) {
+    GRID_STRIDE_Q(e, n_edges) {
+        const int2 ed = edges[e];
+        const int s = tlev[ed.x] + 1;
+        if (s > tlev[ed.y]) {
+            if (s >= n_tiles) {
+                flags[1] = 1;   // a path longer than the number of tiles: the tile graph has a cycle
+            } else {
+                atomicMax(tlev + ed.y, s);
+                flags[0] = 1;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ int block_excl_scan(int v, int *total, int *wsum) {
+    // 1024 threads; wsum: 33 ints of shared memory
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __syncthreads();   // wsum may still be read from a previous call
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int w = wsum[lane], winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, winc, o);
+            if (lane >= o) winc += t;
+        }
+        wsum[lane] = winc - w;
+        if (lane == 31) wsum[32] = winc;
+    }
+    __syncthreads();
+    *total = wsum[32];
+    return wsum[warp] + inc - v;
+}
+
+__device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
+
+// One CTA (1024 threads, one per row) per tile, tiles in schedule order.
+//   COUNT (FILL = false): size of the tile's static block -> blk16[q] (16-byte units), maxima -> stats
+//   FILL: writes the static block at blob + 16 * blk16[q]
+// The rows of a tile are sorted by (global level of the factor, local index): rows of
+// one level never depend on each other, so the distinct levels met in a tile are its
+// local levels.
+template <bool FILL>
+__global__ void __launch_bounds__(TILE_MAX_ROWS)
+tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ tile_ptr,
+           const int *__restrict__ trows, const int *__restrict__ tile_of, const int *__restrict__ tpos,
+           const int *__restrict__ rp, const int *__restrict__ ci, const double *__restrict__ val,
+           const int *__restrict__ glev, int upper, int has_diag, int *blk16, int *stats, unsigned char *blob) {
+    __shared__ int s_key[TILE_MAX_ROWS];     // level of local row i, later level index of slot s
+    __shared__ int s_slot[TILE_MAX_ROWS];    // slot of local row i
+    __shared__ int s_skey[TILE_MAX_ROWS];    // level key of slot s
+    __shared__ int s_lstart[TILE_MAX_ROWS + 1];
+    __shared__ int s_lk[TILE_MAX_ROWS];      // widest row of level l
+    __shared__ int s_lent[TILE_MAX_ROWS + 1];
+    __shared__ int s_eoff[TILE_MAX_ROWS + 1];
+    __shared__ int s_wsum[33];
+    const int q = blockIdx.x;
+    const int t = tsched[q];
+    const int base = tile_ptr[t], T = tile_ptr[t + 1] - base;
+    const int i = threadIdx.x;
+    const bool active = i < T;
+    const int row = active ? trows[base + i] : -1;
+    const int key = active ? glev[row] : 0x7FFFFFFF;
+    s_key[i] = key;
+    s_lk[i] = 0;
+    __syncthreads();
+    // rank = slot
+    int slot = 0;
+    if (active) {
+        for (int j = 0; j < T; ++j) {
+            const int kj = s_key[j];
+            slot += (kj < key || (kj == key && j < i)) ? 1 : 0;
+        }
+        s_slot[i] = slot;
+        s_skey[slot] = key;
+    }
+    __syncthreads();
+    // level index of every slot
+    int total;
+    const int head = (i < T && (i == 0 || s_skey[i] != s_skey[i - 1])) ? 1 : 0;
+    const int lidx_of_slot_i = block_excl_scan(head, &total, s_wsum) + head - 1;
+    const int n_lev = total;
+    if (i < T) {
+        if (head) s_lstart[lidx_of_slot_i] = i;
+        s_key[i] = lidx_of_slot_i;   // s_key now: level index by SLOT
+    }
+    if (i == 0) s_lstart[n_lev] = T;
+    __syncthreads();
+    // dependencies of my row
+    int nd = 0, ne = 0;
+    const int my_l = active ? s_key[slot] : 0;
+    if (active) {
+        for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
+            const int j = ci[k];
+            if (upper ? j > row : j < row) {
+                ++nd;
+                if (tile_of[j] != t) ++ne;
+            }
+        }
+        atomicMax(&s_lk[my_l], nd);
+        s_eoff[slot] = ne;
+    }
+    __syncthreads();
+    // external offsets by slot
+    const int ne_slot = i < T ? s_eoff[i] : 0;
+    int n_ext;
+    const int eoff_i = block_excl_scan(ne_slot, &n_ext, s_wsum);
+    __syncthreads();
+    if (i < T) s_eoff[i] = eoff_i;
+    if (i == 0) s_eoff[T] = n_ext;
+    // entry offsets by level
+    const int lw = i < n_lev ? s_lk[i] * (s_lstart[i + 1] - s_lstart[i]) : 0;
+    int n_ent;
+    const int lent_i = block_excl_scan(lw, &n_ent, s_wsum);
+    if (i < n_lev) s_lent[i] = lent_i;
+    if (i == 0) s_lent[n_lev] = n_ent;
+    __syncthreads();
+    // layout
+    const int off_lvl = TILE_HDR_BYTES;
+    const int off_rows = off_lvl + pad16(16 * (n_lev + 1));
+    const int off_ext = off_rows + pad16(4 * T);
+    const int off_piv = off_ext + pad16(4 * n_ext);
+    const int off_val = off_piv + (has_diag ? pad16(8 * T) : 0);
+    const int off_code = off_val + pad16(8 * n_ent);
+    const int bytes = off_code + pad16(2 * n_ent);
+    if (!FILL) {
+        if (i == 0) {
+            blk16[q] = bytes >> 4;
+            atomicMax(stats + 0, T);
+            atomicMax(stats + 1, n_ext);
+            atomicMax(stats + 2, bytes);
+        }
+        return;
+    }
+    unsigned char *blk = blob + 16LL * blk16[q];
+    int *hdr = (int *)blk;
+    if (i < TILE_HDR_BYTES / 4) {
+        int v = 0;
+        switch (i) {
+            case H_T: v = T; break;
+            case H_NLEV: v = n_lev; break;
+            case H_NEXT: v = n_ext; break;
+            case H_NENT: v = n_ent; break;
+            case H_OFF_ROWS: v = off_rows; break;
+            case H_OFF_EXT: v = off_ext; break;
+            case H_OFF_PIV: v = has_diag ? off_piv : 0; break;
+            case H_OFF_VAL: v = off_val; break;
+            case H_OFF_CODE: v = off_code; break;
+            case H_BYTES: v = bytes; break;
+            default: break;
+        }
+        hdr[i] = v;
+    }
+    int4 *lvl = (int4 *)(blk + off_lvl);
+    if (i <= n_lev)   // .w = externals needed by the levels up to and including l
+        lvl[i] = make_int4(s_lstart[i], s_lent[i], i < n_lev ? s_lk[i] : 0, i < n_lev ? s_eoff[s_lstart[i + 1]] : n_ext);
+    // zero the alignment tails so the blob is fully defined
+    {
+        const int tails[5][2] = {{off_rows + 4 * T, off_ext}, {off_ext + 4 * n_ext, off_piv},
+                                 {off_piv + (has_diag ? 8 * T : 0), off_val}, {off_val + 8 * n_ent, off_code},
+                                 {off_code + 2 * n_ent, bytes}};
+        if (i < 5)
+            for (int p = tails[i][0]; p < tails[i][1]; ++p) blk[p] = 0;
+    }
+    if (!active) return;
+    int *rows_out = (int *)(blk + off_rows);
+    int *ext_out = (int *)(blk + off_ext);
+    double *piv_out = (double *)(blk + off_piv);
+    double *val_out = (double *)(blk + off_val);
+    unsigned short *code_out = (unsigned short *)(blk + off_code);
+    rows_out[slot] = row;
+    const int l0 = s_lstart[my_l], w = s_lstart[my_l + 1] - l0, K = s_lk[my_l];
+    const long long e0 = (long long)s_lent[my_l] + (slot - l0);
+    int kk = 0, e = s_eoff[slot];
+    double diag = 1.0;
+    bool seen = false;
+    for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
+        const int j = ci[k];
+        if (upper ? j > row : j < row) {
+            int code;
+            if (tile_of[j] == t) {
+                code = s_slot[tpos[j] - base];
+            } else {
+                code = T + e;
+                ext_out[e] = j;
+                ++e;
+            }
+            code_out[e0 + (long long)kk * w] = (unsigned short)code;
+            val_out[e0 + (long long)kk * w] = val[k];
+            ++kk;
+        } else if (j == row) {
+            diag = val[k];
+            seen = true;
+        }
+    }
+    for (; kk < K; ++kk) {
+        code_out[e0 + (long long)kk * w] = (unsigned short)TILE_PAD;
+        val_out[e0 + (long long)kk * w] = 0.0;
+    }
+    if (has_diag) {
+        piv_out[slot] = diag;
+        if (!seen || fabs(diag) < 1e-300) atomicMin(stats + 3, row);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solve
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void compute_barrier(int threads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+}
+
+struct TileCtl {
+    uint64_t mbar[TILE_NBUF];
+    unsigned long long ext_prog[2];   // (tile ordinal << 32) | externals delivered
+    int b_ready[2];                   // tile ordinal + 1 whose right-hand side sits in bs[buf]
+    int comp_done;                    // tiles finished by the compute warps
+    int pad;
+};
+
+template <bool HAS_DIAG>
+__global__ void __launch_bounds__(TILE_HELPERS + 256)
+sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
+             int tmax, int emax, int store_mode, const double *__restrict__ b, double *x) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *stat = smem;
+    double *bs = (double *)(smem + (size_t)TILE_NBUF * stat_max);
+    double *xs = bs + 2 * (size_t)tmax;
+    TileCtl *ctl = (TileCtl *)(xs + 2 * (size_t)(tmax + emax));
+    const int xstride = tmax + emax;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    const int nk = (n_tiles - (int)blockIdx.x + G - 1) / G;   // my tiles: blockIdx.x + k*G
+    if (tid == 0) {
+        for (int s = 0; s < TILE_NBUF; ++s) mbar_init(&ctl->mbar[s], 1);
+        ctl->ext_prog[0] = ctl->ext_prog[1] = 0ULL;
+        ctl->b_ready[0] = ctl->b_ready[1] = 0;
+        ctl->comp_done = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    volatile int *comp_done = &ctl->comp_done;
+
+    if (warp == 0) {
+        // ---------------- feeder: TMA of the static blocks + right-hand side gather
+        auto issue = [&](int k) {
+            const long long qq = (long long)blockIdx.x + (long long)k * G;
+            const int o0 = blk_off16[qq], o1 = blk_off16[qq + 1];
+            const uint32_t bytes = (uint32_t)(o1 - o0) << 4;
+            uint64_t *bar = &ctl->mbar[k % TILE_NBUF];
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(stat + (size_t)(k % TILE_NBUF) * stat_max, blob + 16LL * o0, bytes, bar);
+        };
+        if (lane == 0 && nk > 0) issue(0);
+        for (int k = 0; k < nk; ++k) {
+            if (k >= 2)
+                while (*comp_done < k - 1) {
+                }
+            if (lane == 0 && k + 1 < nk) issue(k + 1);
+            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
+            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
+            const int *hdr = (const int *)blk;
+            const int T = hdr[H_T];
+            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+            double *bsk = bs + (size_t)(k & 1) * tmax;
+            for (int s0 = 0; s0 < T; s0 += 256) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int s = s0 + u * 32 + lane;
+                    v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int s = s0 + u * 32 + lane;
+                    if (s < T) bsk[s] = v[u];
+                }
+            }
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) *(volatile int *)&ctl->b_ready[k & 1] = k + 1;
+        }
+    } else if (warp == 1) {
+        // ---------------- poller: boundary dependencies, in the order the levels need them
+        for (int k = 0; k < nk; ++k) {
+            if (k >= 2)
+                while (*comp_done < k - 1) {
+                }
+            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
+            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
+            const int *hdr = (const int *)blk;
+            const int T = hdr[H_T], n_ext = hdr[H_NEXT];
+            const int *ext = (const int *)(blk + hdr[H_OFF_EXT]);
+            double *xe = xs + (size_t)(k & 1) * xstride + T;
+            volatile unsigned long long *prog = &ctl->ext_prog[k & 1];
+            for (int base = 0; base < n_ext; base += 128) {
+                int c[4];
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = base + u * 32 + lane;
+                    c[u] = e < n_ext ? ext[e] : -1;
+                }
+                // all polls of the chunk in flight together; delivered and published 32 at a time, in order
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = c[u] >= 0 ? ld_l2(x + c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (base + u * 32 < n_ext) {
+                        if (c[u] >= 0) {
+                            while (is_sentinel(v[u])) v[u] = ld_l2(x + c[u]);
+                            xe[base + u * 32 + lane] = v[u];
+                        }
+                        __syncwarp();
+                        __threadfence_block();
+                        const int upto = base + (u + 1) * 32 < n_ext ? base + (u + 1) * 32 : n_ext;
+                        if (lane == 0) *prog = ((unsigned long long)(unsigned)k << 32) | (unsigned)upto;
+                    }
+                }
+            }
+        }
+    } else {
+        // ---------------- compute warps
+        const int ctid = tid - TILE_HELPERS, NC = blockDim.x - TILE_HELPERS;
+        for (int k = 0; k < nk; ++k) {
+            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
+            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) {
+            }
+            __threadfence_block();
+            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
+            const int *hdr = (const int *)blk;
+            const int T = hdr[H_T], n_lev = hdr[H_NLEV];
+            const int4 *lvl = (const int4 *)(blk + TILE_HDR_BYTES);
+            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+            const double *piv = (const double *)(blk + hdr[H_OFF_PIV]);
+            const double *vals = (const double *)(blk + hdr[H_OFF_VAL]);
+            const unsigned short *codes = (const unsigned short *)(blk + hdr[H_OFF_CODE]);
+            const double *bsk = bs + (size_t)(k & 1) * tmax;
+            double *xsk = xs + (size_t)(k & 1) * xstride;
+            volatile unsigned long long *prog = &ctl->ext_prog[k & 1];
+            int have = 0;
+            (void)T;
+            int4 d = lvl[0];
+            for (int l = 0; l < n_lev; ++l) {
+                const int4 dn = lvl[l + 1];
+                const int w = dn.x - d.x;
+                if (d.w > have) {
+                    const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)d.w;
+                    unsigned long long got;
+                    do got = *prog; while (got < want);
+                    have = (int)(got & 0xffffffffULL);
+                    __threadfence_block();
+                }
+                for (int p = ctid; p < w; p += NC) {
+                    const int s = d.x + p;
+                    double sum = bsk[s];
+                    const unsigned short *cp = codes + d.y + p;
+                    const double *vp = vals + d.y + p;
+                    for (int kk = 0; kk < d.z; ++kk) {
+                        const int c = cp[kk * w];
+                        if (c != TILE_PAD) sum -= vp[kk * w] * xsk[c];
+                    }
+                    if (HAS_DIAG) sum = sum / piv[s];
+                    sum = scrub_sentinel(sum);
+                    xsk[s] = sum;
+                    if (store_mode == 0) st_l2(x + rows[s], sum);
+                    else if (store_mode == 1) st_gpu(x + rows[s], sum);
+                    else x[rows[s]] = sum;
+                }
+                compute_barrier(NC);
+                d = dn;
+            }
+            if (n_lev == 0) compute_barrier(NC);
+            if (ctid == 0) {
+                __threadfence_block();
+                *comp_done = k + 1;
+            }
+        }
+    }
+}
+
+}  // namespace ddilu
+
+using namespace ddilu;
+#define ST(s) ((cudaStream_t)(s))
+
+extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
+    if (!key) return DDILU_ERR_ARG;
+    const char *k = key;
+    auto eq = [&](const char *s) {
+        int i = 0;
+        while (s[i] && k[i] == s[i]) ++i;
+        return s[i] == 0 && k[i] == 0;
+    };
+    if (eq("compute_threads")) {
+        if (value < 32 || value > 256 || (value & 31)) return DDILU_ERR_ARG;
+        g_tiled.compute_threads = value;
+    } else if (eq("ctas_per_sm")) {
+        g_tiled.ctas_per_sm = value;
+    } else if (eq("store_mode")) {
+        g_tiled.store_mode = value;
+    } else {
+        return DDILU_ERR_ARG;
+    }
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h,
+                                   const int *owner, int *keys, long long *n_keys_h, void *stream) {
+    if (nd < 1 || nd > 3) return DDILU_ERR_ARG;
+    int d[3] = {1, 1, 1}, t[3] = {1, 1, 1}, nb[3];
+    for (int a = 0; a < nd; ++a) {
+        d[a] = dims_h[a];
+        t[a] = tdims_h[a] < 1 ? 1 : tdims_h[a];
+    }
+    long long nboxes = 1;
+    for (int a = 0; a < 3; ++a) {
+        nb[a] = (d[a] + t[a] - 1) / t[a];
+        nboxes *= nb[a];
+    }
+    if (n_keys_h) *n_keys_h = nboxes;
+    if (nboxes > 0x7FFFFFFF) return DDILU_ERR_ARG;
+    if (n <= 0) return DDILU_OK;
+    tile_box_keys<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, nodes, d[0], d[1], t[0], t[1], t[2], nb[0], nb[1],
+                                                              (int)nboxes, owner, keys);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    tile_heads<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, sorted_keys, flags);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_assign(int n, const int *sorted_keys, const int *head_scan, const int *sorted_rows,
+                                 int *tile_of, int *tpos, int *tile_ptr, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    tile_assign<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, sorted_keys, head_scan, sorted_rows, tile_of, tpos,
+                                                            tile_ptr);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_edges_count(int n, const int *row_ptr, const int *col_idx, int upper, const int *tile_of,
+                                      int *cnt, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    tile_edges<false><<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, row_ptr, col_idx, upper, tile_of, cnt, nullptr,
+                                                                  nullptr);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_edges_fill(int n, const int *row_ptr, const int *col_idx, int upper, const int *tile_of,
+                                     const int *off, int *edges, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    tile_edges<true><<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, row_ptr, col_idx, upper, tile_of, nullptr, off,
+                                                                 (int2 *)edges);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* flags[0] = did the LAST of the `passes` sweeps change a level, flags[1] = cycle detected */
+extern "C" int ddilu_tile_relax(long long n_edges, const int *edges, int n_tiles, int *tlev, int *flags, int passes,
+                                void *stream) {
+    if (n_edges <= 0 || passes <= 0) {
+        DDILU_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), ST(stream)));
+        return DDILU_OK;
+    }
+    for (int p = 0; p < passes; ++p) {
+        if (p == passes - 1) DDILU_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), ST(stream)));
+        tile_relax<<<stream_grid(n_edges, 256), 256, 0, ST(stream)>>>(n_edges, (const int2 *)edges, n_tiles, tlev,
+                                                                     flags);
+    }
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_ptr, const int *trows,
+                                const int *tile_of, const int *tpos, const int *row_ptr, const int *col_idx,
+                                const double *values, const int *glev, int upper, int has_diag, int *blk16, int *stats,
+                                unsigned char *blob, void *stream) {
+    if (n_tiles <= 0) return DDILU_OK;
+    if (fill)
+        tile_build<true><<<n_tiles, TILE_MAX_ROWS, 0, ST(stream)>>>(n_tiles, tsched, tile_ptr, trows, tile_of, tpos,
+                                                                   row_ptr, col_idx, values, glev, upper, has_diag,
+                                                                   blk16, stats, blob);
+    else
+        tile_build<false><<<n_tiles, TILE_MAX_ROWS, 0, ST(stream)>>>(n_tiles, tsched, tile_ptr, trows, tile_of, tpos,
+                                                                    row_ptr, col_idx, values, glev, upper, has_diag,
+                                                                    blk16, stats, blob);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax) {
+    return (long long)TILE_NBUF * stat_max + 16LL * tmax + 16LL * (tmax + emax) + (long long)sizeof(TileCtl) + 128;
+}
+
+extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max,
+                                  int tmax, int emax, int has_diag, const double *b, double *x, void *stream) {
+    cudaStream_t st = ST(stream);
+    if (n <= 0 || n_tiles <= 0) return DDILU_OK;
+    if (x == b || (stat_max & 15)) return DDILU_ERR_ARG;
+    const size_t smem = (size_t)ddilu_tiled_smem_bytes(stat_max, tmax, emax);
+    const int threads = TILE_HELPERS + g_tiled.compute_threads;
+    void *fn = has_diag ? (void *)sptrsv_tiled<true> : (void *)sptrsv_tiled<false>;
+    // occupancy of (kernel, threads, smem) is looked up once per configuration
+    struct Cfg { size_t smem; int threads, occ; };
+    static Cfg cache[2] = {{0, 0, 0}, {0, 0, 0}};
+    Cfg &cf = cache[has_diag ? 1 : 0];
+    if (cf.smem != smem || cf.threads != threads) {
+        DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int o = 0;
+        DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+        cf.smem = smem;
+        cf.threads = threads;
+        cf.occ = o;
+    }
+    int occ = cf.occ;
+    if (occ < 1) return DDILU_ERR_ARG;
+    if (g_tiled.ctas_per_sm > 0 && occ > g_tiled.ctas_per_sm) occ = g_tiled.ctas_per_sm;
+    long long grid = (long long)occ * device_info().sm_count;
+    if (grid > n_tiles) grid = n_tiles;
+    DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
+    int store_mode = g_tiled.store_mode;
+    void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &tmax, &emax, &store_mode, &b, &x};
+    DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, threads, args, smem, st));
+    return DDILU_OK;
+}

@@ -159,12 +159,19 @@ class Sell:
     gfar2: torch.Tensor | None = None   # two levels further back
 
 
-def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
+def levels(t: DeviceCsr, upper: bool):
+    """(lev int32[n], n_levels): lev[i] = 1 + max lev[j] over the dependencies of row i."""
     n = t.n_rows
     lev = empty_i32(max(n, 1))
     mx = zeros_i32(1)
     call("ddilu_levels", n, t.rp, t.ci, int(upper), lev, mx)
-    n_levels = int(mx.item()) + 1 if n else 0
+    return lev, (int(mx.item()) + 1 if n else 0)
+
+
+def build_schedule(t: DeviceCsr, upper: bool, lev=None, n_levels: int = 0) -> Schedule:
+    n = t.n_rows
+    if lev is None:
+        lev, n_levels = levels(t, upper)
     if n == 0:
         z = zeros_i32(1)
         return Schedule(0, 0, 0, z, z, z, z)
@@ -180,6 +187,133 @@ def build_schedule(t: DeviceCsr, upper: bool) -> Schedule:
 
 class TriSolveError(ZeroDivisionError):
     pass
+
+
+# ---------------------------------------------------------------------------
+# tiled triangular solve (csrc/tiled.cu)
+
+USE_TILED = True
+TILE_MAX_ROWS = 1024
+TILE_SMEM_LIMIT = 112 * 1024      # per CTA: at least two CTAs per SM
+TILE_RELAX_BATCH = 8
+TILE_RELAX_MAX_BATCHES = 64
+
+
+@dataclass
+class TilePartition:
+    """Rows of a factor clustered into tiles (shared by the L and U solve of a factor pair)."""
+
+    n: int
+    n_tiles: int
+    tile_of: torch.Tensor     # int32[n]
+    tpos: torch.Tensor        # int32[n] position of the row in trows
+    tile_ptr: torch.Tensor    # int32[n_tiles + 1]
+    trows: torch.Tensor       # int32[n] rows grouped by tile, ascending inside a tile
+    max_rows: int
+
+
+@dataclass
+class TileSched:
+    """Static blocks of a tiled factor in tile-schedule order."""
+
+    n: int
+    n_tiles: int
+    n_tile_levels: int
+    blk_off16: torch.Tensor   # int32[n_tiles + 1], 16-byte units into blob
+    blob: torch.Tensor        # uint8
+    stat_max: int
+    tmax: int
+    emax: int
+    has_diag: bool
+    bad_row: int
+
+
+def box_tile_keys(nodes: torch.Tensor | None, n: int, dims, tdims, owner: torch.Tensor | None):
+    """(keys int32[n], keys per owner): key = box of the grid node (+ owner * boxes)."""
+    nd = len(dims)
+    arr = ctypes.c_int * nd
+    d, t = arr(*[int(v) for v in dims]), arr(*[int(v) for v in tdims])
+    nk = ctypes.c_longlong(0)
+    keys = empty_i32(max(1, n))
+    call("ddilu_tile_box_keys", int(n), nodes, nd, ctypes.addressof(d), ctypes.addressof(t), owner, keys,
+         ctypes.addressof(nk))
+    return keys[:n], int(nk.value)
+
+
+def tile_partition(keys: torch.Tensor, key_range: int) -> TilePartition | None:
+    """Compact the keys into tile ids; None if a tile would exceed TILE_MAX_ROWS."""
+    n = keys.numel()
+    if n == 0:
+        return None
+    keys = keys.clone()
+    rows = torch.arange(n, dtype=I32, device=dev())
+    sort_pairs_(keys, rows, max(1, int(key_range - 1).bit_length()))
+    flags = empty_i32(n + 1)
+    call("ddilu_tile_heads", n, keys, flags)
+    exclusive_scan_(flags, n)
+    n_tiles = int(flags[-1].item())
+    tile_of, tpos, tile_ptr = empty_i32(n), empty_i32(n), empty_i32(n_tiles + 1)
+    call("ddilu_tile_assign", n, keys, flags, rows, tile_of, tpos, tile_ptr)
+    max_rows = int((tile_ptr[1:] - tile_ptr[:-1]).max().item())
+    if max_rows > TILE_MAX_ROWS:
+        return None
+    return TilePartition(n, n_tiles, tile_of, tpos, tile_ptr, rows, max_rows)
+
+
+def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: bool, unit_diag: bool) -> TileSched | None:
+    """Tile schedule + static blocks of a triangular factor; None when the tile
+    graph is cyclic / too deep or a tile does not fit the shared-memory budget
+    (the caller then uses the sync-free solve)."""
+    n = t.n_rows
+    if part is None or n == 0 or part.n != n:
+        return None
+    cnt = zeros_i32(n + 1)
+    call("ddilu_tile_edges_count", n, t.rp, t.ci, int(upper), part.tile_of, cnt)
+    exclusive_scan_(cnt, n)
+    n_edges = int(cnt[-1].item())
+    edges = empty_i32(max(2, 2 * n_edges))
+    call("ddilu_tile_edges_fill", n, t.rp, t.ci, int(upper), part.tile_of, cnt, edges)
+    nt = part.n_tiles
+    tlev = zeros_i32(nt)
+    flags = zeros_i32(2)
+    converged = n_edges == 0
+    for _ in range(TILE_RELAX_MAX_BATCHES):
+        if converged:
+            break
+        call("ddilu_tile_relax", n_edges, edges, nt, tlev, flags, TILE_RELAX_BATCH)
+        f = flags.cpu().numpy()
+        if f[1]:
+            return None
+        converged = not f[0]
+    if not converged:
+        return None
+    del edges
+    n_tile_levels = int(tlev.max().item()) + 1
+    tsched = torch.arange(nt, dtype=I32, device=dev())
+    sort_pairs_(tlev, tsched, max(1, int(n_tile_levels - 1).bit_length()))
+    has_diag = not unit_diag
+    blk = zeros_i32(nt + 1)
+    stats = torch.tensor([0, 0, 0, INT_MAX], dtype=I32, device=dev())
+    args = (nt, tsched, part.tile_ptr, part.trows, part.tile_of, part.tpos, t.rp, t.ci, t.val, lev, int(upper),
+            int(has_diag))
+    call("ddilu_tile_build", 0, *args, blk, stats, None)
+    tmax, emax, stat_max, _ = (int(v) for v in stats.cpu().numpy())
+    if tmax + emax >= 0xFFFF or query("ddilu_tiled_smem_bytes", stat_max, tmax, emax) > TILE_SMEM_LIMIT:
+        return None
+    exclusive_scan_(blk, nt)
+    total16 = int(blk[-1].item())
+    blob = torch.empty(max(16, 16 * total16), dtype=torch.uint8, device=dev())
+    call("ddilu_tile_build", 1, *args, blk, stats, blob)
+    bad = int(stats[3].item())
+    return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, has_diag, bad)
+
+
+def sptrsv_tiled(ts: TileSched, b: torch.Tensor, out: torch.Tensor, check: bool = False):
+    if check and ts.bad_row != INT_MAX:
+        raise TriSolveError(f"zero or missing diagonal at row {ts.bad_row}")
+    call("ddilu_sptrsv_tiled", ts.n, ts.n_tiles, ts.blk_off16, ts.blob, ts.stat_max, ts.tmax, ts.emax,
+         int(ts.has_diag), b, out)
+    return out
 
 
 USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)

@@ -80,40 +80,59 @@ class DevFactors:
     def __init__(self, lower: D.DeviceCsr, upper: D.DeviceCsr, sched_l: D.Schedule | None = None):
         self.lower, self.upper = lower, upper
         self._sl, self._su = sched_l, None
+        self._levs = {}            # upper? -> (lev, n_levels), shared by the tiled and the sync-free layouts
+        if sched_l is not None:
+            self._levs[False] = (sched_l.lev, sched_l.n_levels)
+        self._tl = self._tu = None  # tiled layouts (D.TileSched) when the factor tiles
         self._tmp = None
 
     @property
     def n(self):
         return self.lower.n_rows
 
+    def _lev(self, upper: bool):
+        if upper not in self._levs:
+            self._levs[upper] = D.levels(self.upper if upper else self.lower, upper)
+        return self._levs[upper]
+
     @property
     def sched_l(self) -> D.Schedule:
         if self._sl is None:
-            self._sl = D.build_schedule(self.lower, False)
+            self._sl = D.build_schedule(self.lower, False, *self._lev(False))
         return self._sl
 
     @property
     def sched_u(self) -> D.Schedule:
         if self._su is None:
-            self._su = D.build_schedule(self.upper, True)
+            self._su = D.build_schedule(self.upper, True, *self._lev(True))
         return self._su
 
-    def prepare(self, seg_ptr=None):
-        """Build both schedules and their solve layouts now (inside setup).  seg_ptr:
-        row ranges of independent diagonal blocks (one per subdomain), if known."""
-        local = False
-        if seg_ptr is not None:
-            local = D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
-        D.get_sell(self.lower, self.sched_l, False, True)
-        D.get_sell(self.upper, self.sched_u, True, False)
+    def prepare(self, seg_ptr=None, part: "D.TilePartition | None" = None):
+        """Build the solve layouts now (inside setup).  part: tile partition of the
+        rows (structured problems) -> tiled solve, with the sync-free SELL solve as the
+        fallback when the tile graph is not one-way.  seg_ptr: row ranges of independent
+        diagonal blocks (one per subdomain), if known."""
+        if part is not None and D.USE_TILED and self.n:
+            self._tl = D.build_tiles(self.lower, self._lev(False)[0], part, False, True)
+            self._tu = D.build_tiles(self.upper, self._lev(True)[0], part, True, False)
+        if seg_ptr is not None and (self._tl is None or self._tu is None):
+            D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
+        if self._tl is None:
+            D.get_sell(self.lower, self.sched_l, False, True)
+        if self._tu is None:
+            D.get_sell(self.upper, self.sched_u, True, False)
         if self._tmp is None:
             self._tmp = D.empty_f64(max(self.n, 1))
         return self
 
     def lower_solve(self, b, out):
+        if self._tl is not None:
+            return D.sptrsv_tiled(self._tl, b, out)
         return D.sptrsv(self.lower, self.sched_l, b, out, False, True)
 
     def upper_solve(self, b, out):
+        if self._tu is not None:
+            return D.sptrsv_tiled(self._tu, b, out)
         return D.sptrsv(self.upper, self.sched_u, b, out, True, False)
 
     def solve(self, b, out):

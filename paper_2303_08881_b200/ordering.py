@@ -53,11 +53,17 @@ class _Owner(np.ndarray):
     """int64 owner array that remembers its device copy (avoids a re-upload)."""
 
     _dev = None
+    grid_hint = None   # dims of the structured grid the owner map was cut from (tiles the solves)
+
+    def __array_finalize__(self, obj):
+        if obj is not None:
+            self.grid_hint = getattr(obj, "grid_hint", None)
 
 
-def _wrap_owner(host: np.ndarray, dev_t: torch.Tensor) -> np.ndarray:
+def _wrap_owner(host: np.ndarray, dev_t: torch.Tensor | None, grid_hint=None) -> np.ndarray:
     out = host.view(_Owner)
     out._dev = dev_t
+    out.grid_hint = tuple(int(d) for d in grid_hint) if grid_hint is not None else None
     return out
 
 
@@ -78,11 +84,14 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
     if p > n:
         raise ValueError(f"more domains ({p}) than nodes ({n})")
     if p == 1:
-        return np.zeros(n, dtype=np.int64)
+        hint = grid_hint if grid_hint is not None and int(np.prod(grid_hint)) == n and len(grid_hint) <= 3 else None
+        return _wrap_owner(np.zeros(n, dtype=np.int64), None, hint)
+    hint = None
     if grid_hint is not None:
         dims = tuple(int(d) for d in grid_hint)
         if int(np.prod(dims)) != n:
             raise ValueError("grid hint does not match matrix size")
+        hint = dims if len(dims) <= 3 else None
         if len(dims) <= 3:
             factors = _box_factors(dims, p)
             sizes = np.ones(1, dtype=np.int64)
@@ -91,7 +100,7 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
                 sizes = np.outer(chunk, sizes).ravel()
             if np.max(np.abs(sizes - n / p)) <= max(1.0, 0.1 * n / p):
                 owner_d = D.box_owner(n, dims, factors)
-                return _wrap_owner(D.to_host_i64(owner_d), owner_d)
+                return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint)
     # unstructured fallback (ordering.py:192-198): greedy breadth-first growth over the symmetrised pattern
     base, rem = divmod(n, p)
     sizes = np.full(p, base, dtype=np.int32)
@@ -100,14 +109,16 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
     owner_d = D.empty_i32(n)
     work = D.empty_i32(2 * n)
     D.call("ddilu_grow_regions", n, adj.rp, adj.ci, p, torch.from_numpy(sizes).to(D.dev()), owner_d, work)
-    return _wrap_owner(D.to_host_i64(owner_d), owner_d)
+    return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint)
 
 
 class DomainLayout:
     """ordering.py:223-250; host arrays are materialised lazily from the device."""
 
-    def __init__(self, n, p, owner, gorder_d, exterior_d, owner_d, interior_starts, exterior_starts):
+    def __init__(self, n, p, owner, gorder_d, exterior_d, owner_d, interior_starts, exterior_starts,
+                 grid_hint=None):
         self.n, self.p = int(n), int(p)
+        self.grid_hint = grid_hint       # natural-order grid dims (x fastest) if the matrix is structured
         self.owner = owner
         self.interior_starts = interior_starts
         self.exterior_starts = exterior_starts
@@ -147,9 +158,17 @@ class DomainLayout:
         return np.concatenate([self.interior_of[d], self.exterior_of[d]])
 
 
-def classify_and_order(a: CsrMatrix, owner, p: int | None = None) -> DomainLayout:
-    """ordering.py:253-297."""
+def classify_and_order(a: CsrMatrix, owner, p: int | None = None, grid_hint=None) -> DomainLayout:
+    """ordering.py:253-297.  grid_hint (extension): dims of the structured grid in natural
+    order; an owner array made by `partition(a, p, grid_hint)` carries it already.  It only
+    selects the tiled triangular solves, results do not depend on it."""
     n = a.n_rows
+    if grid_hint is None:
+        grid_hint = getattr(owner, "grid_hint", None)
+    if grid_hint is not None:
+        grid_hint = tuple(int(d) for d in grid_hint)
+        if int(np.prod(grid_hint)) != n or len(grid_hint) > 3:
+            grid_hint = None
     owner_h = np.asarray(owner, dtype=np.int64) if not isinstance(owner, _Owner) else owner
     if owner_h.shape != (n,):
         raise ValueError("owner array has wrong length")
@@ -169,7 +188,7 @@ def classify_and_order(a: CsrMatrix, owner, p: int | None = None) -> DomainLayou
     b = D.to_host_i64(bounds)
     interior_starts = b[: p + 1].copy()
     exterior_starts = b[p:] - b[p]
-    return DomainLayout(n, p, owner_h, vals[:n], ext, owner_d, interior_starts, exterior_starts)
+    return DomainLayout(n, p, owner_h, vals[:n], ext, owner_d, interior_starts, exterior_starts, grid_hint)
 
 
 def rcm(a: CsrMatrix) -> Permutation:

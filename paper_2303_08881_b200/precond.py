@@ -90,6 +90,52 @@ class LocalSystem:
         self._colmap = colmap
         self._sendbuf = D.empty_f64(max(1, sum(self.send_counts)))
         self._xbuf = None
+        self._tile_parts = {}
+        self._ext_tdims = None
+
+    # ------------------------------------------------------------------ tiles
+    TILE_TARGET_ROWS = 512
+
+    def _tile_keys(self, r0: int, r1: int, tdims):
+        lay = self.layout
+        owner = lay._owner_d if lay.p > 1 else None
+        return D.box_tile_keys(self.nodes[r0:r1], r1 - r0, lay.grid_hint, tdims, owner)
+
+    def tile_part(self, which: str):
+        """Tile partition of the local rows for the tiled triangular solves: box tiles of
+        the structured grid (`layout.grid_hint`), None for unstructured matrices.
+        which: 'int' (interior rows), 'ext' (interface rows), 'all' (both, interior first)."""
+        lay = self.layout
+        if not D.USE_TILED or lay.grid_hint is None:
+            return None
+        if which in self._tile_parts:
+            return self._tile_parts[which]
+        nd = len(lay.grid_hint)
+        p = max(1, lay.p)
+        part = None
+        if which == "int" and self.n_int:
+            e = {3: 8, 2: 16, 1: self.TILE_TARGET_ROWS}[nd]
+            tdims = [2 * e if (nd == 2 and a == 0) else e for a in range(nd)]
+            keys, nk = self._tile_keys(0, self.n_int, tdims)
+            part = D.tile_partition(keys, nk * p)
+        elif which == "ext" and self.n_ext:
+            e = 32 if nd == 3 else D.TILE_MAX_ROWS
+            while e >= 2 and part is None:
+                keys, nk = self._tile_keys(self.n_int, self.n_loc, [e] * nd)
+                part = D.tile_partition(keys, nk * p)
+                self._ext_tdims = [e] * nd
+                e //= 2
+        elif which == "all":
+            if self.n_ext == 0:
+                part = self.tile_part("int")
+            elif self.tile_part("int") is not None and self.tile_part("ext") is not None:
+                e = {3: 8, 2: 16, 1: self.TILE_TARGET_ROWS}[nd]
+                tdims = [2 * e if (nd == 2 and a == 0) else e for a in range(nd)]
+                ki, nki = self._tile_keys(0, self.n_int, tdims)
+                ke, nke = self._tile_keys(self.n_int, self.n_loc, self._ext_tdims)
+                part = D.tile_partition(torch.cat([ki, ke + nki * p]), (nki + nke) * p)
+        self._tile_parts[which] = part
+        return part
 
     # ------------------------------------------------------------------ halo
     def _plan_halo(self, ad, layout, colmap):
@@ -298,7 +344,7 @@ class BjIluPrecond(_DDPrecond):
             if int(missing.item()):
                 raise NotImplementedError("l1bj on a matrix with structurally missing diagonal entries")
             mat = D.DeviceCsr(mat.n_rows, mat.n_cols, mat.rp, mat.ci, vals, mat.nnz)
-        self._f = d_factorize(mat, rule).prepare()
+        self._f = d_factorize(mat, rule).prepare(part=self.system.tile_part("all"))
         self._factors = None
 
     @property
@@ -324,8 +370,8 @@ class SchurIluPrecond(_DDPrecond):
         s = self.system
         self.rule, self.inner_iters = rule, inner_iters
         self._p = d_partial_ilu(s.a_dom, s.n_int, rule, schur_drop_tol=schur_drop_tol, factor_schur=True)
-        self._p.interior.prepare()
-        self._p.schur.prepare(seg_ptr=s.ext_ptr)       # interface factors: one independent block per subdomain
+        self._p.interior.prepare(part=s.tile_part("int"))
+        self._p.schur.prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))   # interface factors: one block per subdomain
         self._coupling = s.coupling()
         ne, nh = s.n_ext, s.n_halo
         self._inner = InnerGmres(ne, inner_iters, s.comm, pad=nh)
@@ -420,7 +466,7 @@ class RapIluPrecond(_DDPrecond):
         super().__init__(a, layout, use_rcm)
         s = self.system
         self.inner_iters, self.modified = inner_iters, modified
-        plain = d_factor_level0(s.a_dom, s.n_loc).prepare()
+        plain = d_factor_level0(s.a_dom, s.n_loc).prepare(part=s.tile_part("all"))
         self._smoother = plain
         if modified:
             if vecs is None:
@@ -432,9 +478,9 @@ class RapIluPrecond(_DDPrecond):
         else:
             coarse = plain
         l_b, u_b, w, z, l_s, u_s = d_carve(coarse, s.n_int)
-        self._interior = DevFactors(l_b, u_b).prepare()
+        self._interior = DevFactors(l_b, u_b).prepare(part=s.tile_part("int"))
         self._w, self._zt = w, z
-        self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr)
+        self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))
         self._coarse_kind = coarse
         ni, ne, nh = s.n_int, s.n_ext, s.n_halo
         self._inner = InnerGmres(ne, inner_iters, s.comm)
