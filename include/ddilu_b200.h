@@ -117,6 +117,8 @@ int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *or
  *                   scanned offsets, blocks are written to blob, stats[3] = first bad pivot row
  *   sptrsv_tiled  : x = T^-1 b; one cooperative launch */
 int ddilu_tiled_set_tuning(const char *key, int value);
+/* diagnostics: 8 int64 per CTA (life, wait static/rhs, wait boundary, tile time [cycles], levels, tiles); NULL = off */
+int ddilu_tiled_set_debug(long long *device_buf);
 int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *owner,
                         int *keys, long long *n_keys_h, void *stream);
 int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream);

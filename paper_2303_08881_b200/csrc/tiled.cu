@@ -33,15 +33,15 @@ constexpr int TILE_MAX_ROWS = 1024;
 constexpr int TILE_HDR_BYTES = 64;
 constexpr int TILE_PAD = 0xFFFF;
 constexpr int TILE_NBUF = 3;
-constexpr int TILE_HELPERS = 64;   // warp 0: TMA + right-hand side, warp 1: external dependencies
+constexpr int TILE_HELPERS = 96;   // warp 0: TMA + right-hand side, warp 1: external dependencies, warp 2: x -> L2
 
 // header ints of a static block
 enum { H_T = 0, H_NLEV, H_NEXT, H_NENT, H_OFF_ROWS, H_OFF_EXT, H_OFF_PIV, H_OFF_VAL, H_OFF_CODE, H_BYTES };
 
 struct TiledTuning {
-    int compute_threads = 128;
     int ctas_per_sm = 0;  // 0: as many as fit
-    int store_mode = 0;   // how a finished row is published to L2: 0 st.volatile, 1 st.relaxed.gpu, 2 plain st
+    int grid_cap = 0;     // diagnostics: at most this many CTAs
+    long long *debug = nullptr;  // optional device buffer: 8 int64 per CTA of cycle counters (scripts/probe_tiled.py)
 };
 static TiledTuning g_tiled;
 
@@ -342,22 +342,54 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
-__device__ __forceinline__ void compute_barrier(int threads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+constexpr int TILE_NW = 4;   // compute warps
+__device__ __forceinline__ void level_arrive(int l, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(1 + (l & (TILE_NW - 1))), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void level_sync(int l, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (l & (TILE_NW - 1))), "r"(threads) : "memory");
 }
 
 struct TileCtl {
     uint64_t mbar[TILE_NBUF];
     unsigned long long ext_prog[2];   // (tile ordinal << 32) | externals delivered
     int b_ready[2];                   // tile ordinal + 1 whose right-hand side sits in bs[buf]
+    unsigned long long lvl_done[2];   // (tile ordinal << 32) | levels complete, for the writer warp
     int comp_done;                    // tiles finished by the compute warps
-    int pad;
+    int wr_done;                      // tiles whose x the writer warp has stored
 };
 
+constexpr int TILE_PRE = 4;   // entries of a row held in registers one level ahead
+
+struct TilePre {
+    int s;      // slot, -1: this thread has no row in the level
+    int c[TILE_PRE];
+    double a[TILE_PRE];
+    double rhs, piv;
+};
+
+// p: position of this thread's row inside the level (width w)
 template <bool HAS_DIAG>
-__global__ void __launch_bounds__(TILE_HELPERS + 256)
+__device__ __forceinline__ void tile_pre_load(TilePre &r, const int4 d, int w, int ctid, const double *bsk,
+                                              const double *piv, const int *rows, const unsigned short *codes,
+                                              const double *vals) {
+    const bool act = ctid < w;
+    const int s = d.x + ctid;
+    r.s = act ? s : -1;
+    r.rhs = act ? bsk[s] : 0.0;
+    r.piv = (HAS_DIAG && act) ? piv[s] : 1.0;
+#pragma unroll
+    for (int u = 0; u < TILE_PRE; ++u) {
+        const bool in = act && u < d.z;
+        r.c[u] = in ? (int)codes[d.y + u * w + ctid] : TILE_PAD;
+        r.a[u] = in ? vals[d.y + u * w + ctid] : 0.0;
+    }
+}
+
+template <bool HAS_DIAG>
+__global__ void __launch_bounds__(TILE_HELPERS + TILE_NW * 32)
 sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
-             int tmax, int emax, int store_mode, const double *__restrict__ b, double *x) {
+             int tmax, int emax, long long *dbg, const double *__restrict__ b, double *x) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *stat = smem;
     double *bs = (double *)(smem + (size_t)TILE_NBUF * stat_max);
@@ -372,10 +404,13 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         ctl->ext_prog[0] = ctl->ext_prog[1] = 0ULL;
         ctl->b_ready[0] = ctl->b_ready[1] = 0;
         ctl->comp_done = 0;
+        ctl->wr_done = 0;
+        ctl->lvl_done[0] = ctl->lvl_done[1] = 0ULL;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     volatile int *comp_done = &ctl->comp_done;
+    volatile int *wr_done = &ctl->wr_done;
 
     if (warp == 0) {
         // ---------------- feeder: TMA of the static blocks + right-hand side gather
@@ -390,7 +425,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         if (lane == 0 && nk > 0) issue(0);
         for (int k = 0; k < nk; ++k) {
             if (k >= 2)
-                while (*comp_done < k - 1) {
+                while (*comp_done < k - 1 || *wr_done < k - 1) {
                 }
             if (lane == 0 && k + 1 < nk) issue(k + 1);
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
@@ -420,7 +455,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         // ---------------- poller: boundary dependencies, in the order the levels need them
         for (int k = 0; k < nk; ++k) {
             if (k >= 2)
-                while (*comp_done < k - 1) {
+                while (*comp_done < k - 1 || *wr_done < k - 1) {
                 }
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
@@ -455,17 +490,56 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 }
             }
         }
-    } else {
-        // ---------------- compute warps
-        const int ctid = tid - TILE_HELPERS, NC = blockDim.x - TILE_HELPERS;
+    } else if (warp == 2) {
+        // ---------------- writer: publishes finished levels to L2 so that the compute warps never wait
+        // for a global store (a barrier arrive after st.global costs an L2 round trip: scripts/probe_lat.cu)
         for (int k = 0; k < nk; ++k) {
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) {
-            }
-            __threadfence_block();
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
-            const int T = hdr[H_T], n_lev = hdr[H_NLEV];
+            const int n_lev = hdr[H_NLEV];
+            const int4 *lvl = (const int4 *)(blk + TILE_HDR_BYTES);
+            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+            const double *xsk = xs + (size_t)(k & 1) * xstride;
+            volatile unsigned long long *ld = &ctl->lvl_done[k & 1];
+            int seen = 0;
+            while (seen < n_lev) {
+                const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)(seen + 1);
+                unsigned long long got;
+                do got = *ld; while (got < want);
+                asm volatile("" ::: "memory");
+                const int upto = (int)(got & 0xffffffffULL);
+                const int s1 = lvl[upto].x;
+                for (int s = lvl[seen].x + lane; s < s1; s += 32) st_l2(x + rows[s], xsk[s]);
+                seen = upto;
+            }
+            __syncwarp();
+            if (lane == 0) *wr_done = k + 1;
+        }
+    } else {
+        // ---------------- compute warps
+        // Level l of a tile is cut into chunks of 32 rows; chunk c goes to compute warp (l + c) mod 4.
+        // Every level has a chunk 0, so a warp works at least every 4th level and is otherwise free
+        // to prefetch its next chunk (TilePre) while the other warps compute.  Barrier B_l (hardware
+        // id 1 + l mod 4) completes when every warp has passed level l: a warp ARRIVES (non-blocking)
+        // at the levels it skips and SYNCS only on the level right before its next chunk, so the
+        // per-level critical path is  wake-up -> x loads -> multiply/subtract chain -> store -> arrive.
+        const int cw = warp - TILE_HELPERS / 32;
+        constexpr int NC = TILE_NW * 32;
+        long long t_start = 0, t_wait_tile = 0, t_wait_ext = 0, t_levels = 0, n_lv = 0, seg0 = 0, seg1 = 0, seg2 = 0, ta = 0;
+        if (dbg) t_start = clock64();
+        for (int k = 0; k < nk; ++k) {
+            long long t0 = 0;
+            if (dbg) t0 = clock64();
+            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
+            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1 || *wr_done < k - 1) {
+            }
+            asm volatile("" ::: "memory");
+            if (dbg) t_wait_tile += clock64() - t0;
+            volatile unsigned long long *lvl_done = &ctl->lvl_done[k & 1];
+            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
+            const int *hdr = (const int *)blk;
+            const int n_lev = hdr[H_NLEV];
             const int4 *lvl = (const int4 *)(blk + TILE_HDR_BYTES);
             const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
             const double *piv = (const double *)(blk + hdr[H_OFF_PIV]);
@@ -475,19 +549,69 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             double *xsk = xs + (size_t)(k & 1) * xstride;
             volatile unsigned long long *prog = &ctl->ext_prog[k & 1];
             int have = 0;
-            (void)T;
-            int4 d = lvl[0];
-            for (int l = 0; l < n_lev; ++l) {
-                const int4 dn = lvl[l + 1];
-                const int w = dn.x - d.x;
+            // first level >= l in which this warp owns a chunk (n_lev if none); chunk index -> c_out
+            auto next_work = [&](int l, int &c_out) {
+                for (; l < n_lev; ++l) {
+                    const int c = (cw - l) & (TILE_NW - 1);
+                    if (c * 32 < lvl[l + 1].x - lvl[l].x) {
+                        c_out = c;
+                        break;
+                    }
+                }
+                return l;
+            };
+            int chunk = 0, nchunk = 0;
+            int cur = next_work(0, chunk);
+            // levels before my first chunk: arrive at once (B_{cur-1} is my sync)
+            for (int l = 0; l <= (cur < n_lev ? cur - 2 : n_lev - 1); ++l) level_arrive(l, NC);
+            int nxt = cur < n_lev ? next_work(cur + 1, nchunk) : n_lev;
+            TilePre pre;
+            int4 d = lvl[cur < n_lev ? cur : 0];
+            int w = lvl[(cur < n_lev ? cur : 0) + 1].x - d.x;
+            if (cur < n_lev) tile_pre_load<HAS_DIAG>(pre, d, w, chunk * 32 + lane, bsk, piv, rows, codes, vals);
+            while (cur < n_lev) {
+                if (dbg) ta = clock64();
+                if (cur >= 1) {
+                    level_sync(cur - 1, NC);
+                    if (chunk == 0 && lane == 0) *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)cur;
+                }
                 if (d.w > have) {
+                    long long t1 = 0;
+                    if (dbg) t1 = clock64();
                     const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)d.w;
                     unsigned long long got;
                     do got = *prog; while (got < want);
                     have = (int)(got & 0xffffffffULL);
-                    __threadfence_block();
+                    asm volatile("" ::: "memory");   // shared-memory loads of a thread stay in order
+                    if (dbg) t_wait_ext += clock64() - t1;
                 }
-                for (int p = ctid; p < w; p += NC) {
+                if (pre.s >= 0) {
+                    double xv[TILE_PRE];
+#pragma unroll
+                    for (int u = 0; u < TILE_PRE; ++u) xv[u] = pre.c[u] != TILE_PAD ? xsk[pre.c[u]] : 0.0;
+                    double sum = pre.rhs;
+#pragma unroll
+                    for (int u = 0; u < TILE_PRE; ++u)
+                        if (pre.c[u] != TILE_PAD) sum -= pre.a[u] * xv[u];
+                    if (d.z > TILE_PRE) {   // long rows: the remaining entries straight from the static block
+                        const unsigned short *cp = codes + d.y + (pre.s - d.x);
+                        const double *vp = vals + d.y + (pre.s - d.x);
+                        for (int kk = TILE_PRE; kk < d.z; ++kk) {
+                            const int c = cp[kk * w];
+                            if (c != TILE_PAD) sum -= vp[kk * w] * xsk[c];
+                        }
+                    }
+                    if (HAS_DIAG) sum = sum / pre.piv;
+                    sum = scrub_sentinel(sum);
+                    if (dbg) {
+                        asm volatile("" ::"d"(sum));
+                        const long long tb = clock64();
+                        seg0 += tb - ta;
+                        ta = tb;
+                    }
+                    xsk[pre.s] = sum;
+                }
+                for (int p = (chunk + TILE_NW) * 32 + lane; p < w; p += NC) {   // levels wider than 128 rows
                     const int s = d.x + p;
                     double sum = bsk[s];
                     const unsigned short *cp = codes + d.y + p;
@@ -499,18 +623,49 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                     if (HAS_DIAG) sum = sum / piv[s];
                     sum = scrub_sentinel(sum);
                     xsk[s] = sum;
-                    if (store_mode == 0) st_l2(x + rows[s], sum);
-                    else if (store_mode == 1) st_gpu(x + rows[s], sum);
-                    else x[rows[s]] = sum;
                 }
-                compute_barrier(NC);
-                d = dn;
+                // release this level and every level I skip RIGHT AWAY (B_{nxt-1} is my next sync);
+                // only then the prefetch of my next chunk, off everybody's critical path
+                for (int l = cur; l <= (nxt < n_lev ? nxt - 2 : n_lev - 1); ++l) level_arrive(l, NC);
+                if (dbg) {
+                    const long long tb = clock64();
+                    seg1 += tb - ta;
+                    ta = tb;
+                }
+                cur = nxt;
+                chunk = nchunk;
+                if (cur < n_lev) {
+                    d = lvl[cur];
+                    w = lvl[cur + 1].x - d.x;
+                    tile_pre_load<HAS_DIAG>(pre, d, w, chunk * 32 + lane, bsk, piv, rows, codes, vals);
+                    nxt = next_work(cur + 1, nchunk);
+                }
+                if (dbg) {
+                    asm volatile("" ::"d"(pre.a[0]), "d"(pre.rhs), "r"(nxt));
+                    seg2 += clock64() - ta;
+                    ++n_lv;
+                }
             }
-            if (n_lev == 0) compute_barrier(NC);
-            if (ctid == 0) {
+            asm volatile("bar.sync 5, %0;" ::"r"(NC) : "memory");   // tile finished by every compute warp
+            if (cw == 0 && lane == 0) *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)n_lev;
+            if (dbg) {
+                t_levels += clock64() - t0;
+            }
+            if (cw == 0 && lane == 0) {
                 __threadfence_block();
                 *comp_done = k + 1;
             }
+        }
+        if (dbg && cw == 0 && lane == 0) {
+            long long *o = dbg + 8LL * blockIdx.x;
+            o[0] = clock64() - t_start;   // whole CTA life
+            o[1] = t_wait_tile;           // waiting for the static block / right-hand side
+            o[2] = t_wait_ext;            // waiting for boundary dependencies (at this warp's levels)
+            o[3] = t_levels;              // tile time including both waits
+            o[4] = n_lv;
+            o[5] = nk;
+            o[6] = seg0 + (seg1 << 32);   // sync + chain | store + arrives (cycles, warp 0 lane 0)
+            o[7] = seg2;                  // prefetch of the next chunk
         }
     }
 }
@@ -528,16 +683,18 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
         while (s[i] && k[i] == s[i]) ++i;
         return s[i] == 0 && k[i] == 0;
     };
-    if (eq("compute_threads")) {
-        if (value < 32 || value > 256 || (value & 31)) return DDILU_ERR_ARG;
-        g_tiled.compute_threads = value;
-    } else if (eq("ctas_per_sm")) {
+    if (eq("ctas_per_sm")) {
         g_tiled.ctas_per_sm = value;
-    } else if (eq("store_mode")) {
-        g_tiled.store_mode = value;
+    } else if (eq("grid_cap")) {
+        g_tiled.grid_cap = value;
     } else {
         return DDILU_ERR_ARG;
     }
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tiled_set_debug(long long *device_buf) {
+    g_tiled.debug = device_buf;
     return DDILU_OK;
 }
 
@@ -640,7 +797,7 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
     if (n <= 0 || n_tiles <= 0) return DDILU_OK;
     if (x == b || (stat_max & 15)) return DDILU_ERR_ARG;
     const size_t smem = (size_t)ddilu_tiled_smem_bytes(stat_max, tmax, emax);
-    const int threads = TILE_HELPERS + g_tiled.compute_threads;
+    const int threads = TILE_HELPERS + TILE_NW * 32;
     void *fn = has_diag ? (void *)sptrsv_tiled<true> : (void *)sptrsv_tiled<false>;
     // occupancy of (kernel, threads, smem) is looked up once per configuration
     struct Cfg { size_t smem; int threads, occ; };
@@ -659,9 +816,10 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
     if (g_tiled.ctas_per_sm > 0 && occ > g_tiled.ctas_per_sm) occ = g_tiled.ctas_per_sm;
     long long grid = (long long)occ * device_info().sm_count;
     if (grid > n_tiles) grid = n_tiles;
+    if (g_tiled.grid_cap > 0 && grid > g_tiled.grid_cap) grid = g_tiled.grid_cap;
     DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
-    int store_mode = g_tiled.store_mode;
-    void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &tmax, &emax, &store_mode, &b, &x};
+    long long *dbg = g_tiled.debug;
+    void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &tmax, &emax, &dbg, &b, &x};
     DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, threads, args, smem, st));
     return DDILU_OK;
 }

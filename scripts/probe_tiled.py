@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/probe_tiled.jsonl")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--no-sell", action="store_true")
+    ap.add_argument("--grid-cap", type=int, default=0)
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
@@ -53,6 +54,7 @@ def main():
         out.write(json.dumps(kw) + "\n")
         out.flush()
 
+    query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
     dims = (args.n,) * 3
     a = P.aniso3d(*dims)
     a.device()
@@ -83,19 +85,34 @@ def main():
                 rec.update(tiles=ts.n_tiles, tile_levels=ts.n_tile_levels, tmax=ts.tmax, emax=ts.emax,
                            stat_max=ts.stat_max, blob_bytes=int(ts.blob.numel()),
                            smem=int(query("ddilu_tiled_smem_bytes", ts.stat_max, ts.tmax, ts.emax)))
-                cfgs = [(128, 0, 0)]
+                cfgs = [(128, 0)]
                 if args.sweep:
-                    cfgs = [(128, 0, sm) for sm in (0, 1, 2)] + [(c, k, 2) for c in (64, 256) for k in (0, 1, 2)]
-                for ct, cps, sm in cfgs:
-                    query("ddilu_tiled_set_tuning", b"compute_threads", ct)
+                    cfgs = [(128, k) for k in (0, 1, 2)]
+                for ct, cps in cfgs:
                     query("ddilu_tiled_set_tuning", b"ctas_per_sm", cps)
-                    query("ddilu_tiled_set_tuning", b"store_mode", sm)
                     t = timed(solve_t, flush=flush)
-                    rec[f"tiled_c{ct}_k{cps}_s{sm}_us"] = round(t * 1e6, 1)
-                    rec[f"tiled_c{ct}_k{cps}_s{sm}_frac"] = round(nbytes / t / 1e9 / PEAK, 4)
-                query("ddilu_tiled_set_tuning", b"compute_threads", 128)
+                    rec[f"tiled_c{ct}_k{cps}_us"] = round(t * 1e6, 1)
+                    rec[f"tiled_c{ct}_k{cps}_frac"] = round(nbytes / t / 1e9 / PEAK, 4)
                 query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
-                query("ddilu_tiled_set_tuning", b"store_mode", 0)
+            if ts is not None:
+                for cps in ((0, 1) if args.sweep else (0,)):
+                    query("ddilu_tiled_set_tuning", b"ctas_per_sm", cps)
+                    dbg = torch.zeros(8 * 148 * 8, dtype=torch.int64, device="cuda")
+                    query("ddilu_tiled_set_debug", dbg.data_ptr())
+                    solve_t()
+                    torch.cuda.synchronize()
+                    query("ddilu_tiled_set_debug", None)
+                    d = dbg.view(-1, 8).cpu().numpy()
+                    d = d[d[:, 5] > 0]
+                    rec[f"dbg_k{cps}"] = dict(
+                        ctas=int(len(d)), life_us=float(d[:, 0].mean() / 1965), wait_tile_us=float(d[:, 1].mean() / 1965),
+                        wait_ext_us=float(d[:, 2].mean() / 1965), tiles_us=float(d[:, 3].mean() / 1965),
+                        levels=float(d[:, 4].mean()), tiles=float(d[:, 5].mean()),
+                        seg0_sync_chain=float(((d[:, 6] & 0xffffffff) / np.maximum(1, d[:, 4])).mean()),
+                        seg1_store_arrive=float(((d[:, 6] >> 32) / np.maximum(1, d[:, 4])).mean()),
+                        seg2_prefetch=float((d[:, 7] / np.maximum(1, d[:, 4])).mean()),
+                        cyc_per_work=float(((d[:, 3] - d[:, 1]) / np.maximum(1, d[:, 4])).mean()))
+                query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
             if not args.no_sell:
                 sched = f.sched_l if which == "L" else f.sched_u
                 sell_t = (lambda: D.sptrsv(f.lower, sched, r, x, False, True)) if which == "L" else \
