@@ -113,7 +113,7 @@ int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *or
  *   tile_relax    : `passes` sweeps of tlev[c] = max(tlev[c], tlev[p]+1); flags[0] = last sweep
  *                   changed something, flags[1] = cycle (a level reached n_tiles)
  *   tile_build    : fill = 0: size of every tile's static block (16-byte units) -> blk16[q],
- *                   stats[0..2] = max rows, max externals, max bytes; fill = 1: blk16 holds the
+ *                   stats[0..2] = max rows, max externals, max bytes, stats[4] = longest row (kmax); fill = 1: blk16 holds the
  *                   scanned offsets, blocks are written to blob, stats[3] = first bad pivot row
  *   sptrsv_tiled  : x = T^-1 b; one cooperative launch */
 int ddilu_tiled_set_tuning(const char *key, int value);
@@ -136,7 +136,7 @@ int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_p
                      unsigned char *blob, void *stream);
 long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax);
 int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
-                       int emax, int has_diag, const double *b, double *x, void *stream);
+                       int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,

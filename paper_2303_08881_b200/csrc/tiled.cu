@@ -30,13 +30,16 @@
 namespace ddilu {
 
 constexpr int TILE_MAX_ROWS = 1024;
-constexpr int TILE_HDR_BYTES = 64;
-constexpr int TILE_PAD = 0xFFFF;
-constexpr int TILE_NBUF = 3;
+constexpr int TILE_HDR_BYTES = 96;
+constexpr int TILE_NW = 4;          // compute warps of the solve kernel (the item lists are cut for them)
+constexpr int ITEM_SYNC = 1 << 8;   // first chunk of this warp in a level >= 1: wait for the previous level
+constexpr int ITEM_PUBLISH = 1 << 9;   // chunk 0 of a level: tells the writer warp that the levels before are complete
+constexpr int TILE_NBUF = 2;
 constexpr int TILE_HELPERS = 96;   // warp 0: TMA + right-hand side, warp 1: external dependencies, warp 2: x -> L2
 
 // header ints of a static block
-enum { H_T = 0, H_NLEV, H_NEXT, H_NENT, H_OFF_ROWS, H_OFF_EXT, H_OFF_PIV, H_OFF_VAL, H_OFF_CODE, H_BYTES };
+enum { H_T = 0, H_NLEV, H_NEXT, H_NENT, H_OFF_ROWS, H_OFF_EXT, H_OFF_PIV, H_OFF_VAL, H_OFF_CODE, H_BYTES, H_OFF_ITEMS,
+       H_NITEMS = 12, H_FIRST = 16 };   // H_NITEMS..+3: items per compute warp, H_FIRST..+3: its first level
 
 struct TiledTuning {
     int ctas_per_sm = 0;  // 0: as many as fit
@@ -144,6 +147,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int *total, int *wsum) {
     return wsum[warp] + inc - v;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
 
 // One CTA (1024 threads, one per row) per tile, tiles in schedule order.
@@ -227,9 +232,25 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
     if (i < n_lev) s_lent[i] = lent_i;
     if (i == 0) s_lent[n_lev] = n_ent;
     __syncthreads();
+    // work items: level l is cut into chunks of 32 rows, chunk c belongs to compute warp (l + c) mod 4;
+    // every warp gets the ordered list of its chunks, so the solve kernel never scans level tables
+    int cntw[TILE_NW], basew[TILE_NW], totw[TILE_NW];
+#pragma unroll
+    for (int cwp = 0; cwp < TILE_NW; ++cwp) {
+        cntw[cwp] = 0;
+        if (i < n_lev) {
+            const int nch = (s_lstart[i + 1] - s_lstart[i] + 31) >> 5;
+            const int c0 = (cwp - i) & (TILE_NW - 1);
+            cntw[cwp] = c0 < nch ? (nch - c0 + TILE_NW - 1) / TILE_NW : 0;
+        }
+    }
+#pragma unroll
+    for (int cwp = 0; cwp < TILE_NW; ++cwp) basew[cwp] = block_excl_scan(cntw[cwp], &totw[cwp], s_wsum);
+    const int n_items = totw[0] + totw[1] + totw[2] + totw[3];
     // layout
-    const int off_lvl = TILE_HDR_BYTES;
-    const int off_rows = off_lvl + pad16(16 * (n_lev + 1));
+    const int off_lst = TILE_HDR_BYTES;
+    const int off_items = off_lst + pad16(4 * (n_lev + 1));
+    const int off_rows = off_items + 32 * n_items;
     const int off_ext = off_rows + pad16(4 * T);
     const int off_piv = off_ext + pad16(4 * n_ext);
     const int off_val = off_piv + (has_diag ? pad16(8 * T) : 0);
@@ -242,10 +263,19 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
             atomicMax(stats + 1, n_ext);
             atomicMax(stats + 2, bytes);
         }
+        if (i < n_lev) atomicMax(stats + 4, s_lk[i]);
         return;
     }
     unsigned char *blk = blob + 16LL * blk16[q];
     int *hdr = (int *)blk;
+    // first level with a chunk of warp cwp after level `from` (n_lev + 1 if none)
+    auto next_level_of = [&](int cwp, int from) {
+        for (int l = from; l < n_lev; ++l) {
+            const int nch = (s_lstart[l + 1] - s_lstart[l] + 31) >> 5;
+            if (((cwp - l) & (TILE_NW - 1)) < nch) return l;
+        }
+        return n_lev + 1;
+    };
     if (i < TILE_HDR_BYTES / 4) {
         int v = 0;
         switch (i) {
@@ -259,19 +289,45 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
             case H_OFF_VAL: v = off_val; break;
             case H_OFF_CODE: v = off_code; break;
             case H_BYTES: v = bytes; break;
+            case H_OFF_ITEMS: v = off_items; break;
             default: break;
         }
+        if (i >= H_NITEMS && i < H_NITEMS + TILE_NW) v = totw[i - H_NITEMS];
+        if (i >= H_FIRST && i < H_FIRST + TILE_NW) v = next_level_of(i - H_FIRST, 0);
         hdr[i] = v;
     }
-    int4 *lvl = (int4 *)(blk + off_lvl);
-    if (i <= n_lev)   // .w = externals needed by the levels up to and including l
-        lvl[i] = make_int4(s_lstart[i], s_lent[i], i < n_lev ? s_lk[i] : 0, i < n_lev ? s_eoff[s_lstart[i + 1]] : n_ext);
+    int *lst = (int *)(blk + off_lst);
+    if (i <= n_lev) lst[i] = s_lstart[i];
+    if (i < n_lev) {
+        const int l0 = s_lstart[i], wl = s_lstart[i + 1] - l0, nch = (wl + 31) >> 5;
+        const int need = s_eoff[s_lstart[i + 1]];   // externals needed by the levels up to and including this one
+        int wbase = 0;
+#pragma unroll
+        for (int cwp = 0; cwp < TILE_NW; ++cwp) {
+            int4 *it = (int4 *)(blk + off_items) + 2 * (wbase + basew[cwp]);
+            const int c0 = (cwp - i) & (TILE_NW - 1);
+            int nth = 0;
+            for (int c = c0; c < nch; c += TILE_NW, ++nth) {
+                const bool first = c == c0, last = c + TILE_NW >= nch;
+                int n_arr = 0;
+                if (last) {
+                    const int nxt = next_level_of(cwp, i + 1);
+                    n_arr = nxt > n_lev ? n_lev - i : nxt - 1 - i;
+                }
+                const int cnt = wl - c * 32 < 32 ? wl - c * 32 : 32;
+                const int flags = cnt | ((first && i >= 1) ? ITEM_SYNC : 0) | (c == 0 ? ITEM_PUBLISH : 0);
+                it[2 * nth] = make_int4(l0 + c * 32, s_lent[i] + c * 32, wl, s_lk[i]);
+                it[2 * nth + 1] = make_int4(i, need, flags, n_arr);
+            }
+            wbase += totw[cwp];
+        }
+    }
     // zero the alignment tails so the blob is fully defined
     {
-        const int tails[5][2] = {{off_rows + 4 * T, off_ext}, {off_ext + 4 * n_ext, off_piv},
-                                 {off_piv + (has_diag ? 8 * T : 0), off_val}, {off_val + 8 * n_ent, off_code},
-                                 {off_code + 2 * n_ent, bytes}};
-        if (i < 5)
+        const int tails[6][2] = {{off_lst + 4 * (n_lev + 1), off_items}, {off_rows + 4 * T, off_ext},
+                                 {off_ext + 4 * n_ext, off_piv}, {off_piv + (has_diag ? 8 * T : 0), off_val},
+                                 {off_val + 8 * n_ent, off_code}, {off_code + 2 * n_ent, bytes}};
+        if (i < 6)
             for (int p = tails[i][0]; p < tails[i][1]; ++p) blk[p] = 0;
     }
     if (!active) return;
@@ -305,8 +361,8 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
             seen = true;
         }
     }
-    for (; kk < K; ++kk) {
-        code_out[e0 + (long long)kk * w] = (unsigned short)TILE_PAD;
+    for (; kk < K; ++kk) {   // padding: coefficient 0 times the tile's zero slot (x[T + n_ext] = 0)
+        code_out[e0 + (long long)kk * w] = (unsigned short)(T + n_ext);
         val_out[e0 + (long long)kk * w] = 0.0;
     }
     if (has_diag) {
@@ -317,8 +373,6 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
 
 // ---------------------------------------------------------------------------
 // solve
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -332,6 +386,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done;
     do {
@@ -342,7 +405,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
-constexpr int TILE_NW = 4;   // compute warps
 __device__ __forceinline__ void level_arrive(int l, int threads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(1 + (l & (TILE_NW - 1))), "r"(threads) : "memory");
 }
@@ -357,45 +419,66 @@ struct TileCtl {
     unsigned long long lvl_done[2];   // (tile ordinal << 32) | levels complete, for the writer warp
     int comp_done;                    // tiles finished by the compute warps
     int wr_done;                      // tiles whose x the writer warp has stored
+    int poll_done;                    // tiles whose boundary dependencies the poller has delivered
+    int pad[3];
 };
 
-constexpr int TILE_PRE = 4;   // entries of a row held in registers one level ahead
-
-struct TilePre {
-    int s;      // slot, -1: this thread has no row in the level
-    int c[TILE_PRE];
-    double a[TILE_PRE];
+// One work item (a chunk of <= 32 rows of one level) as a compute warp holds it one item ahead:
+// everything that does not depend on x is in registers before the level's barrier opens.
+template <int KP>
+struct TileItem {
+    int level, need, flags, n_arr;   // flags: rows in the chunk | ITEM_SYNC | ITEM_PUBLISH
+    int ent0, w, K;                  // entry k of lane i: ent0 + k*w + i (long rows, k >= KP)
+    uint32_t xaddr[KP];              // shared-memory byte address of the x operand of entry k
+    uint32_t saddr;                  // where this lane's result goes
+    double a[KP];
     double rhs, piv;
 };
 
-// p: position of this thread's row inside the level (width w)
-template <bool HAS_DIAG>
-__device__ __forceinline__ void tile_pre_load(TilePre &r, const int4 d, int w, int ctid, const double *bsk,
-                                              const double *piv, const int *rows, const unsigned short *codes,
-                                              const double *vals) {
-    const bool act = ctid < w;
-    const int s = d.x + ctid;
-    r.s = act ? s : -1;
-    r.rhs = act ? bsk[s] : 0.0;
+template <bool HAS_DIAG, int KP>
+__device__ __forceinline__ void tile_item_load(TileItem<KP> &r, const int4 *it, int lane,
+                                               const double *xsk, int zslot, const double *piv,
+                                               const unsigned short *codes, const double *vals) {
+    const int4 A = it[0], B = it[1];   // A = {slot0, ent0, w, K}, B = {level, need, flags, n_arr}
+    r.level = B.x;
+    r.need = B.y;
+    r.flags = B.z;
+    r.n_arr = B.w;
+    r.ent0 = A.y;
+    r.w = A.z;
+    r.K = A.w;
+    const bool act = lane < (B.z & 0xff);
+    const int s = A.x + lane;
+    r.saddr = smem_u32(xsk + s);
+    r.rhs = act ? xsk[s] : 0.0;   // the feeder parked b[row] in the row's own x slot
     r.piv = (HAS_DIAG && act) ? piv[s] : 1.0;
 #pragma unroll
-    for (int u = 0; u < TILE_PRE; ++u) {
-        const bool in = act && u < d.z;
-        r.c[u] = in ? (int)codes[d.y + u * w + ctid] : TILE_PAD;
-        r.a[u] = in ? vals[d.y + u * w + ctid] : 0.0;
+    for (int u = 0; u < KP; ++u) {
+        const bool in = act && u < A.w;
+        const int c = in ? (int)codes[A.y + u * A.z + lane] : zslot;
+        r.a[u] = in ? vals[A.y + u * A.z + lane] : 0.0;
+        r.xaddr[u] = smem_u32(xsk + c);
     }
 }
 
-template <bool HAS_DIAG>
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+template <bool HAS_DIAG, int KP>
 __global__ void __launch_bounds__(TILE_HELPERS + TILE_NW * 32)
 sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
              int tmax, int emax, long long *dbg, const double *__restrict__ b, double *x) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *stat = smem;
-    double *bs = (double *)(smem + (size_t)TILE_NBUF * stat_max);
-    double *xs = bs + 2 * (size_t)tmax;
-    TileCtl *ctl = (TileCtl *)(xs + 2 * (size_t)(tmax + emax));
-    const int xstride = tmax + emax;
+    double *xs = (double *)(smem + (size_t)TILE_NBUF * stat_max);
+    const int xstride = tmax + emax + 2;   // + the zero slot that padded entries point to
+    TileCtl *ctl = (TileCtl *)(xs + 2 * (size_t)xstride);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int nk = (n_tiles - (int)blockIdx.x + G - 1) / G;   // my tiles: blockIdx.x + k*G
@@ -405,12 +488,14 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         ctl->b_ready[0] = ctl->b_ready[1] = 0;
         ctl->comp_done = 0;
         ctl->wr_done = 0;
+        ctl->poll_done = 0;
         ctl->lvl_done[0] = ctl->lvl_done[1] = 0ULL;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     volatile int *comp_done = &ctl->comp_done;
     volatile int *wr_done = &ctl->wr_done;
+    volatile int *poll_done = &ctl->poll_done;
 
     if (warp == 0) {
         // ---------------- feeder: TMA of the static blocks + right-hand side gather
@@ -422,34 +507,43 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             mbar_expect_tx(bar, bytes);
             bulk_g2s(stat + (size_t)(k % TILE_NBUF) * stat_max, blob + 16LL * o0, bytes, bar);
         };
-        if (lane == 0 && nk > 0) issue(0);
-        for (int k = 0; k < nk; ++k) {
-            if (k >= 2)
-                while (*comp_done < k - 1 || *wr_done < k - 1) {
-                }
-            if (lane == 0 && k + 1 < nk) issue(k + 1);
-            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
-            const int *hdr = (const int *)blk;
-            const int T = hdr[H_T];
-            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
-            double *bsk = bs + (size_t)(k & 1) * tmax;
-            for (int s0 = 0; s0 < T; s0 += 256) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int s = s0 + u * 32 + lane;
-                    v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int s = s0 + u * 32 + lane;
-                    if (s < T) bsk[s] = v[u];
-                }
+        // event loop: issue the TMA of tile `issued` as soon as its ring slot is free (the tile that used it
+        // is computed AND written back), gather the right-hand side of tile `fed` into the x buffer as soon
+        // as its static block has landed and the x buffer of tile fed-2 is free
+        int issued = 0, fed = 0;
+        while (fed < nk) {
+            if (issued < nk &&
+                (issued < TILE_NBUF || (*comp_done > issued - TILE_NBUF && *wr_done > issued - TILE_NBUF &&
+                                        *poll_done > issued - TILE_NBUF))) {
+                if (lane == 0) issue(issued);
+                ++issued;
             }
-            __syncwarp();
-            __threadfence_block();
-            if (lane == 0) *(volatile int *)&ctl->b_ready[k & 1] = k + 1;
+            if (fed < issued && (fed < 2 || (*comp_done >= fed - 1 && *wr_done >= fed - 1)) &&
+                mbar_test(&ctl->mbar[fed % TILE_NBUF], (uint32_t)((fed / TILE_NBUF) & 1))) {
+                const int k = fed;
+                const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
+                const int *hdr = (const int *)blk;
+                const int T = hdr[H_T];
+                const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+                double *xsk = xs + (size_t)(k & 1) * xstride;   // slot s holds b[row] until the row is solved
+                for (int s0 = 0; s0 < T; s0 += 256) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int s = s0 + u * 32 + lane;
+                        v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int s = s0 + u * 32 + lane;
+                        if (s < T) xsk[s] = v[u];
+                    }
+                }
+                __syncwarp();
+                __threadfence_block();
+                if (lane == 0) *(volatile int *)&ctl->b_ready[k & 1] = k + 1;
+                ++fed;
+            }
         }
     } else if (warp == 1) {
         // ---------------- poller: boundary dependencies, in the order the levels need them
@@ -489,6 +583,8 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                     }
                 }
             }
+            __syncwarp();
+            if (lane == 0) *poll_done = k + 1;
         }
     } else if (warp == 2) {
         // ---------------- writer: publishes finished levels to L2 so that the compute warps never wait
@@ -498,7 +594,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
             const int n_lev = hdr[H_NLEV];
-            const int4 *lvl = (const int4 *)(blk + TILE_HDR_BYTES);
+            const int *lst = (const int *)(blk + TILE_HDR_BYTES);
             const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
             const double *xsk = xs + (size_t)(k & 1) * xstride;
             volatile unsigned long long *ld = &ctl->lvl_done[k & 1];
@@ -509,8 +605,8 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 do got = *ld; while (got < want);
                 asm volatile("" ::: "memory");
                 const int upto = (int)(got & 0xffffffffULL);
-                const int s1 = lvl[upto].x;
-                for (int s = lvl[seen].x + lane; s < s1; s += 32) st_l2(x + rows[s], xsk[s]);
+                const int s1 = lst[upto];
+                for (int s = lst[seen] + lane; s < s1; s += 32) st_l2(x + rows[s], xsk[s]);
                 seen = upto;
             }
             __syncwarp();
@@ -526,13 +622,13 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         // per-level critical path is  wake-up -> x loads -> multiply/subtract chain -> store -> arrive.
         const int cw = warp - TILE_HELPERS / 32;
         constexpr int NC = TILE_NW * 32;
-        long long t_start = 0, t_wait_tile = 0, t_wait_ext = 0, t_levels = 0, n_lv = 0, seg0 = 0, seg1 = 0, seg2 = 0, ta = 0;
+        long long t_start = 0, t_wait_tile = 0, t_wait_ext = 0, t_levels = 0, n_lv = 0;
         if (dbg) t_start = clock64();
         for (int k = 0; k < nk; ++k) {
             long long t0 = 0;
             if (dbg) t0 = clock64();
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1 || *wr_done < k - 1) {
+            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) {
             }
             asm volatile("" ::: "memory");
             if (dbg) t_wait_tile += clock64() - t0;
@@ -540,116 +636,68 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
             const int n_lev = hdr[H_NLEV];
-            const int4 *lvl = (const int4 *)(blk + TILE_HDR_BYTES);
-            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
             const double *piv = (const double *)(blk + hdr[H_OFF_PIV]);
             const double *vals = (const double *)(blk + hdr[H_OFF_VAL]);
             const unsigned short *codes = (const unsigned short *)(blk + hdr[H_OFF_CODE]);
-            const double *bsk = bs + (size_t)(k & 1) * tmax;
             double *xsk = xs + (size_t)(k & 1) * xstride;
+            const int zslot = hdr[H_T] + hdr[H_NEXT];
             volatile unsigned long long *prog = &ctl->ext_prog[k & 1];
+            int n_it = 0, it_base = 0;
+#pragma unroll
+            for (int q = 0; q < TILE_NW; ++q) {
+                const int nq = hdr[H_NITEMS + q];
+                if (q < cw) it_base += nq;
+                if (q == cw) n_it = nq;
+            }
+            const int4 *items = (const int4 *)(blk + hdr[H_OFF_ITEMS]) + 2 * it_base;
+            const int first = hdr[H_FIRST + cw];
+            if (lane == 0) xsk[zslot] = 0.0;   // every warp writes the same value; its own reads follow in order
+            __syncwarp();
+            // levels before my first chunk (all levels if I have none): arrive at once
+            for (int l = 0; l <= (n_it ? first - 2 : n_lev - 1); ++l) level_arrive(l, NC);
+            TileItem<KP> itm;
+            if (n_it) tile_item_load<HAS_DIAG, KP>(itm, items, lane, xsk, zslot, piv, codes, vals);
             int have = 0;
-            // first level >= l in which this warp owns a chunk (n_lev if none); chunk index -> c_out
-            auto next_work = [&](int l, int &c_out) {
-                for (; l < n_lev; ++l) {
-                    const int c = (cw - l) & (TILE_NW - 1);
-                    if (c * 32 < lvl[l + 1].x - lvl[l].x) {
-                        c_out = c;
-                        break;
-                    }
-                }
-                return l;
-            };
-            int chunk = 0, nchunk = 0;
-            int cur = next_work(0, chunk);
-            // levels before my first chunk: arrive at once (B_{cur-1} is my sync)
-            for (int l = 0; l <= (cur < n_lev ? cur - 2 : n_lev - 1); ++l) level_arrive(l, NC);
-            int nxt = cur < n_lev ? next_work(cur + 1, nchunk) : n_lev;
-            TilePre pre;
-            int4 d = lvl[cur < n_lev ? cur : 0];
-            int w = lvl[(cur < n_lev ? cur : 0) + 1].x - d.x;
-            if (cur < n_lev) tile_pre_load<HAS_DIAG>(pre, d, w, chunk * 32 + lane, bsk, piv, rows, codes, vals);
-            while (cur < n_lev) {
-                if (dbg) ta = clock64();
-                if (cur >= 1) {
-                    level_sync(cur - 1, NC);
-                    if (chunk == 0 && lane == 0) *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)cur;
-                }
-                if (d.w > have) {
+            for (int q = 0; q < n_it; ++q) {
+                if (itm.flags & ITEM_SYNC) level_sync(itm.level - 1, NC);
+                if ((itm.flags & ITEM_PUBLISH) && lane == 0)
+                    *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.level;
+                if (itm.need > have) {
                     long long t1 = 0;
                     if (dbg) t1 = clock64();
-                    const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)d.w;
+                    const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.need;
                     unsigned long long got;
                     do got = *prog; while (got < want);
                     have = (int)(got & 0xffffffffULL);
-                    asm volatile("" ::: "memory");   // shared-memory loads of a thread stay in order
                     if (dbg) t_wait_ext += clock64() - t1;
                 }
-                if (pre.s >= 0) {
-                    double xv[TILE_PRE];
+                // ---- the level's critical path: x loads -> multiply/subtract chain -> store -> arrive
+                double xv[KP];
 #pragma unroll
-                    for (int u = 0; u < TILE_PRE; ++u) xv[u] = pre.c[u] != TILE_PAD ? xsk[pre.c[u]] : 0.0;
-                    double sum = pre.rhs;
+                for (int u = 0; u < KP; ++u) xv[u] = lds_f64(itm.xaddr[u]);
+                double sum = itm.rhs;
 #pragma unroll
-                    for (int u = 0; u < TILE_PRE; ++u)
-                        if (pre.c[u] != TILE_PAD) sum -= pre.a[u] * xv[u];
-                    if (d.z > TILE_PRE) {   // long rows: the remaining entries straight from the static block
-                        const unsigned short *cp = codes + d.y + (pre.s - d.x);
-                        const double *vp = vals + d.y + (pre.s - d.x);
-                        for (int kk = TILE_PRE; kk < d.z; ++kk) {
-                            const int c = cp[kk * w];
-                            if (c != TILE_PAD) sum -= vp[kk * w] * xsk[c];
-                        }
-                    }
-                    if (HAS_DIAG) sum = sum / pre.piv;
-                    sum = scrub_sentinel(sum);
-                    if (dbg) {
-                        asm volatile("" ::"d"(sum));
-                        const long long tb = clock64();
-                        seg0 += tb - ta;
-                        ta = tb;
-                    }
-                    xsk[pre.s] = sum;
+                for (int u = 0; u < KP; ++u) sum -= itm.a[u] * xv[u];
+                if (itm.K > KP) {   // long rows: the remaining entries straight from the static block
+                    const unsigned short *cp = codes + itm.ent0 + lane;
+                    const double *vp = vals + itm.ent0 + lane;
+                    if (lane < (itm.flags & 0xff))
+                        for (int kk = KP; kk < itm.K; ++kk) sum -= vp[kk * itm.w] * xsk[cp[kk * itm.w]];
                 }
-                for (int p = (chunk + TILE_NW) * 32 + lane; p < w; p += NC) {   // levels wider than 128 rows
-                    const int s = d.x + p;
-                    double sum = bsk[s];
-                    const unsigned short *cp = codes + d.y + p;
-                    const double *vp = vals + d.y + p;
-                    for (int kk = 0; kk < d.z; ++kk) {
-                        const int c = cp[kk * w];
-                        if (c != TILE_PAD) sum -= vp[kk * w] * xsk[c];
-                    }
-                    if (HAS_DIAG) sum = sum / piv[s];
-                    sum = scrub_sentinel(sum);
-                    xsk[s] = sum;
-                }
-                // release this level and every level I skip RIGHT AWAY (B_{nxt-1} is my next sync);
-                // only then the prefetch of my next chunk, off everybody's critical path
-                for (int l = cur; l <= (nxt < n_lev ? nxt - 2 : n_lev - 1); ++l) level_arrive(l, NC);
-                if (dbg) {
-                    const long long tb = clock64();
-                    seg1 += tb - ta;
-                    ta = tb;
-                }
-                cur = nxt;
-                chunk = nchunk;
-                if (cur < n_lev) {
-                    d = lvl[cur];
-                    w = lvl[cur + 1].x - d.x;
-                    tile_pre_load<HAS_DIAG>(pre, d, w, chunk * 32 + lane, bsk, piv, rows, codes, vals);
-                    nxt = next_work(cur + 1, nchunk);
-                }
-                if (dbg) {
-                    asm volatile("" ::"d"(pre.a[0]), "d"(pre.rhs), "r"(nxt));
-                    seg2 += clock64() - ta;
-                    ++n_lv;
-                }
+                if (HAS_DIAG) sum = sum / itm.piv;
+                sum = scrub_sentinel(sum);
+                if (lane < (itm.flags & 0xff)) sts_f64(itm.saddr, sum);
+                // release this level and every level I skip right away; then the next item's prefetch,
+                // off everybody's critical path
+                for (int j = 0; j < itm.n_arr; ++j) level_arrive(itm.level + j, NC);
+                if (q + 1 < n_it)
+                    tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, codes, vals);
             }
             asm volatile("bar.sync 5, %0;" ::"r"(NC) : "memory");   // tile finished by every compute warp
             if (cw == 0 && lane == 0) *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)n_lev;
             if (dbg) {
                 t_levels += clock64() - t0;
+                n_lv += n_lev;
             }
             if (cw == 0 && lane == 0) {
                 __threadfence_block();
@@ -664,8 +712,6 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             o[3] = t_levels;              // tile time including both waits
             o[4] = n_lv;
             o[5] = nk;
-            o[6] = seg0 + (seg1 << 32);   // sync + chain | store + arrives (cycles, warp 0 lane 0)
-            o[7] = seg2;                  // prefetch of the next chunk
         }
     }
 }
@@ -788,27 +834,31 @@ extern "C" int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const 
 }
 
 extern "C" long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax) {
-    return (long long)TILE_NBUF * stat_max + 16LL * tmax + 16LL * (tmax + emax) + (long long)sizeof(TileCtl) + 128;
+    return (long long)TILE_NBUF * stat_max + 16LL * (tmax + emax + 2) + (long long)sizeof(TileCtl) + 128;
 }
 
 extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max,
-                                  int tmax, int emax, int has_diag, const double *b, double *x, void *stream) {
+                                  int tmax, int emax, int kmax, int has_diag, const double *b, double *x,
+                                  void *stream) {
     cudaStream_t st = ST(stream);
     if (n <= 0 || n_tiles <= 0) return DDILU_OK;
     if (x == b || (stat_max & 15)) return DDILU_ERR_ARG;
     const size_t smem = (size_t)ddilu_tiled_smem_bytes(stat_max, tmax, emax);
     const int threads = TILE_HELPERS + TILE_NW * 32;
-    void *fn = has_diag ? (void *)sptrsv_tiled<true> : (void *)sptrsv_tiled<false>;
-    // occupancy of (kernel, threads, smem) is looked up once per configuration
-    struct Cfg { size_t smem; int threads, occ; };
-    static Cfg cache[2] = {{0, 0, 0}, {0, 0, 0}};
-    Cfg &cf = cache[has_diag ? 1 : 0];
-    if (cf.smem != smem || cf.threads != threads) {
+    // entries of a row held in registers: 3 covers 7-point factors, 6 everything else (+ a loop for the rest)
+    const int wide = kmax > 3 ? 1 : 0;
+    void *fns[2][2] = {{(void *)sptrsv_tiled<false, 3>, (void *)sptrsv_tiled<false, 6>},
+                       {(void *)sptrsv_tiled<true, 3>, (void *)sptrsv_tiled<true, 6>}};
+    void *fn = fns[has_diag ? 1 : 0][wide];
+    // occupancy of (kernel, smem) is looked up once per configuration
+    struct Cfg { size_t smem; int occ; };
+    static Cfg cache[2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+    Cfg &cf = cache[has_diag ? 1 : 0][wide];
+    if (cf.smem != smem) {
         DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int o = 0;
         DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
         cf.smem = smem;
-        cf.threads = threads;
         cf.occ = o;
     }
     int occ = cf.occ;

@@ -224,6 +224,7 @@ class TileSched:
     stat_max: int
     tmax: int
     emax: int
+    kmax: int
     has_diag: bool
     bad_row: int
 
@@ -293,25 +294,25 @@ def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: boo
     sort_pairs_(tlev, tsched, max(1, int(n_tile_levels - 1).bit_length()))
     has_diag = not unit_diag
     blk = zeros_i32(nt + 1)
-    stats = torch.tensor([0, 0, 0, INT_MAX], dtype=I32, device=dev())
+    stats = torch.tensor([0, 0, 0, INT_MAX, 0], dtype=I32, device=dev())
     args = (nt, tsched, part.tile_ptr, part.trows, part.tile_of, part.tpos, t.rp, t.ci, t.val, lev, int(upper),
             int(has_diag))
     call("ddilu_tile_build", 0, *args, blk, stats, None)
-    tmax, emax, stat_max, _ = (int(v) for v in stats.cpu().numpy())
-    if tmax + emax >= 0xFFFF or query("ddilu_tiled_smem_bytes", stat_max, tmax, emax) > TILE_SMEM_LIMIT:
+    tmax, emax, stat_max, _, kmax = (int(v) for v in stats.cpu().numpy())
+    if tmax + emax + 2 >= 0xFFFF or query("ddilu_tiled_smem_bytes", stat_max, tmax, emax) > TILE_SMEM_LIMIT:
         return None
     exclusive_scan_(blk, nt)
     total16 = int(blk[-1].item())
     blob = torch.empty(max(16, 16 * total16), dtype=torch.uint8, device=dev())
     call("ddilu_tile_build", 1, *args, blk, stats, blob)
     bad = int(stats[3].item())
-    return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, has_diag, bad)
+    return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, kmax, has_diag, bad)
 
 
 def sptrsv_tiled(ts: TileSched, b: torch.Tensor, out: torch.Tensor, check: bool = False):
     if check and ts.bad_row != INT_MAX:
         raise TriSolveError(f"zero or missing diagonal at row {ts.bad_row}")
-    call("ddilu_sptrsv_tiled", ts.n, ts.n_tiles, ts.blk_off16, ts.blob, ts.stat_max, ts.tmax, ts.emax,
+    call("ddilu_sptrsv_tiled", ts.n, ts.n_tiles, ts.blk_off16, ts.blob, ts.stat_max, ts.tmax, ts.emax, ts.kmax,
          int(ts.has_diag), b, out)
     return out
 

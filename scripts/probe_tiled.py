@@ -108,10 +108,7 @@ def main():
                         ctas=int(len(d)), life_us=float(d[:, 0].mean() / 1965), wait_tile_us=float(d[:, 1].mean() / 1965),
                         wait_ext_us=float(d[:, 2].mean() / 1965), tiles_us=float(d[:, 3].mean() / 1965),
                         levels=float(d[:, 4].mean()), tiles=float(d[:, 5].mean()),
-                        seg0_sync_chain=float(((d[:, 6] & 0xffffffff) / np.maximum(1, d[:, 4])).mean()),
-                        seg1_store_arrive=float(((d[:, 6] >> 32) / np.maximum(1, d[:, 4])).mean()),
-                        seg2_prefetch=float((d[:, 7] / np.maximum(1, d[:, 4])).mean()),
-                        cyc_per_work=float(((d[:, 3] - d[:, 1]) / np.maximum(1, d[:, 4])).mean()))
+                        cyc_per_level=float(((d[:, 3] - d[:, 1]) / np.maximum(1, d[:, 4])).mean()))
                 query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
             if not args.no_sell:
                 sched = f.sched_l if which == "L" else f.sched_u
