@@ -135,6 +135,9 @@ int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_p
                      const double *values, const int *glev, int upper, int has_diag, int *blk16, int *stats,
                      unsigned char *blob, void *stream);
 long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax);
+/* self-check of the division the U solves use (pivot reciprocal + two FMA corrections) against the
+ * IEEE division on n pseudo-random / adversarial operand pairs; *mismatch = pairs whose bits differ */
+int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigned long long *mismatch, void *stream);
 int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
                        int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 

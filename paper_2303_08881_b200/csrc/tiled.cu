@@ -149,6 +149,31 @@ __device__ __forceinline__ int block_excl_scan(int v, int *total, int *wsum) {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// s / d with the pivot's reciprocal r = RN(1/d) precomputed at setup: one multiply and two
+// remainder/correction FMA pairs instead of the ~30-instruction division routine on every level's
+// critical path.  q1 = RN(s r) is within 2 ulp of s/d, q2 is faithful, and by Markstein's theorem
+// (r correctly rounded, the remainder s - d q2 exact) the last correction rounds exactly like the
+// IEEE division, so the result has the bits of the reference's `s / d` (sparse.py:271).  Operands
+// outside a safe exponent window (zero, subnormal, huge, inf/nan: the remainder would not be exact)
+// and pivots flagged r = 0 at setup take the real division.  Verified bit-for-bit on random and
+// adversarial operands by ddilu_fastdiv_selftest (tests/test_gpu_tiled.py).
+__device__ __forceinline__ double exact_div(double s, double d, double r) {
+    const unsigned es = ((unsigned)__double2hiint(s) >> 20) & 0x7ffu;
+    if (r != 0.0 && es - 623u <= 800u) {
+        const double q1 = s * r;
+        const double e1 = __fma_rn(-d, q1, s);
+        const double q2 = __fma_rn(e1, r, q1);
+        const double e2 = __fma_rn(-d, q2, s);
+        return __fma_rn(e2, r, q2);
+    }
+    return s / d;
+}
+// reciprocal to store for a pivot, 0 = "always divide" (pivot outside the safe exponent window)
+__device__ __forceinline__ double safe_reciprocal(double d) {
+    const unsigned ed = ((unsigned)__double2hiint(d) >> 20) & 0x7ffu;
+    return (ed - 623u <= 800u) ? 1.0 / d : 0.0;
+}
+
 __device__ __forceinline__ int pad16(int bytes) { return (bytes + 15) & ~15; }
 
 // One CTA (1024 threads, one per row) per tile, tiles in schedule order.
@@ -253,7 +278,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
     const int off_rows = off_items + 32 * n_items;
     const int off_ext = off_rows + pad16(4 * T);
     const int off_piv = off_ext + pad16(4 * n_ext);
-    const int off_val = off_piv + (has_diag ? pad16(8 * T) : 0);
+    const int off_val = off_piv + (has_diag ? 16 * T : 0);   // (pivot, reciprocal) pairs
     const int off_code = off_val + pad16(8 * n_ent);
     const int bytes = off_code + pad16(2 * n_ent);
     if (!FILL) {
@@ -325,7 +350,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
     // zero the alignment tails so the blob is fully defined
     {
         const int tails[6][2] = {{off_lst + 4 * (n_lev + 1), off_items}, {off_rows + 4 * T, off_ext},
-                                 {off_ext + 4 * n_ext, off_piv}, {off_piv + (has_diag ? 8 * T : 0), off_val},
+                                 {off_ext + 4 * n_ext, off_piv}, {off_val, off_val},
                                  {off_val + 8 * n_ent, off_code}, {off_code + 2 * n_ent, bytes}};
         if (i < 6)
             for (int p = tails[i][0]; p < tails[i][1]; ++p) blk[p] = 0;
@@ -366,7 +391,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
         val_out[e0 + (long long)kk * w] = 0.0;
     }
     if (has_diag) {
-        piv_out[slot] = diag;
+        ((double2 *)piv_out)[slot] = make_double2(diag, safe_reciprocal(diag));
         if (!seen || fabs(diag) < 1e-300) atomicMin(stats + 3, row);
     }
 }
@@ -423,6 +448,51 @@ struct TileCtl {
     int pad[3];
 };
 
+__global__ void fastdiv_selftest(long long n, unsigned long long seed, unsigned long long *mismatch) {
+    unsigned long long bad = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        // splitmix64 stream per sample
+        unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * (unsigned long long)(i + 1);
+        auto next = [&]() {
+            z += 0x9E3779B97F4A7C15ULL;
+            unsigned long long x = z;
+            x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+            return x ^ (x >> 31);
+        };
+        unsigned long long ms = next(), md = next(), m = next();
+        // exponents: mostly near 1, sometimes anywhere (incl. subnormal / inf / nan), sometimes at the window edges
+        auto expo = [&](unsigned long long r) -> unsigned long long {
+            const unsigned sel = (unsigned)(r & 7);
+            const unsigned v = (unsigned)(r >> 8);
+            if (sel < 4) return 1023 - 40 + v % 81;
+            if (sel < 6) return v % 2048;
+            return (v & 1) ? 623 - 3 + (v >> 1) % 7 : 1423 - 3 + (v >> 1) % 7;
+        };
+        unsigned long long fs = ms & 0xFFFFFFFFFFFFFULL, fd = md & 0xFFFFFFFFFFFFFULL;
+        // adversarial mantissas: all ones, all zeros, few bits, near-all-ones
+        switch ((m >> 20) & 15) {
+            case 0: fd = 0xFFFFFFFFFFFFFULL; break;
+            case 1: fd = 0; break;
+            case 2: fd = 0xFFFFFFFFFFFFFULL ^ (1ULL << (m % 52)); break;
+            case 3: fd = 1ULL << (m % 52); break;
+            case 4: fs = 0xFFFFFFFFFFFFFULL; break;
+            case 5: fs = 0; break;
+            case 6: fs = fd; break;
+            case 7: fs = 0xFFFFFFFFFFFFFULL ^ (1ULL << (m % 52)); break;
+            default: break;
+        }
+        const unsigned long long bs = ((m >> 62) & 1) << 63 | expo(m >> 24) << 52 | fs;
+        const unsigned long long bd = ((m >> 63) & 1) << 63 | expo(m >> 40) << 52 | fd;
+        const double sv = __longlong_as_double((long long)bs), dv = __longlong_as_double((long long)bd);
+        const double ref = sv / dv;
+        const double got = exact_div(sv, dv, safe_reciprocal(dv));
+        const long long br = __double_as_longlong(ref), bg = __double_as_longlong(got);
+        if (br != bg && !(ref != ref && got != got)) ++bad;   // NaN payloads may differ, values may not
+    }
+    if (bad) atomicAdd(mismatch, bad);
+}
+
 // One work item (a chunk of <= 32 rows of one level) as a compute warp holds it one item ahead:
 // everything that does not depend on x is in registers before the level's barrier opens.
 template <int KP>
@@ -431,8 +501,9 @@ struct TileItem {
     int ent0, w, K;                  // entry k of lane i: ent0 + k*w + i (long rows, k >= KP)
     uint32_t xaddr[KP];              // shared-memory byte address of the x operand of entry k
     uint32_t saddr;                  // where this lane's result goes
+    int bar;                         // hardware barrier id of this item's level
     double a[KP];
-    double rhs, piv;
+    double rhs, piv, rinv;
 };
 
 template <bool HAS_DIAG, int KP>
@@ -450,8 +521,12 @@ __device__ __forceinline__ void tile_item_load(TileItem<KP> &r, const int4 *it, 
     const bool act = lane < (B.z & 0xff);
     const int s = A.x + lane;
     r.saddr = smem_u32(xsk + s);
-    r.rhs = act ? xsk[s] : 0.0;   // the feeder parked b[row] in the row's own x slot
-    r.piv = (HAS_DIAG && act) ? piv[s] : 1.0;
+    r.rhs = act ? xsk[s] : 1.0;   // the feeder parked b[row] in the row's own x slot (idle lanes: keep the
+                                  // division on its fast path)
+    const double2 pr = (HAS_DIAG && act) ? ((const double2 *)piv)[s] : make_double2(1.0, 1.0);
+    r.piv = pr.x;
+    r.rinv = pr.y;
+    r.bar = 1 + (B.x & (TILE_NW - 1));
 #pragma unroll
     for (int u = 0; u < KP; ++u) {
         const bool in = act && u < A.w;
@@ -606,7 +681,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 asm volatile("" ::: "memory");
                 const int upto = (int)(got & 0xffffffffULL);
                 const int s1 = lst[upto];
-                for (int s = lst[seen] + lane; s < s1; s += 32) st_l2(x + rows[s], xsk[s]);
+                for (int s = lst[seen] + lane; s < s1; s += 32) st_l2(x + rows[s], scrub_sentinel(xsk[s]));
                 seen = upto;
             }
             __syncwarp();
@@ -684,12 +759,12 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                     if (lane < (itm.flags & 0xff))
                         for (int kk = KP; kk < itm.K; ++kk) sum -= vp[kk * itm.w] * xsk[cp[kk * itm.w]];
                 }
-                if (HAS_DIAG) sum = sum / itm.piv;
-                sum = scrub_sentinel(sum);
+                if (HAS_DIAG) sum = exact_div(sum, itm.piv, itm.rinv);
                 if (lane < (itm.flags & 0xff)) sts_f64(itm.saddr, sum);
                 // release this level and every level I skip right away; then the next item's prefetch,
                 // off everybody's critical path
-                for (int j = 0; j < itm.n_arr; ++j) level_arrive(itm.level + j, NC);
+                if (itm.n_arr > 0) asm volatile("bar.arrive %0, %1;" ::"r"(itm.bar), "r"(NC) : "memory");
+                for (int j = 1; j < itm.n_arr; ++j) level_arrive(itm.level + j, NC);
                 if (q + 1 < n_it)
                     tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, codes, vals);
             }
@@ -736,6 +811,15 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
     } else {
         return DDILU_ERR_ARG;
     }
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigned long long *mismatch,
+                                      void *stream) {
+    DDILU_CHECK(cudaMemsetAsync(mismatch, 0, sizeof(unsigned long long), ST(stream)));
+    if (n_samples <= 0) return DDILU_OK;
+    fastdiv_selftest<<<stream_grid(n_samples, 256, 64), 256, 0, ST(stream)>>>(n_samples, seed, mismatch);
+    DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
 

@@ -92,6 +92,14 @@ def main():
                     query("ddilu_tiled_set_tuning", b"ctas_per_sm", cps)
                     t = timed(solve_t, flush=flush)
                     rec[f"tiled_c{ct}_k{cps}_us"] = round(t * 1e6, 1)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(50):
+                        solve_t()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    rec[f"tiled_c{ct}_k{cps}_chain_us"] = round(e0.elapsed_time(e1) * 1e3 / 50, 1)
                     rec[f"tiled_c{ct}_k{cps}_frac"] = round(nbytes / t / 1e9 / PEAK, 4)
                 query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
             if ts is not None:

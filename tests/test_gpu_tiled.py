@@ -114,3 +114,14 @@ def test_cyclic_tile_graph_is_refused(P):
     D.sptrsv_tiled(ts, b, x1)
     D.sptrsv(f.lower, f.sched_l, b, x2, False, True)
     assert torch.equal(x1, x2)
+
+
+def test_pivot_division_is_ieee_division(P):
+    """The U solves divide by a pivot through its precomputed reciprocal and two FMA corrections;
+    the result must have the bits of s / d for every operand pair (2^31 random + adversarial pairs)."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for seed in (1, 2, 3, 4):
+        D.call("ddilu_fastdiv_selftest", 1 << 29, seed, bad)
+        assert int(bad.item()) == 0, seed
