@@ -178,6 +178,8 @@ def run_ours(args):
         step(True)
     # --- timed region 1: inputs resident in HBM, kernels watched with CUDA events
     watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_spmv_csr_f64", "ddilu_axpy_dot", "ddilu_dot")
+    if args.watch_all:
+        watch = tuple(k for k, (res, a) in _lib.SIGNATURES.items() if res is _lib._I and a and a[-1] is _lib._P)
     _lib.profile = {k: [] for k in watch}
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     total, recs, launches, m = timed(True, args.steps)
@@ -330,6 +332,7 @@ def main():
     ap.add_argument("--domains", type=int, default=P_DOMAINS)
     ap.add_argument("--cpu-sample", type=int, default=96, help="grid size of the CPU baseline sample (~10 s of CPU)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--watch-all", action="store_true", help="CUDA-event timing of every C-ABI entry (diagnostics)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

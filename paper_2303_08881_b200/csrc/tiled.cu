@@ -340,7 +340,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
                     n_arr = nxt > n_lev ? n_lev - i : nxt - 1 - i;
                 }
                 const int cnt = wl - c * 32 < 32 ? wl - c * 32 : 32;
-                const int flags = cnt | ((first && i >= 1) ? ITEM_SYNC : 0) | (c == 0 ? ITEM_PUBLISH : 0);
+                const int flags = cnt | ((first && i >= 1) ? ITEM_SYNC : 0) | ((c == 0 && i >= 1) ? ITEM_PUBLISH : 0);
                 it[2 * nth] = make_int4(l0 + c * 32, s_lent[i] + c * 32, wl, s_lk[i]);
                 it[2 * nth + 1] = make_int4(i, need, flags, n_arr);
             }
@@ -420,6 +420,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
         : "memory");
     return done != 0;
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// sleep (in hardware) until the phase with this parity completes or ~hint_ns pass; the caller re-checks its condition
+__device__ __forceinline__ void mbar_nap(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done;
     do {
@@ -439,6 +449,7 @@ __device__ __forceinline__ void level_sync(int l, int threads) {
 
 struct TileCtl {
     uint64_t mbar[TILE_NBUF];
+    uint64_t wbar;                    // one arrival per published level: lets the writer warp sleep
     unsigned long long ext_prog[2];   // (tile ordinal << 32) | externals delivered
     int b_ready[2];                   // tile ordinal + 1 whose right-hand side sits in bs[buf]
     unsigned long long lvl_done[2];   // (tile ordinal << 32) | levels complete, for the writer warp
@@ -559,6 +570,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
     const int nk = (n_tiles - (int)blockIdx.x + G - 1) / G;   // my tiles: blockIdx.x + k*G
     if (tid == 0) {
         for (int s = 0; s < TILE_NBUF; ++s) mbar_init(&ctl->mbar[s], 1);
+        mbar_init(&ctl->wbar, 1);
         ctl->ext_prog[0] = ctl->ext_prog[1] = 0ULL;
         ctl->b_ready[0] = ctl->b_ready[1] = 0;
         ctl->comp_done = 0;
@@ -618,14 +630,15 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 __threadfence_block();
                 if (lane == 0) *(volatile int *)&ctl->b_ready[k & 1] = k + 1;
                 ++fed;
+            } else {
+                __nanosleep(200);   // a tile ahead of the compute warps: leave the issue slots to them
             }
         }
     } else if (warp == 1) {
         // ---------------- poller: boundary dependencies, in the order the levels need them
         for (int k = 0; k < nk; ++k) {
             if (k >= 2)
-                while (*comp_done < k - 1 || *wr_done < k - 1) {
-                }
+                while (*comp_done < k - 1 || *wr_done < k - 1) __nanosleep(100);
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
@@ -664,6 +677,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
     } else if (warp == 2) {
         // ---------------- writer: publishes finished levels to L2 so that the compute warps never wait
         // for a global store (a barrier arrive after st.global costs an L2 round trip: scripts/probe_lat.cu)
+        unsigned npub = 0;   // level publishes consumed so far (= completed phases of wbar)
         for (int k = 0; k < nk; ++k) {
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
@@ -676,12 +690,16 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             int seen = 0;
             while (seen < n_lev) {
                 const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)(seen + 1);
-                unsigned long long got;
-                do got = *ld; while (got < want);
+                unsigned long long got = *ld;
+                if (got < want) {   // nothing new: sleep on the publish barrier (phase = publishes consumed so far)
+                    mbar_nap(&ctl->wbar, npub & 1u, 1000);
+                    continue;
+                }
                 asm volatile("" ::: "memory");
                 const int upto = (int)(got & 0xffffffffULL);
                 const int s1 = lst[upto];
                 for (int s = lst[seen] + lane; s < s1; s += 32) st_l2(x + rows[s], scrub_sentinel(xsk[s]));
+                npub += (unsigned)(upto - seen);
                 seen = upto;
             }
             __syncwarp();
@@ -735,8 +753,10 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             int have = 0;
             for (int q = 0; q < n_it; ++q) {
                 if (itm.flags & ITEM_SYNC) level_sync(itm.level - 1, NC);
-                if ((itm.flags & ITEM_PUBLISH) && lane == 0)
+                if ((itm.flags & ITEM_PUBLISH) && lane == 0) {
                     *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.level;
+                    mbar_arrive(&ctl->wbar);
+                }
                 if (itm.need > have) {
                     long long t1 = 0;
                     if (dbg) t1 = clock64();
@@ -769,7 +789,10 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                     tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, codes, vals);
             }
             asm volatile("bar.sync 5, %0;" ::"r"(NC) : "memory");   // tile finished by every compute warp
-            if (cw == 0 && lane == 0) *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)n_lev;
+            if (cw == 0 && lane == 0) {
+                *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)n_lev;
+                mbar_arrive(&ctl->wbar);
+            }
             if (dbg) {
                 t_levels += clock64() - t0;
                 n_lv += n_lev;
