@@ -17,6 +17,7 @@ namespace ddilu {
 
 constexpr int SPMV_ROWS = 256;       // rows (= threads) per CTA
 constexpr int SPMV_STAGE = 4096;     // products staged per CTA (32 KB)
+constexpr int SPMV_UNROLL = 8;       // entries per thread and round
 
 // mode 0: y = A x      mode 1: y = b - A x      mode 2: y = b + A x
 template <int MODE>
@@ -34,7 +35,25 @@ __global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const i
     const int e0 = srp[0], e1 = srp[nrows];
     const int row = row0 + threadIdx.x;
     if (e1 - e0 <= SPMV_STAGE) {
-        for (int e = e0 + threadIdx.x; e < e1; e += SPMV_ROWS) prod[e - e0] = val[e] * x[ci[e]];
+        // all (column, value) loads of a round in flight together, then all the x gathers: eight
+        // independent 2-deep load chains per thread instead of one (HBM latency x bandwidth needs ~44 KB
+        // in flight per SM)
+        for (int base = e0 + threadIdx.x; base < e1; base += SPMV_UNROLL * SPMV_ROWS) {
+            int c[SPMV_UNROLL];
+            double v[SPMV_UNROLL], xv[SPMV_UNROLL];
+#pragma unroll
+            for (int u = 0; u < SPMV_UNROLL; ++u) {
+                const int e = base + u * SPMV_ROWS;
+                const bool in = e < e1;
+                c[u] = in ? ci[e] : -1;
+                v[u] = in ? val[e] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SPMV_UNROLL; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < SPMV_UNROLL; ++u)
+                if (c[u] >= 0) prod[base + u * SPMV_ROWS - e0] = v[u] * xv[u];
+        }
         __syncthreads();
         if (threadIdx.x < nrows) {
             double s = 0.0;
