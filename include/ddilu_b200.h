@@ -240,6 +240,11 @@ int ddilu_drop_small_fill(int n, const int *rp, const int *ci, const double *v, 
 /* ---- ordering.py:304-397 `_bfs_ecc` + `_rcm_order`: Cuthill-McKee order (not reversed) */
 long long ddilu_cm_work_elems(int n);
 int ddilu_cm_order(int n, const int *adj_rp, const int *adj_ci, int *order, int *work, void *stream);
+/* the same when the node ranges [seg_ptr[s], seg_ptr[s+1]) (device array, n_seg + 1 entries) are mutually
+ * disconnected (one per subdomain, precond.py:141-144 calls rcm once per domain): disjoint CTA groups order
+ * the ranges concurrently; identical output */
+int ddilu_cm_order_segments(int n, const int *adj_rp, const int *adj_ci, int n_seg, const int *seg_ptr, int *order,
+                            int *work, void *stream);
 /* ordering.py:416 reversal, per domain segment */
 int ddilu_reverse_segments(int n, const int *cm, int n_seg, const int *seg_ptr, int *out, void *stream);
 

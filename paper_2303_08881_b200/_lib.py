@@ -88,6 +88,7 @@ SIGNATURES = {
     "ddilu_row_lengths": (_I, [_I, _P, _P, _P]),
     "ddilu_cm_work_elems": (_L, [_I]),
     "ddilu_cm_order": (_I, [_I, _P, _P, _P, _P, _P]),
+    "ddilu_cm_order_segments": (_I, [_I, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_reverse_segments": (_I, [_I, _P, _I, _P, _P, _P]),
     "ddilu_narrow_i64": (_I, [_L, _P, _P, _P]),
     "ddilu_widen_i32": (_I, [_L, _P, _P, _P]),

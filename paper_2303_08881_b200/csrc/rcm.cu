@@ -33,6 +33,30 @@ struct RcmState {
     int fcnt[3];
     unsigned long long best;
     int total;
+    unsigned barrier;   // monotone arrival counter of the CTA group that owns this state
+    int pad;
+};
+
+// A group of consecutive CTAs that orders one independent segment of the graph (one subdomain's
+// interior block).  sync() is a barrier over the group's CTAs only (monotone counter in L2): the
+// segments advance concurrently instead of paying every grid barrier once per segment.
+struct CtaGroup {
+    unsigned *bar;
+    int nblk, blk;      // CTAs in the group, my index inside it
+    unsigned phase;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(bar, 1u);
+            const unsigned target = (phase + 1u) * (unsigned)nblk;
+            while ((int)(ld_acquire((const int *)bar) - (int)target) < 0) {
+            }
+            __threadfence();
+        }
+        ++phase;
+        __syncthreads();
+    }
 };
 
 __device__ __forceinline__ int block_excl_scan_512(int v, int *total, int *wtot) {
@@ -62,9 +86,9 @@ __device__ __forceinline__ unsigned long long node_key(const int *rp, int v) {
 }
 
 // level BFS from `root`; returns eccentricity, *last = min (degree, index) node of the last level
-__device__ int bfs_ecc(cg::grid_group &grid, int n, const int *__restrict__ rp, const int *__restrict__ ci, int root,
+__device__ int bfs_ecc(CtaGroup &grid, int n, const int *__restrict__ rp, const int *__restrict__ ci, int root,
                        int stamp, int *mark, int *fa, int *fb, RcmState *st, int *last) {
-    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x, gsize = (long long)gridDim.x * blockDim.x;
+    const long long gtid = (long long)grid.blk * blockDim.x + threadIdx.x, gsize = (long long)grid.nblk * blockDim.x;
     if (gtid == 0) {
         fa[0] = root;
         mark[root] = stamp;
@@ -98,16 +122,31 @@ __device__ int bfs_ecc(cg::grid_group &grid, int n, const int *__restrict__ rp, 
     return level;
 }
 
-__global__ void __launch_bounds__(RCM_THREADS) cm_order_kernel(int n, const int *__restrict__ rp,
-                                                               const int *__restrict__ ci, int *order, int *visited,
-                                                               int *mark, int *ppos, int *fa, int *fb, int *cnt,
-                                                               int *tile_tot, RcmState *st) {
-    cg::grid_group grid = cg::this_grid();
+// n_seg segments [seg_ptr[s], seg_ptr[s+1]) with no edges between them (n_seg = 1, seg_ptr = NULL: the
+// whole graph); the CTAs are dealt to the segments in equal groups.  Scratch arrays are indexed by node or
+// by position, both of which stay inside the segment, so the groups never touch each other's data.
+__global__ void __launch_bounds__(RCM_THREADS) cm_order_kernel(int n_all, const int *__restrict__ rp,
+                                                               const int *__restrict__ ci, int n_seg,
+                                                               const int *__restrict__ seg_ptr, int *order,
+                                                               int *visited, int *mark, int *ppos, int *fa, int *fb,
+                                                               int *cnt, int *tile_tot_all, RcmState *st_all) {
     __shared__ int wtot[RCM_THREADS / 32];
     __shared__ int sh_base, sh_total;
-    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x, gsize = (long long)gridDim.x * blockDim.x;
-    const int G = gridDim.x;
-    int pos = 0, scan = 0, stamp = 0;
+    const int per_seg = (int)gridDim.x / n_seg;           // CTAs per segment (the remainder idles)
+    const int seg = (int)blockIdx.x / per_seg;
+    if (seg >= n_seg) return;
+    RcmState *st = st_all + seg;
+    CtaGroup grid{&st->barrier, per_seg, (int)blockIdx.x - seg * per_seg, 0u};
+    int *tile_tot = tile_tot_all + seg * per_seg;
+    const int node0 = seg_ptr ? seg_ptr[seg] : 0;
+    const int n = seg_ptr ? seg_ptr[seg + 1] : n_all;      // nodes of this segment: [node0, n)
+    // frontier / count scratch of this segment starts at its first node
+    fa += node0;
+    fb += node0;
+    cnt += node0;
+    const long long gtid = (long long)grid.blk * blockDim.x + threadIdx.x, gsize = (long long)grid.nblk * blockDim.x;
+    const int G = grid.nblk;
+    int pos = node0, scan = node0, stamp = 0;
     while (pos < n) {
         // ---- smallest unvisited index >= scan
         int root;
@@ -156,7 +195,7 @@ __global__ void __launch_bounds__(RCM_THREADS) cm_order_kernel(int n, const int 
             // count children per parent; scan inside this CTA's contiguous tile
             const int F = hi - lo;
             const int per = (F + G - 1) / G;
-            const int bx = (int)blockIdx.x;
+            const int bx = grid.blk;
             const int t0 = lo + (int)min((long long)F, (long long)bx * per);
             const int t1 = lo + (int)min((long long)F, (long long)(bx + 1) * per);
             int running = 0;
@@ -172,7 +211,7 @@ __global__ void __launch_bounds__(RCM_THREADS) cm_order_kernel(int n, const int 
                 if (q < t1) cnt[q - lo] = running + ex;
                 running += tot;
             }
-            if (threadIdx.x == 0) tile_tot[blockIdx.x] = running;
+            if (threadIdx.x == 0) tile_tot[grid.blk] = running;
             grid.sync();
             // CTA base = totals of the CTAs before this one
             {
@@ -180,7 +219,7 @@ __global__ void __launch_bounds__(RCM_THREADS) cm_order_kernel(int n, const int 
                 for (int c = threadIdx.x; c < G; c += RCM_THREADS) {
                     const int t = ld_l2(tile_tot + c);
                     all += t;
-                    if (c < (int)blockIdx.x) mine += t;
+                    if (c < grid.blk) mine += t;
                 }
                 int tb, ta;
                 block_excl_scan_512(mine, &tb, wtot);
@@ -271,28 +310,47 @@ __global__ void reverse_segments(int n, const int *__restrict__ cm, int n_seg, c
 using namespace ddilu;
 
 extern "C" long long ddilu_cm_work_elems(int n) {
-    // visited, mark, ppos, fa, fb, cnt: n each; tile totals + state
-    return 6LL * (n > 0 ? n : 1) + 4096 + 64;
+    // visited, mark, ppos, fa, fb, cnt: n each; tile totals + one state per segment group
+    return 6LL * (n > 0 ? n : 1) + 4096 + 16 * 256;
 }
 
-extern "C" int ddilu_cm_order(int n, const int *adj_rp, const int *adj_ci, int *order, int *work, void *stream) {
-    cudaStream_t st = (cudaStream_t)stream;
+static int cm_order_launch(int n, const int *adj_rp, const int *adj_ci, int n_seg, const int *seg_ptr, int *order,
+                           int *work, cudaStream_t st) {
     if (n <= 0) return DDILU_OK;
     const long long nn = n;
     int *visited = work, *mark = work + nn, *ppos = work + 2 * nn, *fa = work + 3 * nn, *fb = work + 4 * nn,
         *cnt = work + 5 * nn, *tile_tot = work + 6 * nn;
     RcmState *state = (RcmState *)(work + 6 * nn + 4096);
+    int grid = device_info().sm_count;  // one CTA per SM keeps the barriers cheap
+    if (grid > 4096) grid = 4096;
+    if (n_seg < 1 || !seg_ptr) {
+        n_seg = 1;
+        seg_ptr = nullptr;
+    }
+    if (n_seg > grid || n_seg > 256) return DDILU_ERR_ARG;
     DDILU_CHECK(cudaMemsetAsync(visited, 0, sizeof(int) * nn, st));
     DDILU_CHECK(cudaMemsetAsync(mark, 0xFF, sizeof(int) * nn, st));
     DDILU_CHECK(cudaMemsetAsync(ppos, 0x7F, sizeof(int) * nn, st));  // 0x7F7F7F7F > any position
+    DDILU_CHECK(cudaMemsetAsync(state, 0, sizeof(RcmState) * n_seg, st));
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cm_order_kernel, RCM_THREADS, 0);
     if (occ < 1) return DDILU_ERR_ARG;
-    int grid = device_info().sm_count;  // one CTA per SM keeps the grid barrier cheap
-    if (grid > 4096) grid = 4096;
-    void *args[] = {&n, &adj_rp, &adj_ci, &order, &visited, &mark, &ppos, &fa, &fb, &cnt, &tile_tot, &state};
+    void *args[] = {&n, &adj_rp, &adj_ci, &n_seg, &seg_ptr, &order, &visited, &mark, &ppos, &fa, &fb, &cnt, &tile_tot,
+                    &state};
+    // cooperative launch: the group barriers need every CTA resident
     DDILU_CHECK(cudaLaunchCooperativeKernel((void *)cm_order_kernel, grid, RCM_THREADS, args, 0, st));
     return DDILU_OK;
+}
+
+extern "C" int ddilu_cm_order(int n, const int *adj_rp, const int *adj_ci, int *order, int *work, void *stream) {
+    return cm_order_launch(n, adj_rp, adj_ci, 1, nullptr, order, work, (cudaStream_t)stream);
+}
+
+/* the same for a graph whose node ranges [seg_ptr[s], seg_ptr[s+1]) are not connected to each other
+ * (one range per subdomain): the ranges are ordered concurrently by disjoint CTA groups */
+extern "C" int ddilu_cm_order_segments(int n, const int *adj_rp, const int *adj_ci, int n_seg, const int *seg_ptr,
+                                       int *order, int *work, void *stream) {
+    return cm_order_launch(n, adj_rp, adj_ci, n_seg, seg_ptr, order, work, (cudaStream_t)stream);
 }
 
 extern "C" int ddilu_reverse_segments(int n, const int *cm, int n_seg, const int *seg_ptr, int *out, void *stream) {

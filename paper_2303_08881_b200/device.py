@@ -483,12 +483,18 @@ def sym_adjacency(pattern: DeviceCsr, sort: bool = False) -> DeviceCsr:
     return DeviceCsr(n, n, rp, ci, None, nnz)
 
 
-def cm_order(adj: DeviceCsr) -> torch.Tensor:
-    """Cuthill-McKee order (not reversed) of a symmetric adjacency."""
+def cm_order(adj: DeviceCsr, seg_ptr: torch.Tensor | None = None) -> torch.Tensor:
+    """Cuthill-McKee order (not reversed) of a symmetric adjacency.  seg_ptr (int32 device,
+    optional): node ranges that are not connected to each other (one per subdomain); they are
+    ordered concurrently, with the same result."""
     n = adj.n_rows
     order = empty_i32(max(n, 1))
     work = empty_i32(query("ddilu_cm_work_elems", n))
-    call("ddilu_cm_order", n, adj.rp, adj.ci, order, work)
+    n_seg = seg_ptr.numel() - 1 if seg_ptr is not None else 1
+    if seg_ptr is not None and 1 < n_seg <= 64:
+        call("ddilu_cm_order_segments", n, adj.rp, adj.ci, n_seg, seg_ptr, order, work)
+    else:
+        call("ddilu_cm_order", n, adj.rp, adj.ci, order, work)
     return order[:n]
 
 

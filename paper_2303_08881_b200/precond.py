@@ -71,8 +71,8 @@ class LocalSystem:
             cmap = D.index_map(n, ints)
             pat = D.gather_rows(ad, ints, self.n_int, cmap, self.n_int, filt=4, resort=True, with_values=False)
             adj = D.sym_adjacency(pat)
-            cm = D.cm_order(adj)
             seg = torch.from_numpy(self.int_ptr.astype(np.int32)).to(D.dev())
+            cm = D.cm_order(adj, seg)      # interiors of different domains never couple: ordered concurrently
             ints = D.gather_i32(ints, D.reverse_segments(cm, seg))
         self.nodes = torch.cat([ints, exts]).contiguous()          # global index of each local row
         colmap = D.index_map(n, self.nodes)
