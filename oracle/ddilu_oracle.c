@@ -721,6 +721,125 @@ void orc_ilut_factor(i64 n, const i64 *a_rp, const i64 *a_ci, const double *a_v,
     *u_v_out = U.v;
 }
 
+/* factor.py:270-369 (_iluk_symbolic): level-of-fill pattern.  Row i starts as
+ * pattern(A_i) plus the diagonal, all at level 0; every pivot k < lim of the
+ * working row (in increasing column order, fill included) merges the kept
+ * part of row k beyond its diagonal with level lev(i,k) + lev(k,j) + 1, kept
+ * if <= klevel, the smaller level winning on a position already present.
+ * The working row is a sorted array here (the reference threads a linked
+ * list through an n-vector; the visiting order and the results are the same).
+ * p_rp / k_rp have n+1 entries, column arrays are malloc'ed (orc_free). */
+void orc_iluk_symbolic(i64 n, const i64 *a_rp, const i64 *a_ci, i64 n_elim,
+                       i64 klevel, i64 *p_rp, i64 **p_ci_out, i64 *k_rp,
+                       i64 **k_ci_out)
+{
+    i64 pcap = a_rp[n] + 16, kcap = a_rp[n] + n + 16;
+    i64 *p_ci = (i64 *)malloc(sizeof(i64) * (size_t)pcap);
+    i64 *k_ci = (i64 *)malloc(sizeof(i64) * (size_t)kcap);
+    i64 *k_lv = (i64 *)malloc(sizeof(i64) * (size_t)kcap);
+    i64 wcap = 64;
+    i64 *wc = (i64 *)malloc(sizeof(i64) * (size_t)wcap);   /* working row: columns  */
+    i64 *wl = (i64 *)malloc(sizeof(i64) * (size_t)wcap);   /* ... and their levels  */
+    p_rp[0] = 0;
+    k_rp[0] = 0;
+    for (i64 i = 0; i < n; ++i) {
+        const i64 lim = i < n_elim ? i : n_elim;
+        i64 len = 0;
+        int have_diag = 0;
+        if (a_rp[i + 1] - a_rp[i] + 1 > wcap) {
+            wcap = 2 * (a_rp[i + 1] - a_rp[i] + 1);
+            wc = (i64 *)realloc(wc, sizeof(i64) * (size_t)wcap);
+            wl = (i64 *)realloc(wl, sizeof(i64) * (size_t)wcap);
+        }
+        for (i64 s = a_rp[i]; s < a_rp[i + 1]; ++s) {
+            const i64 j = a_ci[s];
+            if (!have_diag && j >= i) {
+                if (j > i) {
+                    wc[len] = i;
+                    wl[len++] = 0;
+                }
+                have_diag = 1;
+            }
+            wc[len] = j;
+            wl[len++] = 0;
+        }
+        if (!have_diag) {
+            wc[len] = i;
+            wl[len++] = 0;
+        }
+        for (i64 pos = 0; pos < len && wc[pos] < lim; ++pos) {
+            const i64 k = wc[pos], lk = wl[pos];
+            i64 at = pos;                      /* merge cursor: columns only grow */
+            for (i64 t = k_rp[k] + 1; t < k_rp[k + 1]; ++t) {
+                const i64 j = k_ci[t], nl = lk + k_lv[t] + 1;
+                if (nl > klevel)
+                    continue;
+                while (at + 1 < len && wc[at + 1] <= j)
+                    ++at;
+                if (wc[at] == j) {
+                    if (nl < wl[at])
+                        wl[at] = nl;
+                } else {                       /* insert after `at` */
+                    if (len + 1 > wcap) {
+                        wcap *= 2;
+                        wc = (i64 *)realloc(wc, sizeof(i64) * (size_t)wcap);
+                        wl = (i64 *)realloc(wl, sizeof(i64) * (size_t)wcap);
+                    }
+                    memmove(wc + at + 2, wc + at + 1, sizeof(i64) * (size_t)(len - at - 1));
+                    memmove(wl + at + 2, wl + at + 1, sizeof(i64) * (size_t)(len - at - 1));
+                    wc[at + 1] = j;
+                    wl[at + 1] = nl;
+                    ++len;
+                    ++at;
+                }
+            }
+        }
+        i64 np = 0;
+        while (np < len && wc[np] < lim)
+            ++np;
+        if (p_rp[i] + np > pcap) {
+            pcap = 2 * pcap > p_rp[i] + np ? 2 * pcap : p_rp[i] + np;
+            p_ci = (i64 *)realloc(p_ci, sizeof(i64) * (size_t)pcap);
+        }
+        if (k_rp[i] + len - np > kcap) {
+            kcap = 2 * kcap > k_rp[i] + len - np ? 2 * kcap : k_rp[i] + len - np;
+            k_ci = (i64 *)realloc(k_ci, sizeof(i64) * (size_t)kcap);
+            k_lv = (i64 *)realloc(k_lv, sizeof(i64) * (size_t)kcap);
+        }
+        memcpy(p_ci + p_rp[i], wc, sizeof(i64) * (size_t)np);
+        memcpy(k_ci + k_rp[i], wc + np, sizeof(i64) * (size_t)(len - np));
+        memcpy(k_lv + k_rp[i], wl + np, sizeof(i64) * (size_t)(len - np));
+        p_rp[i + 1] = p_rp[i] + np;
+        k_rp[i + 1] = k_rp[i] + len - np;
+    }
+    free(k_lv);
+    free(wc);
+    free(wl);
+    *p_ci_out = p_ci;
+    *k_ci_out = k_ci;
+}
+
+/* factor.py:372-390 (_prefill): values of A into the matching slots of a
+ * superset pattern; fill positions keep 0.  upper_part 0: columns < lim of
+ * every row, 1: columns >= lim (lim = min(i, n_elim)). */
+void orc_prefill(i64 n, const i64 *a_rp, const i64 *a_ci, const double *a_v,
+                 const i64 *rp, const i64 *ci, double *v, i64 n_elim, int upper_part)
+{
+    for (i64 i = 0; i < n; ++i) {
+        const i64 lim = i < n_elim ? i : n_elim;
+        i64 t = rp[i];
+        for (i64 s = a_rp[i]; s < a_rp[i + 1]; ++s) {
+            const i64 j = a_ci[s];
+            if ((upper_part == 0) != (j < lim))
+                continue;
+            while (t < rp[i + 1] && ci[t] < j)
+                ++t;
+            if (t < rp[i + 1] && ci[t] == j)
+                v[t++] = a_v[s];
+        }
+    }
+}
+
 void orc_free(void *p) { free(p); }
 
 /* factor.py:756-781 (_col_split_counts / _col_split_fill): rows [r0, r1) cut

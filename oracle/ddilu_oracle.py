@@ -353,23 +353,28 @@ DIAG_SAFEGUARD = 1e-6
 
 @dataclass(frozen=True)
 class Rule:
-    """factor.py:59-105 (FillRule); iluk is outside the hot path."""
+    """factor.py:59-105 (FillRule)."""
 
     kind: str = "ilu0"
     tau: float = 0.0
     maxfill: int = 0
+    level: int = 0
 
     @staticmethod
     def parse(text):
         head, _, rest = text.partition(":")
         if head == "ilu0" and not rest:
             return Rule("ilu0")
+        if head == "iluk" and rest:
+            return Rule("iluk", level=int(rest))
         if head == "ilut" and rest:
             t, _, f = rest.partition(",")
             return Rule("ilut", float(t), int(f))
         raise ValueError(f"cannot parse fill rule {text!r}")
 
     def __str__(self):
+        if self.kind == "iluk":
+            return f"iluk:{self.level}"
         return f"ilut:{self.tau:g},{self.maxfill}" if self.kind == "ilut" else "ilu0"
 
 
@@ -392,10 +397,34 @@ def level0_split(a: Csr, n_elim):
     return p_rp, p_ci, p_v, k_rp, k_ci, k_v
 
 
-def _factor_on_pattern(a: Csr, n_elim, milu, target, wvec, safeguard):
-    """factor.py:446-458."""
+def iluk_split(a: Csr, n_elim, level):
+    """factor.py:270-390: symbolic level-of-fill pattern + A's values prefilled (fill = 0)."""
     n = a.n_rows
-    p_rp, p_ci, p_v, k_rp, k_ci, k_v = level0_split(a, n_elim)
+    p_rp = np.zeros(n + 1, dtype=np.int64)
+    k_rp = np.zeros(n + 1, dtype=np.int64)
+    ptrs = [ctypes.c_void_p() for _ in range(2)]
+    lib().orc_iluk_symbolic(_I(n), _p(a.row_ptr), _p(a.col_idx), _I(n_elim), _I(level), _p(p_rp),
+                            ctypes.byref(ptrs[0]), _p(k_rp), ctypes.byref(ptrs[1]))
+
+    def take(ptr, count):
+        out = np.empty(0, dtype=np.int64) if count == 0 else \
+            np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_int64)), (count,)).copy()
+        lib().orc_free(ptr)
+        return out
+
+    p_ci, k_ci = take(ptrs[0], int(p_rp[-1])), take(ptrs[1], int(k_rp[-1]))
+    p_v, k_v = np.zeros(len(p_ci)), np.zeros(len(k_ci))
+    lib().orc_prefill(_I(n), _p(a.row_ptr), _p(a.col_idx), _p(a.values), _p(p_rp), _p(p_ci), _p(p_v),
+                      _I(n_elim), ctypes.c_int(0))
+    lib().orc_prefill(_I(n), _p(a.row_ptr), _p(a.col_idx), _p(a.values), _p(k_rp), _p(k_ci), _p(k_v),
+                      _I(n_elim), ctypes.c_int(1))
+    return p_rp, p_ci, p_v, k_rp, k_ci, k_v
+
+
+def _factor_on_pattern(a: Csr, n_elim, milu, target, wvec, safeguard, level=0):
+    """factor.py:446-458 (level > 0: on the iluk pattern, factor.py:704-720, 855-863)."""
+    n = a.n_rows
+    p_rp, p_ci, p_v, k_rp, k_ci, k_v = level0_split(a, n_elim) if level <= 0 else iluk_split(a, n_elim, level)
     rownorm = np.empty(n)
     lib().orc_row_inf_norms(_I(n), _p(a.row_ptr), _p(a.values), _p(rownorm))
     if target is None:
@@ -477,10 +506,22 @@ def ilut(a: Csr, tau, maxfill, safeguard=DIAG_SAFEGUARD):
     return Factors(lo, up, str(Rule("ilut", tau, maxfill)))
 
 
+def iluk(a: Csr, level, safeguard=DIAG_SAFEGUARD):
+    """factor.py:704-720."""
+    if level < 0:
+        raise ValueError("level must be nonnegative")
+    if level == 0:
+        return ilu0(a, safeguard)
+    lo, up = _factor_on_pattern(a, a.n_rows, False, None, None, safeguard, level)
+    return Factors(lo, up, f"iluk:{level}")
+
+
 def factorize(a: Csr, rule: Rule, safeguard=DIAG_SAFEGUARD):
     """factor.py:743-749."""
     if rule.kind == "ilu0":
         return ilu0(a, safeguard)
+    if rule.kind == "iluk":
+        return iluk(a, rule.level, safeguard)
     return ilut(a, rule.tau, rule.maxfill, safeguard)
 
 
@@ -532,7 +573,8 @@ def partial_ilu(a: Csr, n_interior, rule: Rule, schur_drop_tol=0.0, factor_schur
         lower, upper = _ilut_raw(a, n_interior, rule.tau, rule.maxfill, schur_drop_tol, safeguard)
         drop_tol = 0.0
     else:
-        lower, upper = _factor_on_pattern(a, n_interior, False, None, None, safeguard)
+        lower, upper = _factor_on_pattern(a, n_interior, False, None, None, safeguard,
+                                          rule.level if rule.kind == "iluk" else 0)
         drop_tol = schur_drop_tol
     l_b, _ = rows_colsplit(lower, 0, n_interior, n_interior)
     u_b, z_blk = rows_colsplit(upper, 0, n_interior, n_interior)

@@ -47,6 +47,7 @@ struct TiledTuning {
     long long *debug = nullptr;  // optional device buffer: 8 int64 per CTA of cycle counters (scripts/probe_tiled.py)
 };
 static TiledTuning g_tiled;
+__device__ unsigned g_nap_ns = 0;    // back-off of compute warps that wait for boundary dependencies / the next tile
 
 #define GRID_STRIDE_Q(i, n) \
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (long long)gridDim.x * blockDim.x)
@@ -721,8 +722,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             long long t0 = 0;
             if (dbg) t0 = clock64();
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) {
-            }
+            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) __nanosleep(g_nap_ns);
             asm volatile("" ::: "memory");
             if (dbg) t_wait_tile += clock64() - t0;
             volatile unsigned long long *lvl_done = &ctl->lvl_done[k & 1];
@@ -761,8 +761,11 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                     long long t1 = 0;
                     if (dbg) t1 = clock64();
                     const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.need;
-                    unsigned long long got;
-                    do got = *prog; while (got < want);
+                    unsigned long long got = *prog;
+                    while (got < want) {   // producers are behind: do not burn the SM's issue slots meanwhile
+                        __nanosleep(g_nap_ns);
+                        got = *prog;
+                    }
                     have = (int)(got & 0xffffffffULL);
                     if (dbg) t_wait_ext += clock64() - t1;
                 }
@@ -831,6 +834,9 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
         g_tiled.ctas_per_sm = value;
     } else if (eq("grid_cap")) {
         g_tiled.grid_cap = value;
+    } else if (eq("nap_ns")) {
+        unsigned v = (unsigned)value;
+        if (cudaMemcpyToSymbol(g_nap_ns, &v, sizeof(v)) != cudaSuccess) return DDILU_ERR_ARG;
     } else {
         return DDILU_ERR_ARG;
     }

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--no-sell", action="store_true")
     ap.add_argument("--grid-cap", type=int, default=0)
+    ap.add_argument("--nap", type=int, default=-1)
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
@@ -55,6 +56,8 @@ def main():
         out.flush()
 
     query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
+    if args.nap >= 0:
+        query("ddilu_tiled_set_tuning", b"nap_ns", args.nap)
     dims = (args.n,) * 3
     a = P.aniso3d(*dims)
     a.device()
