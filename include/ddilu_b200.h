@@ -101,6 +101,17 @@ int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *or
                             int uniform_width, const int *scol, const double *sval, const double *sdiag,
                             const int *gwait, const double *b, double *x, long long *stamps, void *stream);
 
+/* ---- factor.py:270-369 `_iluk_symbolic`: level-of-fill pattern (levels <= klevel), rows >= n_elim keep
+ * their trailing block un-eliminated.  Row slabs of row_cap entries: p_* = pivot (L) part, k_* = kept
+ * (U / Schur) part with fill levels; *status != 0: a row outgrew row_cap (retry with a larger one).
+ * ddilu_compact_cols: slab -> CSR columns; ddilu_prefill: factor.py:372-390 `_prefill`. */
+long long ddilu_iluk_smem_bytes(int row_cap);
+int ddilu_iluk_symbolic(int n, const int *a_rp, const int *a_ci, int n_elim, int klevel, int row_cap, int *p_cnt,
+                        int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status, void *stream);
+int ddilu_compact_cols(int n, int cap, const int *cnt, const int *ci, const int *out_rp, int *out_ci, void *stream);
+int ddilu_prefill(int n, const int *a_rp, const int *a_ci, const double *a_v, const int *rp, const int *ci, double *v,
+                  int n_elim, int upper_part, void *stream);
+
 /* ---- tiled triangular solve (csrc/tiled.cu): sparse.py:228-272 again, for factors whose
  * rows cluster into tiles (<= 1024 rows) with an ACYCLIC tile dependency graph.  A CTA
  * walks a tile's levels with the tile's x in shared memory; boundary dependencies go

@@ -39,6 +39,10 @@ SIGNATURES = {
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_sell_trace": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_iluk_smem_bytes": (_L, [_I]),
+    "ddilu_iluk_symbolic": (_I, [_I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_compact_cols": (_I, [_I, _I, _P, _P, _P, _P, _P]),
+    "ddilu_prefill": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "ddilu_tiled_set_tuning": (_I, [_S, _I]),
     "ddilu_tiled_set_debug": (_I, [_P]),
     "ddilu_tile_box_keys": (_I, [_I, _P, _I, _P, _P, _P, _P, _P, _P]),

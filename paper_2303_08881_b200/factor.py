@@ -5,8 +5,8 @@ ilu0 / milu0 / partial_ilu run the level-scheduled numeric kernel of
 csrc/factor.cu on the split pattern (factor.py:198-263, 397-432); ilut runs the
 sync-free row kernel of csrc/ilut.cu (factor.py:482-656).  Results are device
 resident; the host CSR arrays of the returned objects are materialised only
-when read.  iluk (level-of-fill k > 0) is a "next" row and is
-not built.
+when read.  iluk (level-of-fill k > 0): symbolic phase in csrc/iluk.cu, numeric
+phase = the same fixed-pattern kernel on the larger pattern.
 """
 
 from __future__ import annotations
@@ -20,7 +20,7 @@ from . import device as D
 from .sparse import CsrMatrix
 
 __all__ = [
-    "FillRule", "IluFactors", "MiluVectors", "PartialIluFactors", "TwoLevelBlocks", "ilu0", "ilut", "milu0",
+    "FillRule", "IluFactors", "MiluVectors", "PartialIluFactors", "TwoLevelBlocks", "ilu0", "iluk", "ilut", "milu0",
     "factorize", "partial_ilu", "extract_two_level_blocks", "DIAG_SAFEGUARD",
 ]
 
@@ -158,10 +158,17 @@ def d_level0_split(a: D.DeviceCsr, n_elim: int):
 
 
 def d_factor_level0(a: D.DeviceCsr, n_elim: int, milu: bool = False, target: torch.Tensor | None = None,
-                    wvec: torch.Tensor | None = None, safeguard: float = DIAG_SAFEGUARD) -> DevFactors:
-    """factor.py:446-458 `_factor_on_pattern`: split, schedule, numeric sweep."""
+                    wvec: torch.Tensor | None = None, safeguard: float = DIAG_SAFEGUARD, level: int = 0) -> DevFactors:
+    """factor.py:446-458 `_factor_on_pattern`: split (level 0) or symbolic level-of-fill pattern
+    (level > 0, factor.py:704-720, 855-863), schedule, numeric sweep."""
     n = a.n_rows
-    lo, up, rownorm = d_level0_split(a, n_elim)
+    if level > 0 and n:
+        from ._iluk import d_iluk_split
+        lo, up = d_iluk_split(a, n_elim, level)
+        rownorm = D.empty_f64(n)                     # row inf-norms of A: by-product of the split's count pass
+        D.call("ddilu_split_count", n, a.rp, a.ci, a.val, int(n_elim), D.empty_i32(n + 1), D.empty_i32(n + 1), rownorm)
+    else:
+        lo, up, rownorm = d_level0_split(a, n_elim)
     sched = D.build_schedule(lo, False)
     done = D.empty_i32(max(n, 1))
     D.call("ddilu_ilu0_numeric", n, sched.n_slots, sched.order, lo.rp, lo.ci, lo.val, up.rp, up.ci, up.val,
@@ -176,11 +183,9 @@ def d_ilut(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float,
 
 
 def d_factorize(a: D.DeviceCsr, rule: FillRule, safeguard: float = DIAG_SAFEGUARD) -> DevFactors:
-    if rule.kind == "ilu0" or (rule.kind == "iluk" and rule.level == 0):
-        return d_factor_level0(a, a.n_rows, safeguard=safeguard)
-    if rule.kind == "ilut":
-        return d_ilut(a, a.n_rows, rule.tau, rule.maxfill, 0.0, safeguard)
-    raise NotImplementedError("iluk with level > 0 is a 'next' row of the hot-path scope (SURVEY.md 8f)")
+    if rule.kind == "ilu0" or rule.kind == "iluk":
+        return d_factor_level0(a, a.n_rows, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
+    return d_ilut(a, a.n_rows, rule.tau, rule.maxfill, 0.0, safeguard)
 
 
 class DevPartial:
@@ -223,11 +228,9 @@ def d_partial_ilu(a: D.DeviceCsr, n_interior: int, rule: FillRule, schur_drop_to
     if rule.kind == "ilut":
         f = d_ilut(a, n_interior, rule.tau, rule.maxfill, schur_drop_tol, safeguard)
         drop_tol = 0.0
-    elif rule.kind == "ilu0" or rule.level == 0:
-        f = d_factor_level0(a, n_interior, safeguard=safeguard)
-        drop_tol = schur_drop_tol
     else:
-        raise NotImplementedError("iluk with level > 0 is a 'next' row of the hot-path scope (SURVEY.md 8f)")
+        f = d_factor_level0(a, n_interior, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
+        drop_tol = schur_drop_tol
     l_b, u_b, w, z, _, s_tilde = d_carve(f, n_interior)
     s_tilde = d_drop_small_rows(s_tilde, drop_tol)
     schur = d_factorize(s_tilde, rule, safeguard) if factor_schur else None
@@ -338,6 +341,17 @@ def milu0(a: CsrMatrix, vecs: MiluVectors | None = None, safeguard: float = DIAG
         raise ValueError("milu target vector must have no zero entries")
     d = d_factor_level0(a.device(), n, True, D.to_device_f64(target), D.to_device_f64(vecs.full_w(n)), safeguard)
     return IluFactors._from_device(d, "milu0")
+
+
+def iluk(a: CsrMatrix, level: int, safeguard: float = DIAG_SAFEGUARD) -> IluFactors:
+    """factor.py:704-720."""
+    _check_square(a)
+    if level < 0:
+        raise ValueError("level must be nonnegative")
+    if level == 0:
+        return ilu0(a, safeguard)
+    d = d_factor_level0(a.device(), a.n_rows, safeguard=safeguard, level=level)
+    return IluFactors._from_device(d, str(FillRule("iluk", level=level)))
 
 
 def ilut(a: CsrMatrix, tau: float, maxfill: int, safeguard: float = DIAG_SAFEGUARD) -> IluFactors:
