@@ -111,10 +111,14 @@ class Arnoldi:
         self.comm.allreduce_sum_(s)
         return math.sqrt(float(s.item()))
 
-    def mgs(self, j: int) -> np.ndarray:
+    def mgs(self, j: int, h: torch.Tensor | None = None):
         """Orthogonalise self.w against V[0..j] (krylov.py:131-136).  Returns the
-        host copy of [h_0j .. h_jj, |w|^2]."""
-        n, V, w, h, red, comm = self.n, self.V, self.w, self.hdev, self.red, self.comm
+        host copy of [h_0j .. h_jj, |w|^2]; with a device buffer `h` (>= j + 2 entries) the column
+        stays on the device and nothing is read back (no host synchronisation)."""
+        n, V, w, red, comm = self.n, self.V, self.w, self.red, self.comm
+        to_host = h is None
+        if to_host:
+            h = self.hdev
         red.dot(n, V[0], w, h[0:1])
         comm.allreduce_sum_(h[0:1])
         for i in range(j):
@@ -122,11 +126,12 @@ class Arnoldi:
             comm.allreduce_sum_(h[i + 1:i + 2])
         red.axpy_dot(n, h[j:j + 1], -1.0, V[j], w, w, h[j + 1:j + 2])
         comm.allreduce_sum_(h[j + 1:j + 2])
-        return h[: j + 2].cpu().numpy()
+        return h[: j + 2].cpu().numpy() if to_host else None
 
-    def normalise_into(self, j: int):
+    def normalise_into(self, j: int, h: torch.Tensor | None = None):
         """V[j+1] = w / hnext with hnext = sqrt(h[j+1]) read on the device (krylov.py:156)."""
-        D.scale(self.n, self.w, self.V[j + 1], alpha_dev=self.hdev[j + 1:j + 2], take_sqrt=True)
+        h = self.hdev if h is None else h
+        D.scale(self.n, self.w, self.V[j + 1], alpha_dev=h[j + 1:j + 2], take_sqrt=True)
 
     def combine(self, basis, y: np.ndarray, x, overwrite: bool):
         """x (+)= sum_i y_i basis[i] (krylov.py:160-166, 264-267)."""
@@ -224,19 +229,73 @@ class InnerGmres:
         self.ws = Arnoldi(self.n, self.m, comm, flexible=False, pad=pad)
         self.z = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
         self.u = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
+        self.hcols = None   # device Hessenberg columns of one solve: row j = [h_0j .. h_jj, |w|^2], last row = <b, b>
 
     def solve(self, apply_a: DevOp, b: torch.Tensor, out: torch.Tensor, apply_m: DevOp | None = None,
               n_global: int | None = None):
+        """The m Arnoldi steps are queued WITHOUT reading anything back: the Hessenberg columns stay in
+        a device buffer, the basis is normalised with device scalars, and ONE copy at the end feeds the
+        reference's host arithmetic (Givens rotations, back substitution: identical operations, identical
+        bits).  The reference's early exits (beta == 0, happy breakdown: krylov.py:228-231, 252-253) are
+        detected in that copy; the breakdown case is then redone step by step, exactly as the reference
+        would have run it."""
         n, ws = self.n, self.ws
         ng = n if n_global is None else n_global
         if ng == 0 or self.iters <= 0:
             out[:n].zero_()
             return out
+        m = min(self.iters, ng)
+        if self.hcols is None:
+            self.hcols = torch.zeros((self.m + 1, self.m + 2), dtype=D.F64, device=D.dev())
+        H = self.hcols
+        V, w = ws.V, ws.w
+        bb = H[self.m, 0:1]                      # <b, b>
+        ws.red.dot(n, b, b, bb)
+        self.comm.allreduce_sum_(bb)
+        D.scale(n, b, V[0], alpha_dev=bb, take_sqrt=True)
+        for j in range(m):
+            if apply_m is not None:
+                apply_m(V[j], self.z)
+                apply_a(self.z, w)
+            else:
+                apply_a(V[j], w)
+            ws.mgs(j, H[j])
+            ws.normalise_into(j, H[j])
+        host = H.cpu().numpy()                   # the one synchronisation of the inner solve
+        beta = math.sqrt(float(host[self.m, 0]))
+        if beta == 0.0:
+            out[:n].zero_()
+            return out
+        h = np.zeros((m + 1, m))
+        cs, sn, g = np.empty(m), np.empty(m), np.zeros(m + 1)
+        g[0] = beta
+        k = 0
+        for j in range(m):
+            col = host[j]
+            h[: j + 1, j] = col[: j + 1]
+            hnext = math.sqrt(col[j + 1]) if col[j + 1] > 0.0 else 0.0
+            h[j + 1, j] = hnext
+            _givens(h, cs, sn, g, j, hnext)
+            k = j + 1
+            if hnext < self.happy_tol:
+                if j + 1 < m:   # the queued steps after a breakdown divided by ~0: redo it the reference's way
+                    return self._solve_stepwise(apply_a, b, out, apply_m, m)
+                break
+        y = _back_substitute(h, g, k)
+        if apply_m is not None:
+            ws.combine(V, y, self.u, overwrite=True)
+            apply_m(self.u, out)
+        else:
+            ws.combine(V, y, out, overwrite=True)
+        return out
+
+    def _solve_stepwise(self, apply_a: DevOp, b: torch.Tensor, out: torch.Tensor, apply_m: DevOp | None, m: int):
+        """krylov.py:213-268 with a host read per Arnoldi step (used after a happy breakdown)."""
+        n, ws = self.n, self.ws
         beta = ws.norm2(b)
         if beta == 0.0:
             out[:n].zero_()
             return out
-        m = min(self.iters, ng)
         V, w = ws.V, ws.w
         h = np.zeros((m + 1, m))
         cs, sn, g = np.empty(m), np.empty(m), np.zeros(m + 1)

@@ -101,6 +101,27 @@ class LocalSystem:
         owner = lay._owner_d if lay.p > 1 else None
         return D.box_tile_keys(self.nodes[r0:r1], r1 - r0, lay.grid_hint, tdims, owner)
 
+    def _ext_partition(self, max_rows: int, int_keys, int_range: int):
+        """Box tiles of the interface rows with at most max_rows rows each (edge 32, 16, ... until it
+        fits); with int_keys the interior rows (keys below int_range) are partitioned along."""
+        lay = self.layout
+        nd, p = len(lay.grid_hint), max(1, lay.p)
+        e = 32 if nd == 3 else D.TILE_MAX_ROWS
+        while e >= 2:
+            keys, nk = self._tile_keys(self.n_int, self.n_loc, [e] * nd)
+            if isinstance(int_keys, torch.Tensor):
+                keys, rng = torch.cat([int_keys, keys + int_range]), int_range + nk * p
+            else:
+                rng = nk * p
+            part = D.tile_partition(keys, rng)
+            if part is not None:
+                sizes = part.tile_ptr[1:] - part.tile_ptr[:-1]
+                ext_tiles = part.tile_of[self.n_int if isinstance(int_keys, torch.Tensor) else 0:].long().unique()
+                if int(sizes[ext_tiles].max().item()) <= max_rows:
+                    return part, [e] * nd
+            e //= 2
+        return None, None
+
     def tile_part(self, which: str):
         """Tile partition of the local rows for the tiled triangular solves: box tiles of
         the structured grid (`layout.grid_hint`), None for unstructured matrices.
@@ -119,21 +140,17 @@ class LocalSystem:
             keys, nk = self._tile_keys(0, self.n_int, tdims)
             part = D.tile_partition(keys, nk * p)
         elif which == "ext" and self.n_ext:
-            e = 32 if nd == 3 else D.TILE_MAX_ROWS
-            while e >= 2 and part is None:
-                keys, nk = self._tile_keys(self.n_int, self.n_loc, [e] * nd)
-                part = D.tile_partition(keys, nk * p)
-                self._ext_tdims = [e] * nd
-                e //= 2
+            part, self._ext_tdims = self._ext_partition(D.TILE_MAX_ROWS, 0, 0)
         elif which == "all":
             if self.n_ext == 0:
                 part = self.tile_part("int")
-            elif self.tile_part("int") is not None and self.tile_part("ext") is not None:
+            elif self.tile_part("int") is not None:
+                # interface rows of a full-block factor also depend on interior rows (W): keep their tiles at
+                # <= 512 rows so that tile + boundary dependencies fit the shared-memory budget
                 e = {3: 8, 2: 16, 1: self.TILE_TARGET_ROWS}[nd]
                 tdims = [2 * e if (nd == 2 and a == 0) else e for a in range(nd)]
                 ki, nki = self._tile_keys(0, self.n_int, tdims)
-                ke, nke = self._tile_keys(self.n_int, self.n_loc, self._ext_tdims)
-                part = D.tile_partition(torch.cat([ki, ke + nki * p]), (nki + nke) * p)
+                part, _ = self._ext_partition(self.TILE_TARGET_ROWS, ki, nki * p)
         self._tile_parts[which] = part
         return part
 
