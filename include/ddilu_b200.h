@@ -42,6 +42,11 @@ int ddilu_sort_pairs_i32(int *keys, int *vals, int *keys_alt, int *vals_alt, lon
  * mode 0: y = A x; 1: y = b - A x; 2: y = b + A x.  y/b are indexed by row. */
 int ddilu_spmv_csr_f64(int row_begin, int row_end, const int *row_ptr, const int *col_idx, const double *values,
                        const double *x, const double *b, double *y, int mode, void *stream);
+/* the same with the average row length of the range as a hint (0 = unknown): picks rows per CTA and the
+ * shared-memory stage so that 27-point / ILUT-length rows still take the staged path and short rows get
+ * full occupancy */
+int ddilu_spmv_csr_f64_tuned(int row_begin, int row_end, const int *row_ptr, const int *col_idx, const double *values,
+                             const double *x, const double *b, double *y, int mode, double avg_row_len, void *stream);
 
 /* ---- level schedules (absent from the reference: SPEC.md:112; definition in
  * lev[i] = 1 + max lev[j] over the dependencies of row i) */

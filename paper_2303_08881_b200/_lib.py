@@ -28,6 +28,7 @@ SIGNATURES = {
     "ddilu_sort_tmp_elems": (_L, [_L]),
     "ddilu_sort_pairs_i32": (_I, [_P, _P, _P, _P, _L, _I, _P, _P]),
     "ddilu_spmv_csr_f64": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P]),
+    "ddilu_spmv_csr_f64_tuned": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _D, _P]),
     "ddilu_levels": (_I, [_I, _P, _P, _I, _P, _P, _P]),
     "ddilu_schedule_build": (_I, [_I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),

@@ -15,35 +15,35 @@
 
 namespace ddilu {
 
-constexpr int SPMV_ROWS = 256;       // rows (= threads) per CTA
-constexpr int SPMV_STAGE = 4096;     // products staged per CTA (32 KB)
 constexpr int SPMV_UNROLL = 8;       // entries per thread and round
 
 // mode 0: y = A x      mode 1: y = b - A x      mode 2: y = b + A x
-template <int MODE>
-__global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const int *__restrict__ rp,
-                                                         const int *__restrict__ ci, const double *__restrict__ val,
-                                                         const double *__restrict__ x, const double *__restrict__ b,
-                                                         double *__restrict__ y) {
-    __shared__ double prod[SPMV_STAGE];
-    __shared__ int srp[SPMV_ROWS + 1];
-    const int row0 = r0 + blockIdx.x * SPMV_ROWS;
-    const int nrows = min(SPMV_ROWS, r1 - row0);
+// ROWS rows (= threads) per CTA, STAGE products staged per CTA: chosen by the launcher from the average
+// row length so that a CTA's entries fit the stage and as many CTAs as possible are resident
+template <int MODE, int ROWS, int STAGE>
+__global__ void __launch_bounds__(ROWS) spmv_stream(int r0, int r1, const int *__restrict__ rp,
+                                                    const int *__restrict__ ci, const double *__restrict__ val,
+                                                    const double *__restrict__ x, const double *__restrict__ b,
+                                                    double *__restrict__ y) {
+    __shared__ double prod[STAGE];
+    __shared__ int srp[ROWS + 1];
+    const int row0 = r0 + blockIdx.x * ROWS;
+    const int nrows = min(ROWS, r1 - row0);
     if (threadIdx.x < nrows) srp[threadIdx.x] = rp[row0 + threadIdx.x];
     if (threadIdx.x == 0) srp[nrows] = rp[row0 + nrows];
     __syncthreads();
     const int e0 = srp[0], e1 = srp[nrows];
     const int row = row0 + threadIdx.x;
-    if (e1 - e0 <= SPMV_STAGE) {
+    if (e1 - e0 <= STAGE) {
         // all (column, value) loads of a round in flight together, then all the x gathers: eight
         // independent 2-deep load chains per thread instead of one (HBM latency x bandwidth needs ~44 KB
         // in flight per SM)
-        for (int base = e0 + threadIdx.x; base < e1; base += SPMV_UNROLL * SPMV_ROWS) {
+        for (int base = e0 + threadIdx.x; base < e1; base += SPMV_UNROLL * ROWS) {
             int c[SPMV_UNROLL];
             double v[SPMV_UNROLL], xv[SPMV_UNROLL];
 #pragma unroll
             for (int u = 0; u < SPMV_UNROLL; ++u) {
-                const int e = base + u * SPMV_ROWS;
+                const int e = base + u * ROWS;
                 const bool in = e < e1;
                 c[u] = in ? ci[e] : -1;
                 v[u] = in ? val[e] : 0.0;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const i
             for (int u = 0; u < SPMV_UNROLL; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
 #pragma unroll
             for (int u = 0; u < SPMV_UNROLL; ++u)
-                if (c[u] >= 0) prod[base + u * SPMV_ROWS - e0] = v[u] * xv[u];
+                if (c[u] >= 0) prod[base + u * ROWS - e0] = v[u] * xv[u];
         }
         __syncthreads();
         if (threadIdx.x < nrows) {
@@ -71,23 +71,39 @@ __global__ void __launch_bounds__(SPMV_ROWS) spmv_stream(int r0, int r1, const i
     }
 }
 
+template <int ROWS, int STAGE>
+static int spmv_launch(int row_begin, int row_end, const int *rp, const int *ci, const double *val, const double *x,
+                       const double *b, double *y, int mode, cudaStream_t st) {
+    const int grid = div_up(row_end - row_begin, ROWS);
+    if (mode == 0) spmv_stream<0, ROWS, STAGE><<<grid, ROWS, 0, st>>>(row_begin, row_end, rp, ci, val, x, b, y);
+    else if (mode == 1) spmv_stream<1, ROWS, STAGE><<<grid, ROWS, 0, st>>>(row_begin, row_end, rp, ci, val, x, b, y);
+    else spmv_stream<2, ROWS, STAGE><<<grid, ROWS, 0, st>>>(row_begin, row_end, rp, ci, val, x, b, y);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
 }  // namespace ddilu
 
 using namespace ddilu;
 
-extern "C" int ddilu_spmv_csr_f64(int row_begin, int row_end, const int *row_ptr, const int *col_idx,
-                                  const double *values, const double *x, const double *b, double *y, int mode,
-                                  void *stream) {
+/* avg_row_len: entries per row of the range (0 = unknown) -- picks rows per CTA and stage size */
+extern "C" int ddilu_spmv_csr_f64_tuned(int row_begin, int row_end, const int *row_ptr, const int *col_idx,
+                                        const double *values, const double *x, const double *b, double *y, int mode,
+                                        double avg_row_len, void *stream) {
     if (row_end <= row_begin) return DDILU_OK;
     if ((mode != 0 && !b) || mode < 0 || mode > 2) return DDILU_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    int grid = div_up(row_end - row_begin, SPMV_ROWS);
-    if (mode == 0)
-        spmv_stream<0><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
-    else if (mode == 1)
-        spmv_stream<1><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
-    else
-        spmv_stream<2><<<grid, SPMV_ROWS, 0, st>>>(row_begin, row_end, row_ptr, col_idx, values, x, b, y);
-    DDILU_LAUNCH_CHECK();
-    return DDILU_OK;
+    if (avg_row_len > 0.0 && avg_row_len <= 7.5)
+        return spmv_launch<256, 2048>(row_begin, row_end, row_ptr, col_idx, values, x, b, y, mode, st);
+    if (avg_row_len <= 0.0 || avg_row_len <= 15.0)
+        return spmv_launch<256, 4096>(row_begin, row_end, row_ptr, col_idx, values, x, b, y, mode, st);
+    if (avg_row_len <= 30.0)
+        return spmv_launch<128, 4096>(row_begin, row_end, row_ptr, col_idx, values, x, b, y, mode, st);
+    return spmv_launch<64, 4096>(row_begin, row_end, row_ptr, col_idx, values, x, b, y, mode, st);
+}
+
+extern "C" int ddilu_spmv_csr_f64(int row_begin, int row_end, const int *row_ptr, const int *col_idx,
+                                  const double *values, const double *x, const double *b, double *y, int mode,
+                                  void *stream) {
+    return ddilu_spmv_csr_f64_tuned(row_begin, row_end, row_ptr, col_idx, values, x, b, y, mode, 0.0, stream);
 }

@@ -118,7 +118,8 @@ def spmv(a: DeviceCsr, x: torch.Tensor, out: torch.Tensor, b: torch.Tensor | Non
          r0: int = 0, r1: int | None = None):
     """out[r0:r1] = A x | b - A x | b + A x  (rows r0..r1)."""
     r1 = a.n_rows if r1 is None else r1
-    call("ddilu_spmv_csr_f64", int(r0), int(r1), a.rp, a.ci, a.val, x, b, out, int(mode))
+    avg = a.nnz / a.n_rows if a.n_rows else 0.0     # row-length hint: rows per CTA / stage size
+    call("ddilu_spmv_csr_f64_tuned", int(r0), int(r1), a.rp, a.ci, a.val, x, b, out, int(mode), float(avg))
     return out
 
 
