@@ -805,6 +805,8 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 *comp_done = k + 1;
             }
         }
+        if (dbg && lane == 0)   // boundary waits of ALL compute warps (each level's wait is seen by its owner only)
+            atomicAdd((unsigned long long *)(dbg + 8LL * blockIdx.x + 6), (unsigned long long)t_wait_ext);
         if (dbg && cw == 0 && lane == 0) {
             long long *o = dbg + 8LL * blockIdx.x;
             o[0] = clock64() - t_start;   // whole CTA life

@@ -95,11 +95,18 @@ class LocalSystem:
 
     # ------------------------------------------------------------------ tiles
     TILE_TARGET_ROWS = 512
+    TILE_DIMS_3D = (8, 8, 8)      # interior box tile (x, y, z nodes); 512 rows, 22 wavefront levels on a 7-point grid
 
     def _tile_keys(self, r0: int, r1: int, tdims):
         lay = self.layout
         owner = lay._owner_d if lay.p > 1 else None
         return D.box_tile_keys(self.nodes[r0:r1], r1 - r0, lay.grid_hint, tdims, owner)
+
+    def _int_tdims(self):
+        nd = len(self.layout.grid_hint)
+        if nd == 3:
+            return list(self.TILE_DIMS_3D)
+        return [32, 16] if nd == 2 else [self.TILE_TARGET_ROWS]
 
     def _ext_partition(self, max_rows: int, int_keys, int_range: int):
         """Box tiles of the interface rows with at most max_rows rows each (edge 32, 16, ... until it
@@ -135,9 +142,7 @@ class LocalSystem:
         p = max(1, lay.p)
         part = None
         if which == "int" and self.n_int:
-            e = {3: 8, 2: 16, 1: self.TILE_TARGET_ROWS}[nd]
-            tdims = [2 * e if (nd == 2 and a == 0) else e for a in range(nd)]
-            keys, nk = self._tile_keys(0, self.n_int, tdims)
+            keys, nk = self._tile_keys(0, self.n_int, self._int_tdims())
             part = D.tile_partition(keys, nk * p)
         elif which == "ext" and self.n_ext:
             part, self._ext_tdims = self._ext_partition(D.TILE_MAX_ROWS, 0, 0)
@@ -147,9 +152,7 @@ class LocalSystem:
             elif self.tile_part("int") is not None:
                 # interface rows of a full-block factor also depend on interior rows (W): keep their tiles at
                 # <= 512 rows so that tile + boundary dependencies fit the shared-memory budget
-                e = {3: 8, 2: 16, 1: self.TILE_TARGET_ROWS}[nd]
-                tdims = [2 * e if (nd == 2 and a == 0) else e for a in range(nd)]
-                ki, nki = self._tile_keys(0, self.n_int, tdims)
+                ki, nki = self._tile_keys(0, self.n_int, self._int_tdims())
                 part, _ = self._ext_partition(self.TILE_TARGET_ROWS, ki, nki * p)
         self._tile_parts[which] = part
         return part

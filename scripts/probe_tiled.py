@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--no-sell", action="store_true")
     ap.add_argument("--grid-cap", type=int, default=0)
     ap.add_argument("--nap", type=int, default=-1)
+    ap.add_argument("--tile", default="")
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
@@ -58,6 +59,9 @@ def main():
     query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
     if args.nap >= 0:
         query("ddilu_tiled_set_tuning", b"nap_ns", args.nap)
+    if args.tile:
+        from paper_2303_08881_b200.precond import LocalSystem
+        LocalSystem.TILE_DIMS_3D = tuple(int(v) for v in args.tile.split(","))
     dims = (args.n,) * 3
     a = P.aniso3d(*dims)
     a.device()
@@ -90,7 +94,7 @@ def main():
                            smem=int(query("ddilu_tiled_smem_bytes", ts.stat_max, ts.tmax, ts.emax)))
                 cfgs = [(128, 0)]
                 if args.sweep:
-                    cfgs = [(128, k) for k in (0, 1, 2)]
+                    cfgs = [(128, k) for k in (0, 1, 2, 3)]
                 for ct, cps in cfgs:
                     query("ddilu_tiled_set_tuning", b"ctas_per_sm", cps)
                     t = timed(solve_t, flush=flush)
@@ -106,7 +110,7 @@ def main():
                     rec[f"tiled_c{ct}_k{cps}_frac"] = round(nbytes / t / 1e9 / PEAK, 4)
                 query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
             if ts is not None:
-                for cps in ((0, 1) if args.sweep else (0,)):
+                for cps in ((0, 1, 2, 3) if args.sweep else (0,)):
                     query("ddilu_tiled_set_tuning", b"ctas_per_sm", cps)
                     dbg = torch.zeros(8 * 148 * 8, dtype=torch.int64, device="cuda")
                     query("ddilu_tiled_set_debug", dbg.data_ptr())
@@ -117,7 +121,7 @@ def main():
                     d = d[d[:, 5] > 0]
                     rec[f"dbg_k{cps}"] = dict(
                         ctas=int(len(d)), life_us=float(d[:, 0].mean() / 1965), wait_tile_us=float(d[:, 1].mean() / 1965),
-                        wait_ext_us=float(d[:, 2].mean() / 1965), tiles_us=float(d[:, 3].mean() / 1965),
+                        wait_ext_us=float(d[:, 2].mean() / 1965), wait_ext_all_warps_us=float(d[:, 6].mean() / 1965), tiles_us=float(d[:, 3].mean() / 1965),
                         levels=float(d[:, 4].mean()), tiles=float(d[:, 5].mean()),
                         cyc_per_level=float(((d[:, 3] - d[:, 1]) / np.maximum(1, d[:, 4])).mean()))
                 query("ddilu_tiled_set_tuning", b"ctas_per_sm", 0)
