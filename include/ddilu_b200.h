@@ -128,7 +128,7 @@ int ddilu_prefill(int n, const int *a_rp, const int *a_ci, const double *a_v, co
  *   tile_edges_*  : (producer tile, consumer tile) pairs of the cross-tile dependencies
  *   tile_relax    : `passes` sweeps of tlev[c] = max(tlev[c], tlev[p]+1); flags[0] = last sweep
  *                   changed something, flags[1] = cycle (a level reached n_tiles)
- *   tile_build    : fill = 0: size of every tile's static block (16-byte units) -> blk16[q],
+ *   tile_build    : item_warps = 4 (rotating-warp kernel), 1 (warp-per-tile kernel) or 0 (lean records, rows with <= 3 dependencies); fill = 0: size of every tile's static block (16-byte units) -> blk16[q],
  *                   stats[0..2] = max rows, max externals, max bytes, stats[4] = longest row (kmax); fill = 1: blk16 holds the
  *                   scanned offsets, blocks are written to blob, stats[3] = first bad pivot row
  *   sptrsv_tiled  : x = T^-1 b; one cooperative launch */
@@ -148,9 +148,19 @@ int ddilu_tile_relax(long long n_edges, const int *edges, int n_tiles, int *tlev
                      void *stream);
 int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_ptr, const int *trows,
                      const int *tile_of, const int *tpos, const int *row_ptr, const int *col_idx,
-                     const double *values, const int *glev, int upper, int has_diag, int *blk16, int *stats,
-                     unsigned char *blob, void *stream);
+                     const double *values, const int *glev, int upper, int has_diag, int item_warps, int *blk16,
+                     int *stats, unsigned char *blob, void *stream);
 long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax);
+/* warp-per-tile variant of the same solve (static blocks built with item_warps = 1): every warp owns a
+ * stream of tiles, no named barriers, no helper warps; as many independent warps per SM as shared
+ * memory allows */
+long long ddilu_warptile_smem_per_warp(int stat_max, int tmax, int emax);
+/* lean variant for rows with <= 3 dependencies (static blocks built with item_warps = 0: pre-digested
+ * 16-byte row records, ~40 instructions per level) */
+int ddilu_sptrsv_lean(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
+                      int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
+int ddilu_sptrsv_warptile(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
+                          int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 /* self-check of the division the U solves use (pivot reciprocal + two FMA corrections) against the
  * IEEE division on n pseudo-random / adversarial operand pairs; *mismatch = pairs whose bits differ */
 int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigned long long *mismatch, void *stream);

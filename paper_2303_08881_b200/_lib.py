@@ -52,8 +52,11 @@ SIGNATURES = {
     "ddilu_tile_edges_count": (_I, [_I, _P, _P, _I, _P, _P, _P]),
     "ddilu_tile_edges_fill": (_I, [_I, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_tile_relax": (_I, [_L, _P, _I, _P, _P, _I, _P]),
-    "ddilu_tile_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
+    "ddilu_tile_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P]),
     "ddilu_tiled_smem_bytes": (_L, [_I, _I, _I]),
+    "ddilu_warptile_smem_per_warp": (_L, [_I, _I, _I]),
+    "ddilu_sptrsv_lean": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_fastdiv_selftest": (_I, [_L, ctypes.c_ulonglong, _P, _P]),
     "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),

@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(TILE_MAX_ROWS)
 tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ tile_ptr,
            const int *__restrict__ trows, const int *__restrict__ tile_of, const int *__restrict__ tpos,
            const int *__restrict__ rp, const int *__restrict__ ci, const double *__restrict__ val,
-           const int *__restrict__ glev, int upper, int has_diag, int *blk16, int *stats, unsigned char *blob) {
+           const int *__restrict__ glev, int upper, int has_diag, int nw, int *blk16, int *stats,
+           unsigned char *blob) {
     __shared__ int s_key[TILE_MAX_ROWS];     // level of local row i, later level index of slot s
     __shared__ int s_slot[TILE_MAX_ROWS];    // slot of local row i
     __shared__ int s_skey[TILE_MAX_ROWS];    // level key of slot s
@@ -260,28 +261,32 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
     __syncthreads();
     // work items: level l is cut into chunks of 32 rows, chunk c belongs to compute warp (l + c) mod 4;
     // every warp gets the ordered list of its chunks, so the solve kernel never scans level tables
+    // (nw = 4: the rotating-warp kernel; nw = 1: the warp-per-tile kernel, one list in (level, chunk) order)
     int cntw[TILE_NW], basew[TILE_NW], totw[TILE_NW];
 #pragma unroll
     for (int cwp = 0; cwp < TILE_NW; ++cwp) {
         cntw[cwp] = 0;
-        if (i < n_lev) {
+        if (i < n_lev && cwp < nw) {
             const int nch = (s_lstart[i + 1] - s_lstart[i] + 31) >> 5;
-            const int c0 = (cwp - i) & (TILE_NW - 1);
-            cntw[cwp] = c0 < nch ? (nch - c0 + TILE_NW - 1) / TILE_NW : 0;
+            const int c0 = (cwp - i) & (nw - 1);
+            cntw[cwp] = c0 < nch ? (nch - c0 + nw - 1) / nw : 0;
         }
     }
 #pragma unroll
     for (int cwp = 0; cwp < TILE_NW; ++cwp) basew[cwp] = block_excl_scan(cntw[cwp], &totw[cwp], s_wsum);
     const int n_items = totw[0] + totw[1] + totw[2] + totw[3];
-    // layout
+    // layout.  nw == 0 ("lean", rows with <= 3 dependencies only): no work items; per level {slot start,
+    // externals needed}, per slot two 16-byte records {a0, a1} and {a2, x-slot indices 0..2} (padding:
+    // coefficient 0, the tile's zero slot), 32 spare records so that idle lanes may read past a level.
+    const bool lean = nw == 0;
     const int off_lst = TILE_HDR_BYTES;
-    const int off_items = off_lst + pad16(4 * (n_lev + 1));
-    const int off_rows = off_items + 32 * n_items;
+    const int off_items = off_lst + pad16((lean ? 8 : 4) * (n_lev + 1));
+    const int off_rows = off_items + (lean ? 0 : 32 * n_items);
     const int off_ext = off_rows + pad16(4 * T);
     const int off_piv = off_ext + pad16(4 * n_ext);
     const int off_val = off_piv + (has_diag ? 16 * T : 0);   // (pivot, reciprocal) pairs
-    const int off_code = off_val + pad16(8 * n_ent);
-    const int bytes = off_code + pad16(2 * n_ent);
+    const int off_code = off_val + (lean ? 16 * (T + 32) : pad16(8 * n_ent));
+    const int bytes = off_code + (lean ? 16 * (T + 32) : pad16(2 * n_ent));
     if (!FILL) {
         if (i == 0) {
             blk16[q] = bytes >> 4;
@@ -298,7 +303,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
     auto next_level_of = [&](int cwp, int from) {
         for (int l = from; l < n_lev; ++l) {
             const int nch = (s_lstart[l + 1] - s_lstart[l] + 31) >> 5;
-            if (((cwp - l) & (TILE_NW - 1)) < nch) return l;
+            if (((cwp - l) & (nw - 1)) < nch) return l;
         }
         return n_lev + 1;
     };
@@ -319,8 +324,62 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
             default: break;
         }
         if (i >= H_NITEMS && i < H_NITEMS + TILE_NW) v = totw[i - H_NITEMS];
-        if (i >= H_FIRST && i < H_FIRST + TILE_NW) v = next_level_of(i - H_FIRST, 0);
+        if (i >= H_FIRST && i < H_FIRST + nw) v = next_level_of(i - H_FIRST, 0);
         hdr[i] = v;
+    }
+    if (lean) {
+        int2 *lvl2 = (int2 *)(blk + off_lst);
+        if (i <= n_lev) lvl2[i] = make_int2(s_lstart[i], i < n_lev ? s_eoff[s_lstart[i + 1]] : n_ext);
+        double2 *recA = (double2 *)(blk + off_val);
+        uint4 *recB = (uint4 *)(blk + off_code);
+        if (i < 32) {   // spare records
+            recA[T + i] = make_double2(0.0, 0.0);
+            recB[T + i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        {
+            const int tails[3][2] = {{off_lst + 8 * (n_lev + 1), off_rows}, {off_rows + 4 * T, off_ext},
+                                     {off_ext + 4 * n_ext, off_piv}};
+            if (i < 3)
+                for (int p = tails[i][0]; p < tails[i][1]; ++p) blk[p] = 0;
+        }
+        if (!active) return;
+        ((int *)(blk + off_rows))[slot] = row;
+        int *ext_out = (int *)(blk + off_ext);
+        const unsigned zs = (unsigned)(T + n_ext);
+        double av[3] = {0.0, 0.0, 0.0};
+        unsigned ix[3] = {zs, zs, zs};
+        int kk = 0, e = s_eoff[slot];
+        double diag = 1.0;
+        bool seen = false;
+        for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
+            const int j = ci[k];
+            if (upper ? j > row : j < row) {
+                unsigned code;
+                if (tile_of[j] == t) {
+                    code = (unsigned)s_slot[tpos[j] - base];
+                } else {
+                    code = (unsigned)(T + e);
+                    ext_out[e] = j;
+                    ++e;
+                }
+                if (kk < 3) {
+                    av[kk] = val[k];
+                    ix[kk] = code;
+                }
+                ++kk;
+            } else if (j == row) {
+                diag = val[k];
+                seen = true;
+            }
+        }
+        recA[slot] = make_double2(av[0], av[1]);
+        recB[slot] = make_uint4((unsigned)__double2loint(av[2]), (unsigned)__double2hiint(av[2]), ix[0] | (ix[1] << 16),
+                                ix[2]);
+        if (has_diag) {
+            ((double2 *)(blk + off_piv))[slot] = make_double2(diag, safe_reciprocal(diag));
+            if (!seen || fabs(diag) < 1e-300) atomicMin(stats + 3, row);
+        }
+        return;
     }
     int *lst = (int *)(blk + off_lst);
     if (i <= n_lev) lst[i] = s_lstart[i];
@@ -330,11 +389,12 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
         int wbase = 0;
 #pragma unroll
         for (int cwp = 0; cwp < TILE_NW; ++cwp) {
+            if (cwp >= nw) break;
             int4 *it = (int4 *)(blk + off_items) + 2 * (wbase + basew[cwp]);
-            const int c0 = (cwp - i) & (TILE_NW - 1);
+            const int c0 = (cwp - i) & (nw - 1);
             int nth = 0;
-            for (int c = c0; c < nch; c += TILE_NW, ++nth) {
-                const bool first = c == c0, last = c + TILE_NW >= nch;
+            for (int c = c0; c < nch; c += nw, ++nth) {
+                const bool first = c == c0, last = c + nw >= nch;
                 int n_arr = 0;
                 if (last) {
                     const int nxt = next_level_of(cwp, i + 1);
@@ -819,6 +879,280 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-tile variant (tiles whose levels are mostly <= 32 rows wide: 8x8x4 interior boxes, 16x16
+// interface patches).  Every WARP owns a stream of tiles and is completely independent of the other
+// warps of its CTA: its own 2-deep TMA ring, its own x slots, no named barrier, no helper warps.  A level
+// is one `__syncwarp()` away from the next, the operands of the next chunk are loaded (shared memory ->
+// registers) before the current chain starts, finished rows go straight to L2 (no barrier follows a
+// global store here), boundary dependencies are polled 32 at a time with the next batch already in
+// flight.  Latencies that a warp cannot hide itself (right-hand-side gather, TMA, polls) are hidden by
+// the other 6-9 resident warps of the SM, which is what the rotating-warp kernel could not do: it keeps
+// at most 4 level chains per SM in flight, this one 7-9.
+// Execution barrier of a warp WITHOUT the memory-fence semantics of __syncwarp(): a shuffle makes the
+// lanes converge, and shared-memory accesses of one warp are performed in issue order, so the level's
+// STS are visible to the next level's LDS.  (__syncwarp / bar.warp.sync additionally waits until the
+// lanes' outstanding GLOBAL stores are performed -- an L2 round trip per level, measured.)
+__device__ __forceinline__ void warp_converge() {
+    int t = 0;
+    asm volatile("shfl.sync.idx.b32 %0, %0, 0, 0x1f, 0xffffffff;" : "+r"(t)::"memory");
+}
+
+// Boundary dependencies of a warp's tile.  At tile start every dependency is polled ONCE, 8 per lane in
+// flight (the producers are usually long finished): the value -- or the not-ready pattern -- goes to the
+// tile's x slots.  A level that needs dependency e < need re-polls only what is still missing.
+__device__ __forceinline__ void ext_prefetch(const double *x, const int *ext, int n_ext, double *xe, int lane) {
+    for (int e0 = 0; e0 < n_ext; e0 += 256) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 32 + lane;
+            v[u] = e < n_ext ? ld_l2(x + ext[e]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 32 + lane;
+            if (e < n_ext) xe[e] = v[u];
+        }
+    }
+}
+__device__ __forceinline__ int ext_deliver(const double *x, const int *ext, int n_ext, double *xe, int lane, int have,
+                                           int need) {
+    while (need > have) {
+        const int e = have + lane;
+        if (e < n_ext) {
+            double v = xe[e];
+            if (is_sentinel(v)) {
+                do v = ld_l2(x + ext[e]); while (is_sentinel(v));
+                xe[e] = v;
+            }
+        }
+        have += 32;
+    }
+    warp_converge();
+    return have;
+}
+
+template <int KP>
+struct WarpItem {
+    int need, cnt, ent0, w, K, row;
+    uint32_t xaddr[KP], saddr;
+    double a[KP];
+    double rhs, piv, rinv;
+};
+
+template <bool HAS_DIAG, int KP>
+__device__ __forceinline__ void warp_item_load(WarpItem<KP> &r, const int4 *it, int lane, const double *xsk, int zslot,
+                                               const double *piv, const int *rows, const unsigned short *codes,
+                                               const double *vals) {
+    const int4 A = it[0], B = it[1];   // A = {slot0, ent0, w, K}, B = {level, need, flags, n_arr}
+    r.need = B.y;
+    r.cnt = B.z & 0xff;
+    r.ent0 = A.y;
+    r.w = A.z;
+    r.K = A.w;
+    const bool act = lane < r.cnt;
+    const int s = A.x + lane;
+    r.saddr = smem_u32(xsk + s);
+    r.row = act ? rows[s] : 0;
+    r.rhs = act ? xsk[s] : 1.0;
+    const double2 pr = (HAS_DIAG && act) ? ((const double2 *)piv)[s] : make_double2(1.0, 1.0);
+    r.piv = pr.x;
+    r.rinv = pr.y;
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
+        const bool in = act && u < A.w;
+        const int c = in ? (int)codes[A.y + u * A.z + lane] : zslot;
+        r.a[u] = in ? vals[A.y + u * A.z + lane] : 0.0;
+        r.xaddr[u] = smem_u32(xsk + c);
+    }
+}
+
+template <bool HAS_DIAG, int KP>
+__global__ void __launch_bounds__(512)
+sptrsv_warptile(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
+                int xcap, int per_warp, const double *__restrict__ b, double *x) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    unsigned char *base = smem + (size_t)warp * per_warp;
+    unsigned char *stat = base;
+    double *xs = (double *)(base + 2 * (size_t)stat_max);
+    uint64_t *mbar = (uint64_t *)(xs + xcap);
+    const long long gw = (long long)blockIdx.x * wpb + warp, nwt = (long long)gridDim.x * wpb;
+    const int nk = gw < n_tiles ? (int)((n_tiles - gw + nwt - 1) / nwt) : 0;   // my tiles: gw + k * nwt
+    if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int k) {
+        const long long qq = gw + (long long)k * nwt;
+        const int o0 = blk_off16[qq], o1 = blk_off16[qq + 1];
+        const uint32_t bytes = (uint32_t)(o1 - o0) << 4;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the slot was read by this warp before
+        mbar_expect_tx(&mbar[k & 1], bytes);
+        bulk_g2s(stat + (size_t)(k & 1) * stat_max, blob + 16LL * o0, bytes, &mbar[k & 1]);
+    };
+    if (lane == 0 && nk > 0) issue(0);
+    for (int k = 0; k < nk; ++k) {
+        if (lane == 0 && k + 1 < nk) issue(k + 1);   // its slot held tile k-1, which this warp has finished
+        mbar_wait(&mbar[k & 1], (uint32_t)((k >> 1) & 1));
+        const unsigned char *blk = stat + (size_t)(k & 1) * stat_max;
+        const int *hdr = (const int *)blk;
+        const int T = hdr[H_T], n_ext = hdr[H_NEXT], n_it = hdr[H_NITEMS];
+        const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+        const int *ext = (const int *)(blk + hdr[H_OFF_EXT]);
+        const double *piv = (const double *)(blk + hdr[H_OFF_PIV]);
+        const double *vals = (const double *)(blk + hdr[H_OFF_VAL]);
+        const unsigned short *codes = (const unsigned short *)(blk + hdr[H_OFF_CODE]);
+        const int4 *items = (const int4 *)(blk + hdr[H_OFF_ITEMS]);
+        const int zslot = T + n_ext;
+        double *xe = xs + T;
+        int have = 0;
+        ext_prefetch(x, ext, n_ext, xe, lane);
+        for (int s0 = 0; s0 < T; s0 += 256) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u * 32 + lane;
+                v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u * 32 + lane;
+                if (s < T) xs[s] = v[u];
+            }
+        }
+        if (lane == 0) xs[zslot] = 0.0;
+        __syncwarp();
+        WarpItem<KP> cur, nxt;
+        if (n_it) warp_item_load<HAS_DIAG, KP>(cur, items, lane, xs, zslot, piv, rows, codes, vals);
+        for (int q = 0; q < n_it; ++q) {
+            // the next chunk never belongs to this level's consumers' producers: its right-hand side and
+            // coefficients can be read now (its x operands are only ADDRESSES here)
+            if (q + 1 < n_it)
+                warp_item_load<HAS_DIAG, KP>(nxt, items + 2 * (q + 1), lane, xs, zslot, piv, rows, codes, vals);
+            if (cur.need > have) have = ext_deliver(x, ext, n_ext, xe, lane, have, cur.need);
+            double xv[KP];
+#pragma unroll
+            for (int u = 0; u < KP; ++u) xv[u] = lds_f64(cur.xaddr[u]);
+            double sum = cur.rhs;
+#pragma unroll
+            for (int u = 0; u < KP; ++u) sum -= cur.a[u] * xv[u];
+            if (cur.K > KP) {   // long rows: the remaining entries straight from the static block
+                const unsigned short *cp = codes + cur.ent0 + lane;
+                const double *vp = vals + cur.ent0 + lane;
+                if (lane < cur.cnt)
+                    for (int kk = KP; kk < cur.K; ++kk) sum -= vp[kk * cur.w] * xs[cp[kk * cur.w]];
+            }
+            if (HAS_DIAG) sum = exact_div(sum, cur.piv, cur.rinv);
+            if (lane < cur.cnt) {
+                sts_f64(cur.saddr, sum);
+                st_l2(x + cur.row, scrub_sentinel(sum));
+            }
+            warp_converge();
+            cur = nxt;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Lean warp-per-tile kernel for factors whose rows have at most 3 dependencies (ILU(0) of 7-point
+// problems: the headline workload).  Same execution model as sptrsv_warptile (independent warps, own TMA
+// ring, own x slots, no barriers), but the static block holds PRE-DIGESTED 16-byte records per row
+// ({a0, a1}, {a2, three 16-bit x-slot indices}) so that a level costs ~40 instructions: a lone warp issues
+// dependent instructions at ~6-8 cycles each, so the instruction count IS the per-level latency.
+template <bool HAS_DIAG>
+__global__ void __launch_bounds__(512)
+sptrsv_lean(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
+            int xcap, int per_warp, const double *__restrict__ b, double *x) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    unsigned char *base = smem + (size_t)warp * per_warp;
+    unsigned char *stat = base;
+    double *xs = (double *)(base + 2 * (size_t)stat_max);
+    uint64_t *mbar = (uint64_t *)(xs + xcap);
+    const uint32_t xs_a = smem_u32(xs);
+    const long long gw = (long long)blockIdx.x * wpb + warp, nwt = (long long)gridDim.x * wpb;
+    const int nk = gw < n_tiles ? (int)((n_tiles - gw + nwt - 1) / nwt) : 0;   // my tiles: gw + k * nwt
+    if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int k) {
+        const long long qq = gw + (long long)k * nwt;
+        const int o0 = blk_off16[qq], o1 = blk_off16[qq + 1];
+        const uint32_t bytes = (uint32_t)(o1 - o0) << 4;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the slot was read by this warp before
+        mbar_expect_tx(&mbar[k & 1], bytes);
+        bulk_g2s(stat + (size_t)(k & 1) * stat_max, blob + 16LL * o0, bytes, &mbar[k & 1]);
+    };
+    if (lane == 0 && nk > 0) issue(0);
+    for (int k = 0; k < nk; ++k) {
+        if (lane == 0 && k + 1 < nk) issue(k + 1);   // its slot held tile k-1, which this warp has finished
+        mbar_wait(&mbar[k & 1], (uint32_t)((k >> 1) & 1));
+        const unsigned char *blk = stat + (size_t)(k & 1) * stat_max;
+        const int *hdr = (const int *)blk;
+        const int T = hdr[H_T], n_ext = hdr[H_NEXT], n_lev = hdr[H_NLEV];
+        const int2 *lvl2 = (const int2 *)(blk + TILE_HDR_BYTES);
+        const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+        const int *ext = (const int *)(blk + hdr[H_OFF_EXT]);
+        const double2 *piv = (const double2 *)(blk + hdr[H_OFF_PIV]);
+        const double2 *recA = (const double2 *)(blk + hdr[H_OFF_VAL]);
+        const uint4 *recB = (const uint4 *)(blk + hdr[H_OFF_CODE]);
+        double *xe = xs + T;
+        int have = 0;
+        ext_prefetch(x, ext, n_ext, xe, lane);
+        for (int s0 = 0; s0 < T; s0 += 256) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u * 32 + lane;
+                v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u * 32 + lane;
+                if (s < T) xs[s] = v[u];
+            }
+        }
+        if (lane == 0) xs[T + n_ext] = 0.0;
+        __syncwarp();
+        int2 lv = lvl2[0];
+        for (int l = 0; l < n_lev; ++l) {
+            const int2 ln = lvl2[l + 1];
+            if (lv.y > have) have = ext_deliver(x, ext, n_ext, xe, lane, have, lv.y);
+            for (int c = lv.x; c < ln.x; c += 32) {
+                const int slot = c + lane;   // idle lanes read a neighbour's (or a spare) record and store nothing
+                const double2 A = recA[slot];
+                const uint4 B = recB[slot];
+                const double rhs = xs[slot];
+                const int row = rows[slot < T ? slot : 0];
+                const double x0 = lds_f64(xs_a + ((B.z & 0xffffu) << 3));
+                const double x1 = lds_f64(xs_a + ((B.z >> 16) << 3));
+                const double x2 = lds_f64(xs_a + ((B.w & 0xffffu) << 3));
+                double sum = rhs - A.x * x0;
+                sum -= A.y * x1;
+                sum -= __hiloint2double((int)B.y, (int)B.x) * x2;
+                if (HAS_DIAG) {
+                    const double2 pr = piv[slot < T ? slot : 0];
+                    if (slot >= ln.x) sum = 1.0;   // idle lanes: stay on the fast path of the division
+                    sum = exact_div(sum, pr.x, pr.y);
+                }
+                if (slot < ln.x) {
+                    xs[slot] = sum;
+                    st_l2(x + row, scrub_sentinel(sum));
+                }
+            }
+            warp_converge();
+            lv = ln;
+        }
+    }
+}
+
 }  // namespace ddilu
 
 using namespace ddilu;
@@ -933,17 +1267,19 @@ extern "C" int ddilu_tile_relax(long long n_edges, const int *edges, int n_tiles
 
 extern "C" int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_ptr, const int *trows,
                                 const int *tile_of, const int *tpos, const int *row_ptr, const int *col_idx,
-                                const double *values, const int *glev, int upper, int has_diag, int *blk16, int *stats,
-                                unsigned char *blob, void *stream) {
+                                const double *values, const int *glev, int upper, int has_diag, int item_warps,
+                                int *blk16, int *stats, unsigned char *blob, void *stream) {
     if (n_tiles <= 0) return DDILU_OK;
+    if (item_warps != 0 && item_warps != 1 && item_warps != TILE_NW) return DDILU_ERR_ARG;
+    const int nw = item_warps;
     if (fill)
         tile_build<true><<<n_tiles, TILE_MAX_ROWS, 0, ST(stream)>>>(n_tiles, tsched, tile_ptr, trows, tile_of, tpos,
                                                                    row_ptr, col_idx, values, glev, upper, has_diag,
-                                                                   blk16, stats, blob);
+                                                                   nw, blk16, stats, blob);
     else
         tile_build<false><<<n_tiles, TILE_MAX_ROWS, 0, ST(stream)>>>(n_tiles, tsched, tile_ptr, trows, tile_of, tpos,
                                                                     row_ptr, col_idx, values, glev, upper, has_diag,
-                                                                    blk16, stats, blob);
+                                                                    nw, blk16, stats, blob);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
@@ -986,5 +1322,73 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
     long long *dbg = g_tiled.debug;
     void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &tmax, &emax, &dbg, &b, &x};
     DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, threads, args, smem, st));
+    return DDILU_OK;
+}
+
+extern "C" long long ddilu_warptile_smem_per_warp(int stat_max, int tmax, int emax) {
+    long long b = 2LL * stat_max + 8LL * (tmax + emax + 2) + 16;
+    return (b + 127) & ~127LL;
+}
+
+/* warp-per-tile solve: static blocks must have been built with item_warps = 1 */
+extern "C" int ddilu_sptrsv_warptile(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max,
+                                     int tmax, int emax, int kmax, int has_diag, const double *b, double *x,
+                                     void *stream) {
+    cudaStream_t st = ST(stream);
+    if (n <= 0 || n_tiles <= 0) return DDILU_OK;
+    if (x == b || (stat_max & 15)) return DDILU_ERR_ARG;
+    int per_warp = (int)ddilu_warptile_smem_per_warp(stat_max, tmax, emax);
+    int xcap = tmax + emax + 2;
+    int wpb = (226 * 1024) / per_warp;     // one CTA per SM holding as many independent warps as fit
+    if (wpb > 16) wpb = 16;
+    if (g_tiled.ctas_per_sm > 0 && wpb > g_tiled.ctas_per_sm) wpb = g_tiled.ctas_per_sm;   // diagnostics: warps per SM
+    if (wpb < 1) return DDILU_ERR_ARG;
+    const size_t smem = (size_t)wpb * per_warp;
+    const int wide = kmax > 3 ? 1 : 0;
+    void *fns[2][2] = {{(void *)sptrsv_warptile<false, 3>, (void *)sptrsv_warptile<false, 6>},
+                       {(void *)sptrsv_warptile<true, 3>, (void *)sptrsv_warptile<true, 6>}};
+    void *fn = fns[has_diag ? 1 : 0][wide];
+    static size_t attr[2][2] = {{0, 0}, {0, 0}};
+    if (attr[has_diag ? 1 : 0][wide] < smem) {
+        DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[has_diag ? 1 : 0][wide] = smem;
+    }
+    long long grid = device_info().sm_count;
+    const long long need = ((long long)n_tiles + wpb - 1) / wpb;
+    if (grid > need) grid = need;
+    if (g_tiled.grid_cap > 0 && grid > g_tiled.grid_cap) grid = g_tiled.grid_cap;
+    DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
+    void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &xcap, &per_warp, &b, &x};
+    // cooperative: every warp waits on tiles of other warps, all CTAs must be resident
+    DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, wpb * 32, args, smem, st));
+    return DDILU_OK;
+}
+
+/* lean warp-per-tile solve (rows with <= 3 dependencies): static blocks built with item_warps = 0 */
+extern "C" int ddilu_sptrsv_lean(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max,
+                                 int tmax, int emax, int kmax, int has_diag, const double *b, double *x, void *stream) {
+    cudaStream_t st = ST(stream);
+    if (n <= 0 || n_tiles <= 0) return DDILU_OK;
+    if (x == b || (stat_max & 15) || kmax > 3) return DDILU_ERR_ARG;
+    int per_warp = (int)ddilu_warptile_smem_per_warp(stat_max, tmax + 32, emax);
+    int xcap = tmax + 32 + emax + 2;
+    int wpb = (226 * 1024) / per_warp;
+    if (wpb > 16) wpb = 16;
+    if (g_tiled.ctas_per_sm > 0 && wpb > g_tiled.ctas_per_sm) wpb = g_tiled.ctas_per_sm;   // diagnostics: warps per SM
+    if (wpb < 1) return DDILU_ERR_ARG;
+    const size_t smem = (size_t)wpb * per_warp;
+    void *fn = has_diag ? (void *)sptrsv_lean<true> : (void *)sptrsv_lean<false>;
+    static size_t attr[2] = {0, 0};
+    if (attr[has_diag ? 1 : 0] < smem) {
+        DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[has_diag ? 1 : 0] = smem;
+    }
+    long long grid = device_info().sm_count;
+    const long long need = ((long long)n_tiles + wpb - 1) / wpb;
+    if (grid > need) grid = need;
+    if (g_tiled.grid_cap > 0 && grid > g_tiled.grid_cap) grid = g_tiled.grid_cap;
+    DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
+    void *args[] = {&n_tiles, &blk_off16, &blob, &stat_max, &xcap, &per_warp, &b, &x};
+    DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, wpb * 32, args, smem, st));
     return DDILU_OK;
 }

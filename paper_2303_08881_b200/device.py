@@ -194,6 +194,9 @@ class TriSolveError(ZeroDivisionError):
 # tiled triangular solve (csrc/tiled.cu)
 
 USE_TILED = True
+TILE_KERNEL = "rot"       # "rot": CTA-per-tile kernel with rotating compute warps (production);
+                          # "warp": warp-per-tile kernels (independent warps; lean records when rows have <= 3
+                          # dependencies) -- measured alternative, same throughput per SM
 TILE_MAX_ROWS = 1024
 TILE_SMEM_LIMIT = 112 * 1024      # per CTA: at least two CTAs per SM
 TILE_RELAX_BATCH = 8
@@ -228,6 +231,7 @@ class TileSched:
     kmax: int
     has_diag: bool
     bad_row: int
+    kind: str = "rot"        # which solve kernel the item lists were cut for
 
 
 def box_tile_keys(nodes: torch.Tensor | None, n: int, dims, tdims, owner: torch.Tensor | None):
@@ -294,27 +298,44 @@ def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: boo
     tsched = torch.arange(nt, dtype=I32, device=dev())
     sort_pairs_(tlev, tsched, max(1, int(n_tile_levels - 1).bit_length()))
     has_diag = not unit_diag
-    blk = zeros_i32(nt + 1)
-    stats = torch.tensor([0, 0, 0, INT_MAX, 0], dtype=I32, device=dev())
     args = (nt, tsched, part.tile_ptr, part.trows, part.tile_of, part.tpos, t.rp, t.ci, t.val, lev, int(upper),
             int(has_diag))
-    call("ddilu_tile_build", 0, *args, blk, stats, None)
-    tmax, emax, stat_max, _, kmax = (int(v) for v in stats.cpu().numpy())
-    if tmax + emax + 2 >= 0xFFFF or query("ddilu_tiled_smem_bytes", stat_max, tmax, emax) > TILE_SMEM_LIMIT:
+    ITEM_WARPS = {"lean": 0, "warp": 1, "rot": 4}
+
+    def count(kind):
+        blk = zeros_i32(nt + 1)
+        stats = torch.tensor([0, 0, 0, INT_MAX, 0], dtype=I32, device=dev())
+        call("ddilu_tile_build", 0, *args, ITEM_WARPS[kind], blk, stats, None)
+        return blk, stats, [int(v) for v in stats.cpu().numpy()]
+
+    # kernel choice: lean records (rows with <= 3 dependencies) > warp-per-tile > CTA-per-tile, by what fits
+    kind = "lean" if TILE_KERNEL == "warp" else TILE_KERNEL
+    blk, stats, (tmax, emax, stat_max, _, kmax) = count(kind)
+    if tmax + emax + 34 >= 0xFFFF:
+        return None
+    if kind == "lean" and (kmax > 3 or query("ddilu_warptile_smem_per_warp", stat_max, tmax + 32, emax) > 226 * 1024):
+        kind = "warp"
+        blk, stats, (tmax, emax, stat_max, _, kmax) = count(kind)
+    if kind == "warp" and (TILE_KERNEL != "warp" or
+                           query("ddilu_warptile_smem_per_warp", stat_max, tmax, emax) > 113 * 1024):
+        kind = "rot"        # fewer than two warps per SM would fit: the CTA-per-tile kernel shares one ring
+        blk, stats, (tmax, emax, stat_max, _, kmax) = count(kind)
+    if kind == "rot" and query("ddilu_tiled_smem_bytes", stat_max, tmax, emax) > TILE_SMEM_LIMIT:
         return None
     exclusive_scan_(blk, nt)
     total16 = int(blk[-1].item())
     blob = torch.empty(max(16, 16 * total16), dtype=torch.uint8, device=dev())
-    call("ddilu_tile_build", 1, *args, blk, stats, blob)
+    call("ddilu_tile_build", 1, *args, ITEM_WARPS[kind], blk, stats, blob)
     bad = int(stats[3].item())
-    return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, kmax, has_diag, bad)
+    return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, kmax, has_diag, bad, kind)
 
 
 def sptrsv_tiled(ts: TileSched, b: torch.Tensor, out: torch.Tensor, check: bool = False):
     if check and ts.bad_row != INT_MAX:
         raise TriSolveError(f"zero or missing diagonal at row {ts.bad_row}")
-    call("ddilu_sptrsv_tiled", ts.n, ts.n_tiles, ts.blk_off16, ts.blob, ts.stat_max, ts.tmax, ts.emax, ts.kmax,
-         int(ts.has_diag), b, out)
+    entry = {"lean": "ddilu_sptrsv_lean", "warp": "ddilu_sptrsv_warptile", "rot": "ddilu_sptrsv_tiled"}[ts.kind]
+    call(entry, ts.n, ts.n_tiles, ts.blk_off16, ts.blob, ts.stat_max, ts.tmax, ts.emax, ts.kmax, int(ts.has_diag),
+         b, out)
     return out
 
 

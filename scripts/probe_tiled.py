@@ -46,6 +46,8 @@ def main():
     ap.add_argument("--grid-cap", type=int, default=0)
     ap.add_argument("--nap", type=int, default=-1)
     ap.add_argument("--tile", default="")
+    ap.add_argument("--kernel", default="")
+    ap.add_argument("--wpb", type=int, default=0)
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
@@ -59,6 +61,8 @@ def main():
     query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
     if args.nap >= 0:
         query("ddilu_tiled_set_tuning", b"nap_ns", args.nap)
+    if args.kernel:
+        D.TILE_KERNEL = args.kernel
     if args.tile:
         from paper_2303_08881_b200.precond import LocalSystem
         LocalSystem.TILE_DIMS_3D = tuple(int(v) for v in args.tile.split(","))
@@ -91,8 +95,10 @@ def main():
             if ts is not None:
                 rec.update(tiles=ts.n_tiles, tile_levels=ts.n_tile_levels, tmax=ts.tmax, emax=ts.emax,
                            stat_max=ts.stat_max, blob_bytes=int(ts.blob.numel()),
-                           smem=int(query("ddilu_tiled_smem_bytes", ts.stat_max, ts.tmax, ts.emax)))
-                cfgs = [(128, 0)]
+                           kind=ts.kind,
+                           smem=int(query("ddilu_tiled_smem_bytes", ts.stat_max, ts.tmax, ts.emax)),
+                           smem_per_warp=int(query("ddilu_warptile_smem_per_warp", ts.stat_max, ts.tmax, ts.emax)))
+                cfgs = [(128, args.wpb)]
                 if args.sweep:
                     cfgs = [(128, k) for k in (0, 1, 2, 3)]
                 for ct, cps in cfgs:

@@ -32,8 +32,18 @@ def _factor_pairs(m):
     return out
 
 
+@pytest.fixture(params=["rot", "warp"])
+def tile_kernel(request):
+    """Run with the production CTA-per-tile kernel and with the warp-per-tile alternatives."""
+    from paper_2303_08881_b200 import device as D
+    old = D.TILE_KERNEL
+    D.TILE_KERNEL = request.param
+    yield request.param
+    D.TILE_KERNEL = old
+
+
 @pytest.mark.parametrize("dims,p", [((20, 20, 20), 8), ((24, 17, 9), 4), ((40, 40), 4), ((33, 33, 33), 1)])
-def test_tiled_solves_bit_exact(P, orc, dims, p):
+def test_tiled_solves_bit_exact(P, orc, dims, p, tile_kernel):
     import torch
     from paper_2303_08881_b200 import device as D
     a = P.aniso3d(*dims) if len(dims) == 3 else P.aniso2d(*dims)
@@ -46,6 +56,10 @@ def test_tiled_solves_bit_exact(P, orc, dims, p):
             if f.n == 0:
                 continue
             assert f._tl is not None and f._tu is not None, (pc, name, "factor did not tile")
+            if tile_kernel == "rot":
+                assert f._tl.kind == "rot" and f._tu.kind == "rot"
+            else:
+                assert f._tl.kind in ("lean", "warp") and f._tu.kind in ("lean", "warp")
             b = rng.standard_normal(f.n)
             bd = D.to_device_f64(b)
             lo = P.CsrMatrix.from_device(f.lower)
