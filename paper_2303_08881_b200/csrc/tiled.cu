@@ -6,14 +6,23 @@
 // Why a second kernel: the sync-free solve pays one L2 round trip (0.4-1.9 us)
 // per LEVEL because consecutive levels live in different warps / SMs.  Here a
 // CTA owns a tile of <= 1024 rows and walks the tile's levels with the tile's
-// part of x in SHARED memory (one named barrier per level, ~0.1 us); only the
-// dependencies that cross a tile boundary travel through L2, and those are
-// fetched by a dedicated polling warp ahead of the compute warps.  The tile's
-// matrix data (one contiguous "static block": level table, row ids, external
-// columns, pivots, values, 16-bit local column codes) arrives by one
-// cp.async.bulk (TMA) per tile into a 3-deep shared-memory ring, signalled
-// through an mbarrier; a feeder warp gathers the tile's right-hand side one
-// tile ahead.  Row sums keep the storage order of the reference: bit-exact.
+// part of x in SHARED memory; only the dependencies that cross a tile boundary
+// travel through L2.  Roles inside a CTA (sptrsv_tiled):
+//   warp 0  feeder   one cp.async.bulk (TMA) per tile of the tile's contiguous
+//                    "static block" (level starts, per-warp work items, row ids,
+//                    external columns, pivot pairs, values, 16-bit local column
+//                    codes) into a 2-deep shared-memory ring (mbarrier), then the
+//                    gather of the tile's right-hand side INTO its x slots
+//   warp 1  poller   polls the tile's boundary dependencies in L2 (x is preset to
+//                    an all-ones NaN: the value is its own flag), in the order
+//                    the levels need them
+//   warps 2-5 compute: level l is cut into chunks of 32 rows, chunk c belongs to
+//                    warp (l + c) mod 4; a warp holds its NEXT chunk's operands
+//                    in registers, syncs on the named barrier of the level
+//                    before, runs  x loads -> multiply/subtract chain -> store,
+//                    ARRIVES at this level's barrier (and at those of the levels
+//                    it skips) and only then sends the results to L2
+// Row sums keep the storage order of the reference: bit-exact.
 //
 // Deadlock freedom: tiles are listed in a topological order of the tile graph,
 // CTA c takes tiles c, c+G, c+2G, ... in that order and the launch is
@@ -35,7 +44,7 @@ constexpr int TILE_NW = 4;          // compute warps of the solve kernel (the it
 constexpr int ITEM_SYNC = 1 << 8;   // first chunk of this warp in a level >= 1: wait for the previous level
 constexpr int ITEM_PUBLISH = 1 << 9;   // chunk 0 of a level: tells the writer warp that the levels before are complete
 constexpr int TILE_NBUF = 2;
-constexpr int TILE_HELPERS = 96;   // warp 0: TMA + right-hand side, warp 1: external dependencies, warp 2: x -> L2
+constexpr int TILE_HELPERS = 64;   // warp 0: TMA + right-hand side, warp 1: external dependencies
 
 // header ints of a static block
 enum { H_T = 0, H_NLEV, H_NEXT, H_NENT, H_OFF_ROWS, H_OFF_EXT, H_OFF_PIV, H_OFF_VAL, H_OFF_CODE, H_BYTES, H_OFF_ITEMS,
@@ -47,7 +56,7 @@ struct TiledTuning {
     long long *debug = nullptr;  // optional device buffer: 8 int64 per CTA of cycle counters (scripts/probe_tiled.py)
 };
 static TiledTuning g_tiled;
-__device__ unsigned g_nap_ns = 0;    // back-off of compute warps that wait for boundary dependencies / the next tile
+
 
 #define GRID_STRIDE_Q(i, n) \
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (long long)gridDim.x * blockDim.x)
@@ -510,12 +519,9 @@ __device__ __forceinline__ void level_sync(int l, int threads) {
 
 struct TileCtl {
     uint64_t mbar[TILE_NBUF];
-    uint64_t wbar;                    // one arrival per published level: lets the writer warp sleep
     unsigned long long ext_prog[2];   // (tile ordinal << 32) | externals delivered
     int b_ready[2];                   // tile ordinal + 1 whose right-hand side sits in bs[buf]
-    unsigned long long lvl_done[2];   // (tile ordinal << 32) | levels complete, for the writer warp
     int comp_done;                    // tiles finished by the compute warps
-    int wr_done;                      // tiles whose x the writer warp has stored
     int poll_done;                    // tiles whose boundary dependencies the poller has delivered
     int pad[3];
 };
@@ -574,13 +580,14 @@ struct TileItem {
     uint32_t xaddr[KP];              // shared-memory byte address of the x operand of entry k
     uint32_t saddr;                  // where this lane's result goes
     int bar;                         // hardware barrier id of this item's level
+    int row;                         // global row of this lane's result (-1: idle lane)
     double a[KP];
     double rhs, piv, rinv;
 };
 
 template <bool HAS_DIAG, int KP>
 __device__ __forceinline__ void tile_item_load(TileItem<KP> &r, const int4 *it, int lane,
-                                               const double *xsk, int zslot, const double *piv,
+                                               const double *xsk, int zslot, const double *piv, const int *rows,
                                                const unsigned short *codes, const double *vals) {
     const int4 A = it[0], B = it[1];   // A = {slot0, ent0, w, K}, B = {level, need, flags, n_arr}
     r.level = B.x;
@@ -593,6 +600,7 @@ __device__ __forceinline__ void tile_item_load(TileItem<KP> &r, const int4 *it, 
     const bool act = lane < (B.z & 0xff);
     const int s = A.x + lane;
     r.saddr = smem_u32(xsk + s);
+    r.row = act ? rows[s] : -1;
     r.rhs = act ? xsk[s] : 1.0;   // the feeder parked b[row] in the row's own x slot (idle lanes: keep the
                                   // division on its fast path)
     const double2 pr = (HAS_DIAG && act) ? ((const double2 *)piv)[s] : make_double2(1.0, 1.0);
@@ -631,18 +639,14 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
     const int nk = (n_tiles - (int)blockIdx.x + G - 1) / G;   // my tiles: blockIdx.x + k*G
     if (tid == 0) {
         for (int s = 0; s < TILE_NBUF; ++s) mbar_init(&ctl->mbar[s], 1);
-        mbar_init(&ctl->wbar, 1);
         ctl->ext_prog[0] = ctl->ext_prog[1] = 0ULL;
         ctl->b_ready[0] = ctl->b_ready[1] = 0;
         ctl->comp_done = 0;
-        ctl->wr_done = 0;
         ctl->poll_done = 0;
-        ctl->lvl_done[0] = ctl->lvl_done[1] = 0ULL;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     volatile int *comp_done = &ctl->comp_done;
-    volatile int *wr_done = &ctl->wr_done;
     volatile int *poll_done = &ctl->poll_done;
 
     if (warp == 0) {
@@ -655,51 +659,43 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             mbar_expect_tx(bar, bytes);
             bulk_g2s(stat + (size_t)(k % TILE_NBUF) * stat_max, blob + 16LL * o0, bytes, bar);
         };
-        // event loop: issue the TMA of tile `issued` as soon as its ring slot is free (the tile that used it
-        // is computed AND written back), gather the right-hand side of tile `fed` into the x buffer as soon
-        // as its static block has landed and the x buffer of tile fed-2 is free
-        int issued = 0, fed = 0;
-        while (fed < nk) {
-            if (issued < nk &&
-                (issued < TILE_NBUF || (*comp_done > issued - TILE_NBUF && *wr_done > issued - TILE_NBUF &&
-                                        *poll_done > issued - TILE_NBUF))) {
-                if (lane == 0) issue(issued);
-                ++issued;
-            }
-            if (fed < issued && (fed < 2 || (*comp_done >= fed - 1 && *wr_done >= fed - 1)) &&
-                mbar_test(&ctl->mbar[fed % TILE_NBUF], (uint32_t)((fed / TILE_NBUF) & 1))) {
-                const int k = fed;
-                const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
-                const int *hdr = (const int *)blk;
-                const int T = hdr[H_T];
-                const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
-                double *xsk = xs + (size_t)(k & 1) * xstride;   // slot s holds b[row] until the row is solved
-                for (int s0 = 0; s0 < T; s0 += 256) {
-                    double v[8];
+        // Tile j needs: its ring slot and x buffer free (tile j-2 computed and its boundary values
+        // delivered), then the TMA of its static block, then the right-hand side gathered INTO its x slots.
+        // All of that happens while tile j-1 is being computed.  The waits sleep (the ncu profile of the
+        // first version showed 40 % of all issued instructions in helper-warp spin loops, and the kernel is
+        // issue-bound).
+        for (int j = 0; j < nk; ++j) {
+            if (j >= 2)
+                while (*comp_done < j - 1 || *poll_done < j - 1) __nanosleep(600);
+            if (lane == 0) issue(j);
+            mbar_wait(&ctl->mbar[j % TILE_NBUF], (uint32_t)((j / TILE_NBUF) & 1));
+            const unsigned char *blk = stat + (size_t)(j % TILE_NBUF) * stat_max;
+            const int *hdr = (const int *)blk;
+            const int T = hdr[H_T];
+            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
+            double *xsk = xs + (size_t)(j & 1) * xstride;   // slot s holds b[row] until the row is solved
+            for (int s0 = 0; s0 < T; s0 += 256) {
+                double v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int s = s0 + u * 32 + lane;
-                        v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int s = s0 + u * 32 + lane;
-                        if (s < T) xsk[s] = v[u];
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const int s = s0 + u * 32 + lane;
+                    v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
                 }
-                __syncwarp();
-                __threadfence_block();
-                if (lane == 0) *(volatile int *)&ctl->b_ready[k & 1] = k + 1;
-                ++fed;
-            } else {
-                __nanosleep(200);   // a tile ahead of the compute warps: leave the issue slots to them
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int s = s0 + u * 32 + lane;
+                    if (s < T) xsk[s] = v[u];
+                }
             }
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) *(volatile int *)&ctl->b_ready[j & 1] = j + 1;
         }
     } else if (warp == 1) {
         // ---------------- poller: boundary dependencies, in the order the levels need them
         for (int k = 0; k < nk; ++k) {
             if (k >= 2)
-                while (*comp_done < k - 1 || *wr_done < k - 1) __nanosleep(100);
+                while (*comp_done < k - 1) __nanosleep(600);   // x buffer of tile k-2 still in use
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
@@ -735,37 +731,6 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             __syncwarp();
             if (lane == 0) *poll_done = k + 1;
         }
-    } else if (warp == 2) {
-        // ---------------- writer: publishes finished levels to L2 so that the compute warps never wait
-        // for a global store (a barrier arrive after st.global costs an L2 round trip: scripts/probe_lat.cu)
-        unsigned npub = 0;   // level publishes consumed so far (= completed phases of wbar)
-        for (int k = 0; k < nk; ++k) {
-            mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
-            const int *hdr = (const int *)blk;
-            const int n_lev = hdr[H_NLEV];
-            const int *lst = (const int *)(blk + TILE_HDR_BYTES);
-            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
-            const double *xsk = xs + (size_t)(k & 1) * xstride;
-            volatile unsigned long long *ld = &ctl->lvl_done[k & 1];
-            int seen = 0;
-            while (seen < n_lev) {
-                const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)(seen + 1);
-                unsigned long long got = *ld;
-                if (got < want) {   // nothing new: sleep on the publish barrier (phase = publishes consumed so far)
-                    mbar_nap(&ctl->wbar, npub & 1u, 1000);
-                    continue;
-                }
-                asm volatile("" ::: "memory");
-                const int upto = (int)(got & 0xffffffffULL);
-                const int s1 = lst[upto];
-                for (int s = lst[seen] + lane; s < s1; s += 32) st_l2(x + rows[s], scrub_sentinel(xsk[s]));
-                npub += (unsigned)(upto - seen);
-                seen = upto;
-            }
-            __syncwarp();
-            if (lane == 0) *wr_done = k + 1;
-        }
     } else {
         // ---------------- compute warps
         // Level l of a tile is cut into chunks of 32 rows; chunk c goes to compute warp (l + c) mod 4.
@@ -782,13 +747,13 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             long long t0 = 0;
             if (dbg) t0 = clock64();
             mbar_wait(&ctl->mbar[k % TILE_NBUF], (uint32_t)((k / TILE_NBUF) & 1));
-            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) __nanosleep(g_nap_ns);
+            while (*(volatile int *)&ctl->b_ready[k & 1] != k + 1) __nanosleep(200);
             asm volatile("" ::: "memory");
             if (dbg) t_wait_tile += clock64() - t0;
-            volatile unsigned long long *lvl_done = &ctl->lvl_done[k & 1];
             const unsigned char *blk = stat + (size_t)(k % TILE_NBUF) * stat_max;
             const int *hdr = (const int *)blk;
             const int n_lev = hdr[H_NLEV];
+            const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
             const double *piv = (const double *)(blk + hdr[H_OFF_PIV]);
             const double *vals = (const double *)(blk + hdr[H_OFF_VAL]);
             const unsigned short *codes = (const unsigned short *)(blk + hdr[H_OFF_CODE]);
@@ -809,23 +774,16 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             // levels before my first chunk (all levels if I have none): arrive at once
             for (int l = 0; l <= (n_it ? first - 2 : n_lev - 1); ++l) level_arrive(l, NC);
             TileItem<KP> itm;
-            if (n_it) tile_item_load<HAS_DIAG, KP>(itm, items, lane, xsk, zslot, piv, codes, vals);
+            if (n_it) tile_item_load<HAS_DIAG, KP>(itm, items, lane, xsk, zslot, piv, rows, codes, vals);
             int have = 0;
             for (int q = 0; q < n_it; ++q) {
                 if (itm.flags & ITEM_SYNC) level_sync(itm.level - 1, NC);
-                if ((itm.flags & ITEM_PUBLISH) && lane == 0) {
-                    *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.level;
-                    mbar_arrive(&ctl->wbar);
-                }
                 if (itm.need > have) {
                     long long t1 = 0;
                     if (dbg) t1 = clock64();
                     const unsigned long long want = ((unsigned long long)(unsigned)k << 32) | (unsigned)itm.need;
                     unsigned long long got = *prog;
-                    while (got < want) {   // producers are behind: do not burn the SM's issue slots meanwhile
-                        __nanosleep(g_nap_ns);
-                        got = *prog;
-                    }
+                    while (got < want) got = *prog;
                     have = (int)(got & 0xffffffffULL);
                     if (dbg) t_wait_ext += clock64() - t1;
                 }
@@ -848,14 +806,13 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 // off everybody's critical path
                 if (itm.n_arr > 0) asm volatile("bar.arrive %0, %1;" ::"r"(itm.bar), "r"(NC) : "memory");
                 for (int j = 1; j < itm.n_arr; ++j) level_arrive(itm.level + j, NC);
+                // publish to L2 AFTER the arrives: a barrier operation issued behind a global store waits for
+                // the store (an L2 round trip); this warp's next barrier operation is >= 1 level away
+                if (itm.row >= 0) st_l2(x + itm.row, scrub_sentinel(sum));
                 if (q + 1 < n_it)
-                    tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, codes, vals);
+                    tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, rows, codes, vals);
             }
             asm volatile("bar.sync 5, %0;" ::"r"(NC) : "memory");   // tile finished by every compute warp
-            if (cw == 0 && lane == 0) {
-                *lvl_done = ((unsigned long long)(unsigned)k << 32) | (unsigned)n_lev;
-                mbar_arrive(&ctl->wbar);
-            }
             if (dbg) {
                 t_levels += clock64() - t0;
                 n_lv += n_lev;
@@ -1170,9 +1127,7 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
         g_tiled.ctas_per_sm = value;
     } else if (eq("grid_cap")) {
         g_tiled.grid_cap = value;
-    } else if (eq("nap_ns")) {
-        unsigned v = (unsigned)value;
-        if (cudaMemcpyToSymbol(g_nap_ns, &v, sizeof(v)) != cudaSuccess) return DDILU_ERR_ARG;
+
     } else {
         return DDILU_ERR_ARG;
     }

@@ -139,3 +139,43 @@ def test_pivot_division_is_ieee_division(P):
     for seed in (1, 2, 3, 4):
         D.call("ddilu_fastdiv_selftest", 1 << 29, seed, bad)
         assert int(bad.item()) == 0, seed
+
+
+def test_wide_levels_and_many_externals(P, tile_kernel):
+    """Tiles whose levels are wider than the 4 x 32 rows the compute warps cover at once (several chunks
+    per warp and level) and tiles that import hundreds of boundary dependencies."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    rng = np.random.default_rng(7)
+    n, half = 600, 300
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        rows.append(i); cols.append(i); vals.append(2.0 + rng.random())
+        if i >= half:                       # every late row depends on 2-5 early rows and on one late row
+            for j in sorted(set(rng.integers(0, half, size=rng.integers(2, 4)))):
+                rows.append(i); cols.append(int(j)); vals.append(rng.standard_normal())
+            if i >= half + 40:
+                rows.append(i); cols.append(i - 40); vals.append(rng.standard_normal())
+    a = P.csr_from_coo(n, n, np.array(rows), np.array(cols), np.array(vals))
+    lo = P.CsrMatrix(n, n, *_strict_lower(a))
+    ld = lo.device()
+    lev, _ = D.levels(ld, False)
+    keys = torch.tensor([0 if i < half else 1 for i in range(n)], dtype=torch.int32, device="cuda")
+    part = D.tile_partition(keys, 2)
+    ts = D.build_tiles(ld, lev, part, False, True)
+    assert ts is not None and ts.n_tiles == 2
+    b = torch.from_numpy(rng.standard_normal(n)).cuda()
+    x1, x2 = D.empty_f64(n), D.empty_f64(n)
+    D.sptrsv_tiled(ts, b, x1)
+    D.sptrsv(ld, D.build_schedule(ld, False), b, x2, False, True)
+    assert torch.equal(x1, x2)
+
+
+def _strict_lower(a):
+    rp, ci, v = [0], [], []
+    for i in range(a.n_rows):
+        for k in range(int(a.row_ptr[i]), int(a.row_ptr[i + 1])):
+            if a.col_idx[k] < i:
+                ci.append(int(a.col_idx[k])); v.append(float(a.values[k]))
+        rp.append(len(ci))
+    return np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int64), np.array(v)
