@@ -137,6 +137,11 @@ int ddilu_tiled_set_tuning(const char *key, int value);
 int ddilu_tiled_set_debug(long long *device_buf);
 int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *owner,
                         int *keys, long long *n_keys_h, void *stream);
+/* "wavefront slab" tiles: key = (owner, box of the first two grid coordinates, lev[i] / delta) with lev =
+ * the factor's level of row i; *n_keys_h = size of the key range */
+int ddilu_tile_slab_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *lev,
+                         int n_levels, int delta, const int *owner, int n_owners, int *keys, long long *n_keys_h,
+                         void *stream);
 int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream);
 int ddilu_tile_assign(int n, const int *sorted_keys, const int *head_scan, const int *sorted_rows, int *tile_of,
                       int *tpos, int *tile_ptr, void *stream);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "ddilu_tiled_set_tuning": (_I, [_S, _I]),
     "ddilu_tiled_set_debug": (_I, [_P]),
     "ddilu_tile_box_keys": (_I, [_I, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_tile_slab_keys": (_I, [_I, _P, _I, _P, _P, _P, _I, _I, _P, _I, _P, _P, _P]),
     "ddilu_tile_heads": (_I, [_I, _P, _P, _P]),
     "ddilu_tile_assign": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_tile_edges_count": (_I, [_I, _P, _P, _I, _P, _P, _P]),

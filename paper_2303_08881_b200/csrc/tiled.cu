@@ -72,6 +72,21 @@ __global__ void tile_box_keys(int n, const int *__restrict__ nodes, int d0, int 
     }
 }
 
+// "Wavefront slab" tiles: footprint box in the first two grid coordinates x a range of `delta` consecutive
+// LEVELS of the factor.  On a wavefront-ordered stencil factor every level of such a tile holds the whole
+// footprint (t0*t1 rows), so a tile of t0*t1*delta rows has only delta levels (a t^3 box has 3t-2).
+__global__ void tile_slab_keys(int n, const int *__restrict__ nodes, int d0, int d1, int t0, int t1, int nb0, int nb1,
+                               const int *__restrict__ lev, int delta, int n_slabs, const int *__restrict__ owner,
+                               int *__restrict__ keys) {
+    GRID_STRIDE_Q(i, n) {
+        const int g = nodes ? nodes[i] : (int)i;
+        const int c0 = g % d0, c1 = (g / d0) % d1;
+        int key = (c1 / t1) * nb0 + (c0 / t0);
+        if (owner) key += owner[g] * (nb0 * nb1);
+        keys[i] = key * n_slabs + lev[i] / delta;
+    }
+}
+
 __global__ void tile_heads(int n, const int *__restrict__ skeys, int *__restrict__ flags) {
     GRID_STRIDE_Q(q, n) flags[q] = (q == 0 || skeys[q] != skeys[q - 1]) ? 1 : 0;
 }
@@ -1166,6 +1181,23 @@ extern "C" int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *d
     if (n <= 0) return DDILU_OK;
     tile_box_keys<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, nodes, d[0], d[1], t[0], t[1], t[2], nb[0], nb[1],
                                                               (int)nboxes, owner, keys);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_tile_slab_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h,
+                                    const int *lev, int n_levels, int delta, const int *owner, int n_owners, int *keys,
+                                    long long *n_keys_h, void *stream) {
+    if (nd < 2 || nd > 3 || delta < 1 || n_levels < 1 || n_owners < 1) return DDILU_ERR_ARG;
+    const int d0 = dims_h[0], d1 = dims_h[1];
+    const int t0 = tdims_h[0] < 1 ? 1 : tdims_h[0], t1 = tdims_h[1] < 1 ? 1 : tdims_h[1];
+    const int nb0 = (d0 + t0 - 1) / t0, nb1 = (d1 + t1 - 1) / t1, n_slabs = (n_levels + delta - 1) / delta;
+    const long long range = (long long)nb0 * nb1 * n_slabs * n_owners;
+    if (n_keys_h) *n_keys_h = range;
+    if (range > 0x7FFFFFFF) return DDILU_ERR_ARG;
+    if (n <= 0) return DDILU_OK;
+    tile_slab_keys<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, nodes, d0, d1, t0, t1, nb0, nb1, lev, delta, n_slabs,
+                                                               owner, keys);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -246,6 +246,21 @@ def box_tile_keys(nodes: torch.Tensor | None, n: int, dims, tdims, owner: torch.
     return keys[:n], int(nk.value)
 
 
+def slab_tile_keys(nodes: torch.Tensor | None, n: int, dims, tdims2, lev: torch.Tensor, n_levels: int, delta: int,
+                   owner: torch.Tensor | None, n_owners: int):
+    """(keys int32[n], key range): key = (owner, footprint box in the first two grid coordinates,
+    lev // delta) -- wavefront-slab tiles of a factor whose levels are `lev`."""
+    nd = len(dims)
+    arr = ctypes.c_int * nd
+    arr2 = ctypes.c_int * 2
+    d, t = arr(*[int(v) for v in dims]), arr2(int(tdims2[0]), int(tdims2[1]))
+    nk = ctypes.c_longlong(0)
+    keys = empty_i32(max(1, n))
+    call("ddilu_tile_slab_keys", int(n), nodes, nd, ctypes.addressof(d), ctypes.addressof(t), lev, int(n_levels),
+         int(delta), owner, int(n_owners), keys, ctypes.addressof(nk))
+    return keys[:n], int(nk.value)
+
+
 def tile_partition(keys: torch.Tensor, key_range: int) -> TilePartition | None:
     """Compact the keys into tile ids; None if a tile would exceed TILE_MAX_ROWS."""
     n = keys.numel()

@@ -113,8 +113,19 @@ class DevFactors:
         fallback when the tile graph is not one-way.  seg_ptr: row ranges of independent
         diagonal blocks (one per subdomain), if known."""
         if part is not None and D.USE_TILED and self.n:
-            self._tl = D.build_tiles(self.lower, self._lev(False)[0], part, False, True)
-            self._tu = D.build_tiles(self.upper, self._lev(True)[0], part, True, False)
+            # part: one TilePartition for both factors, or a callable (lev, n_levels) -> TilePartition for
+            # partitions that depend on the factor's own levels (wavefront-slab tiles)
+            for upper in (False, True):
+                lev, nlev = self._lev(upper)
+                pt = part(lev, nlev) if callable(part) else part
+                ts = D.build_tiles(self.upper if upper else self.lower, lev, pt, upper, not upper) \
+                    if pt is not None else None
+                if ts is None and callable(part) and getattr(part, "fallback", None) is not None:
+                    ts = D.build_tiles(self.upper if upper else self.lower, lev, part.fallback, upper, not upper)
+                if upper:
+                    self._tu = ts
+                else:
+                    self._tl = ts
         if seg_ptr is not None and (self._tl is None or self._tu is None):
             D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
         if self._tl is None:

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--nap", type=int, default=-1)
     ap.add_argument("--tile", default="")
     ap.add_argument("--kernel", default="")
+    ap.add_argument("--slab", default="")
     ap.add_argument("--wpb", type=int, default=0)
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
@@ -61,6 +62,9 @@ def main():
     query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
     if args.nap >= 0:
         query("ddilu_tiled_set_tuning", b"nap_ns", args.nap)
+    if args.slab:
+        from paper_2303_08881_b200.precond import LocalSystem as _LS
+        _LS.SLAB = None if args.slab == "0" else tuple(int(v) for v in args.slab.split(","))
     if args.kernel:
         D.TILE_KERNEL = args.kernel
     if args.tile:
