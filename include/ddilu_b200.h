@@ -80,10 +80,11 @@ int ddilu_sell_fill(int n_slots, const int *order, const int *row_ptr, const int
 /* out[g] = gwait[group of prev[g]]: the same kind of indicator one level further back */
 int ddilu_compose_wait(int n_groups, const int *gwait, const int *pos, const int *prev, int *out, void *stream);
 /* gwait / gfar1 / gfar2 (each optional): single addresses 1 / 2 / 3 levels back a warp waits on before
- * it polls its own dependencies ("trsv_stage_mask" selects which are used) */
+ * it polls its own dependencies ("trsv_stage_mask" selects which are used); avg_width = average padded
+ * entries per lane (0: the uniform width): rows longer than 6 / 14 poll 8 / 16 dependencies per round */
 int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff, int uniform_width,
                       const int *scol, const double *sval, const double *sdiag, const int *gwait, const int *gfar1,
-                      const int *gfar2, const double *b, double *x, void *stream);
+                      const int *gfar2, double avg_width, const double *b, double *x, void *stream);
 
 /* Block-local variant for small, deep, block-diagonal factors (interface factors L_S/U_S:
  * precond.py:239-245 `_schur_solve`, :361-366 `_coarse_precond`): one CTA per independent row

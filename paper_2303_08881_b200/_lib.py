@@ -35,7 +35,7 @@ SIGNATURES = {
     "ddilu_sell_width": (_I, [_I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sell_fill": (_I, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
     "ddilu_compose_wait": (_I, [_I, _P, _P, _P, _P, _P]),
-    "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),
     "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),

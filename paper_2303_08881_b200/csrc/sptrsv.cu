@@ -38,6 +38,7 @@ struct TrsvTuning {
                              // bit0: far stage (sleep-poll 3 levels back), bit1: mid stage (spin 2 levels
                              // back), bit2: near stage (spin on the group's own latest dependency)
     int far_sleep_ns = 400;
+    int chunk = 0;           // dependencies polled per round by the SELL kernel; 0: by average row width
     int depth = 24;          // resident warps ~ depth x (groups per level): enough lookahead to hide the
                              // startup loads of a group, few enough pollers not to slow the producers
 };
@@ -298,14 +299,15 @@ constexpr int SELL_CHUNK = 4;
 // re-polled on its own.  (Measured on B200: re-issuing ALL pending polls every
 // round is slower -- more simultaneous polls of the line the producer is about
 // to store to: 0.81 vs 0.48 us per level on a one-warp-per-level chain.)
-__device__ __forceinline__ void poll_chunk(const double *x, const int (&c)[SELL_CHUNK], double (&xv)[SELL_CHUNK]) {
+template <int C>
+__device__ __forceinline__ void poll_chunk(const double *x, const int (&c)[C], double (&xv)[C]) {
 #pragma unroll
-    for (int u = 0; u < SELL_CHUNK; ++u) xv[u] = c[u] >= 0 ? ld_l2(x + c[u]) : 0.0;
+    for (int u = 0; u < C; ++u) xv[u] = c[u] >= 0 ? ld_l2(x + c[u]) : 0.0;
     bool pending;
     do {
         pending = false;
 #pragma unroll
-        for (int u = 0; u < SELL_CHUNK; ++u)
+        for (int u = 0; u < C; ++u)
             if (is_sentinel(xv[u])) {
                 xv[u] = ld_l2(x + c[u]);
                 pending |= is_sentinel(xv[u]);
@@ -313,7 +315,9 @@ __device__ __forceinline__ void poll_chunk(const double *x, const int (&c)[SELL_
     } while (pending);
 }
 
-template <bool HAS_DIAG>
+// CHUNK = dependencies of a row polled together: 4 for stencil-length rows, 12 for long rows (27-point /
+// ILUT / ILU(k) factors: a 19-entry row is 2 poll rounds instead of 5)
+template <bool HAS_DIAG, int CHUNK>
 __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const int *__restrict__ order,
                                                             const int *__restrict__ goff, int uw,
                                                             const int *__restrict__ scol,
@@ -348,18 +352,18 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
         if (wait_col >= 0)
             while (is_sentinel(ld_l2(x + wait_col))) {
             }
-        for (int k0 = 0; k0 < w; k0 += SELL_CHUNK) {
-            int c[SELL_CHUNK];
-            double a[SELL_CHUNK], xv[SELL_CHUNK];
+        for (int k0 = 0; k0 < w; k0 += CHUNK) {
+            int c[CHUNK];
+            double a[CHUNK], xv[CHUNK];
 #pragma unroll
-            for (int u = 0; u < SELL_CHUNK; ++u) {
+            for (int u = 0; u < CHUNK; ++u) {
                 const bool in = k0 + u < w;
                 c[u] = in ? scol[off + 32 * (k0 + u) + lane] : -1;
                 a[u] = in ? sval[off + 32 * (k0 + u) + lane] : 0.0;
             }
             poll_chunk(x, c, xv);
 #pragma unroll
-            for (int u = 0; u < SELL_CHUNK; ++u)
+            for (int u = 0; u < CHUNK; ++u)
                 if (c[u] >= 0) s -= a[u] * xv[u];
         }
         if (row >= 0) st_l2(x + row, scrub_sentinel(HAS_DIAG ? s / d : s));
@@ -696,6 +700,7 @@ extern "C" int ddilu_set_tuning(const char *key, int value) {
     else if (!strcmp(key, "trsv_sleep_ns")) g_trsv.sleep_ns = (unsigned)value;
     else if (!strcmp(key, "trsv_pipe")) g_trsv.pipe = value;
     else if (!strcmp(key, "trsv_depth")) g_trsv.depth = value;
+    else if (!strcmp(key, "trsv_chunk")) g_trsv.chunk = value;
     else if (!strcmp(key, "trsv_stage_mask")) g_trsv.stage_mask = value;
     else if (!strcmp(key, "trsv_far_sleep_ns")) g_trsv.far_sleep_ns = value;
     else if (!strcmp(key, "trsv_pipe_warps_per_sm")) g_trsv.pipe_warps_per_sm = value;
@@ -795,8 +800,8 @@ extern "C" int ddilu_compose_wait(int n_groups, const int *gwait, const int *pos
 
 extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const int *goff,
                                  int uniform_width, const int *scol, const double *sval, const double *sdiag,
-                                 const int *gwait, const int *gfar1, const int *gfar2, const double *b, double *x,
-                                 void *stream) {
+                                 const int *gwait, const int *gfar1, const int *gfar2, double avg_width,
+                                 const double *b, double *x, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) return DDILU_OK;
     if (x == b || (n_slots & 31)) return DDILU_ERR_ARG;
@@ -826,8 +831,22 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
         DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, 128, pargs, 0, st));
         return DDILU_OK;
     }
-    int grid = sdiag ? coop_grid(sptrsv_sell<true>, SELL_THREADS, g_trsv.blocks_per_sm, n_slots)
-                     : coop_grid(sptrsv_sell<false>, SELL_THREADS, g_trsv.blocks_per_sm, n_slots);
+    // dependencies polled per round: 4 for stencil-length rows, 8 / 16 for long rows (ILUT / ILU(k) /
+    // 27-point factors); avg_width = average padded entries per lane of the layout
+    if (avg_width <= 0.0) avg_width = uniform_width;
+    int chunk = g_trsv.chunk;
+    if (chunk <= 0) chunk = avg_width > 14.0 ? 16 : (avg_width > 6.0 ? 8 : 4);
+    void *fn;
+    if (chunk >= 16) fn = sdiag ? (void *)sptrsv_sell<true, 16> : (void *)sptrsv_sell<false, 16>;
+    else if (chunk >= 8) fn = sdiag ? (void *)sptrsv_sell<true, 8> : (void *)sptrsv_sell<false, 8>;
+    else fn = sdiag ? (void *)sptrsv_sell<true, 4> : (void *)sptrsv_sell<false, 4>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SELL_THREADS, 0);
+    if (occ < 1) occ = 1;
+    if (g_trsv.blocks_per_sm > 0 && occ > g_trsv.blocks_per_sm) occ = g_trsv.blocks_per_sm;
+    long long cap = (long long)occ * device_info().sm_count;
+    long long need_blocks = ((long long)n_slots + SELL_THREADS - 1) / SELL_THREADS;
+    int grid = (int)(cap < need_blocks ? cap : (need_blocks < 1 ? 1 : need_blocks));
     if (g_trsv.depth > 0 && n_levels > 0) {
         // narrow levels: cap the resident warps at depth x (groups per level)
         long long want_warps = (long long)g_trsv.depth * ((n_groups + n_levels - 1) / n_levels);
@@ -835,8 +854,7 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
         if (want < 16) want = 16;
         if (want < grid) grid = (int)want;
     }
-    if (sdiag) DDILU_CHECK(cudaLaunchCooperativeKernel((void *)sptrsv_sell<true>, grid, SELL_THREADS, args, 0, st));
-    else DDILU_CHECK(cudaLaunchCooperativeKernel((void *)sptrsv_sell<false>, grid, SELL_THREADS, args, 0, st));
+    DDILU_CHECK(cudaLaunchCooperativeKernel(fn, grid, SELL_THREADS, args, 0, st));
     return DDILU_OK;
 }
 

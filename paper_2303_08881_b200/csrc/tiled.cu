@@ -42,7 +42,6 @@ constexpr int TILE_MAX_ROWS = 1024;
 constexpr int TILE_HDR_BYTES = 96;
 constexpr int TILE_NW = 4;          // compute warps of the solve kernel (the item lists are cut for them)
 constexpr int ITEM_SYNC = 1 << 8;   // first chunk of this warp in a level >= 1: wait for the previous level
-constexpr int ITEM_PUBLISH = 1 << 9;   // chunk 0 of a level: tells the writer warp that the levels before are complete
 constexpr int TILE_NBUF = 2;
 constexpr int TILE_HELPERS = 64;   // warp 0: TMA + right-hand side, warp 1: external dependencies
 
@@ -425,7 +424,7 @@ tile_build(int n_tiles, const int *__restrict__ tsched, const int *__restrict__ 
                     n_arr = nxt > n_lev ? n_lev - i : nxt - 1 - i;
                 }
                 const int cnt = wl - c * 32 < 32 ? wl - c * 32 : 32;
-                const int flags = cnt | ((first && i >= 1) ? ITEM_SYNC : 0) | ((c == 0 && i >= 1) ? ITEM_PUBLISH : 0);
+                const int flags = cnt | ((first && i >= 1) ? ITEM_SYNC : 0);
                 it[2 * nth] = make_int4(l0 + c * 32, s_lent[i] + c * 32, wl, s_lk[i]);
                 it[2 * nth + 1] = make_int4(i, need, flags, n_arr);
             }
@@ -495,25 +494,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return done != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// sleep (in hardware) until the phase with this parity completes or ~hint_ns pass; the caller re-checks its condition
-__device__ __forceinline__ void mbar_nap(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(hint_ns)
-        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done;
@@ -590,7 +570,7 @@ __global__ void fastdiv_selftest(long long n, unsigned long long seed, unsigned 
 // everything that does not depend on x is in registers before the level's barrier opens.
 template <int KP>
 struct TileItem {
-    int level, need, flags, n_arr;   // flags: rows in the chunk | ITEM_SYNC | ITEM_PUBLISH
+    int level, need, flags, n_arr;   // flags: rows in the chunk | ITEM_SYNC
     int ent0, w, K;                  // entry k of lane i: ent0 + k*w + i (long rows, k >= KP)
     uint32_t xaddr[KP];              // shared-memory byte address of the x operand of entry k
     uint32_t saddr;                  // where this lane's result goes

@@ -457,7 +457,8 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
             raise TriSolveError(f"zero or missing diagonal at row {sell.bad_row}")
         call("ddilu_sptrsv_sell", t.n_rows, sched.n_slots, sched.n_levels, sched.order, sell.goff, sell.width,
              sell.scol, sell.sval, sell.sdiag, sell.gwait if USE_GWAIT else None,
-             sell.gfar1 if USE_GWAIT else None, sell.gfar2 if USE_GWAIT else None, b, out)
+             sell.gfar1 if USE_GWAIT else None, sell.gfar2 if USE_GWAIT else None,
+             float(sell.scol.numel() / max(1, sched.n_slots)), b, out)
         return out
     call("ddilu_sptrsv", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
          int(unit_diag), _err())
