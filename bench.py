@@ -185,7 +185,7 @@ def run_ours(args):
     clocks = sampler.stop() if sampler else None
     prof, _lib.profile = _lib.profile, None
     # --- one extra UNTIMED step with events on the other hot kernels (or on every entry: --watch-all)
-    watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_spmv_csr_f64_tuned", "ddilu_axpy_dot", "ddilu_dot")
+    watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_spmv_csr_f64_tuned", "ddilu_axpy_dot_dir", "ddilu_dot_dir")
     if args.watch_all:
         watch = tuple(k for k, (res, a) in _lib.SIGNATURES.items() if res is _lib._I and a and a[-1] is _lib._P)
     _lib.profile = {k: [] for k in watch}
@@ -271,7 +271,7 @@ def run_ours(args):
         line["roofline_spmv"] = {"kernel": "spmv_stream (outer A z, one per iteration)", "achieved": spmv_bytes / d_sp / 1e9,
                                  "peak": peak, "unit": "GB/s", "frac": spmv_bytes / d_sp / 1e9 / peak,
                                  "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_us": d_sp * 1e6}
-    mg = sorted(e0.elapsed_time(e1) * 1e-3 for e0, e1, _ in prof_all.get("ddilu_axpy_dot", []))
+    mg = sorted(e0.elapsed_time(e1) * 1e-3 for e0, e1, _ in prof_all.get("ddilu_axpy_dot_dir", []))
     if mg:
         big_mg = mg[len(mg) // 2:]
         d_mg = float(np.mean(big_mg))

@@ -207,13 +207,20 @@ int ddilu_csr_block_fill(const int *rp, const int *ci, const double *v, int r0, 
  * krylov.py:74-77 `_axpy`, and the numpy expressions of krylov.py:122,156,160-167 */
 long long ddilu_reduce_ws_bytes(void);
 int ddilu_dot(long long n, const double *x, const double *y, double *out, void *ws, void *stream);
+int ddilu_dot_dir(long long n, const double *x, const double *y, double *out, void *ws, int reverse, void *stream);
 /* w += (alpha_dev ? alpha_host * *alpha_dev : alpha_host) * v; if u: *out = dot(u, w) */
 int ddilu_axpy_dot(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
                    const double *u, double *out, void *ws, void *stream);
+/* the same walking the vectors from the end when reverse != 0: consecutive MGS steps alternate the direction
+ * so that a step starts with the part of w and of the shared basis vector that is still in L2 */
+int ddilu_axpy_dot_dir(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
+                       const double *u, double *out, void *ws, int reverse, void *stream);
 /* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
 int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
                 double *y, void *stream);
 /* x (+)= sum_i coef[i] * basis[i*ld + :] in increasing i */
+/* L2 residency hint for the Arnoldi work vector (stream access-policy window, persisting L2); bytes = 0 clears */
+int ddilu_l2_persist_window(const void *ptr, long long bytes, void *stream);
 int ddilu_multi_axpy(long long n, int k, const double *basis, long long ld, const double *coef, double *x,
                      int overwrite, void *stream);
 /* z = a + b (0), a - b (1), -a (2) */

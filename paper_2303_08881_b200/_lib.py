@@ -71,8 +71,11 @@ SIGNATURES = {
     "ddilu_csr_block_fill": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ddilu_reduce_ws_bytes": (_L, []),
     "ddilu_dot": (_I, [_L, _P, _P, _P, _P, _P]),
+    "ddilu_dot_dir": (_I, [_L, _P, _P, _P, _P, _I, _P]),
     "ddilu_axpy_dot": (_I, [_L, _P, _D, _P, _P, _P, _P, _P, _P]),
+    "ddilu_axpy_dot_dir": (_I, [_L, _P, _D, _P, _P, _P, _P, _P, _I, _P]),
     "ddilu_scale": (_I, [_L, _P, _P, _D, _I, _I, _P, _P]),
+    "ddilu_l2_persist_window": (_I, [_P, _L, _P]),
     "ddilu_multi_axpy": (_I, [_L, _I, _P, _L, _P, _P, _I, _P]),
     "ddilu_ewise": (_I, [_L, _P, _P, _I, _P, _P]),
     "ddilu_gather": (_I, [_L, _P, _P, _P, _P]),

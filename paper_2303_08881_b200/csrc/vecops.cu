@@ -7,6 +7,8 @@
 //
 // Algorithmic bytes: dot 16n; axpy 24n; fused axpy+dot 32n (the reference's
 // separate dot and axpy move 40n per MGS step).
+#include <string.h>
+
 #include "common.cuh"
 #include "ddilu_b200.h"
 
@@ -61,11 +63,13 @@ __device__ __forceinline__ void finish_reduction(double part, RedWs *ws, double 
 
 // out = sum x[i]*y[i]
 __global__ void __launch_bounds__(VEC_THREADS) dot_kernel(long long n, const double *__restrict__ x,
-                                                          const double *__restrict__ y, RedWs *ws, double *out) {
+                                                          const double *__restrict__ y, RedWs *ws, double *out,
+                                                          int reverse) {
     double acc = 0.0;
     const long long n2 = aligned16(x, y) ? n >> 1 : 0;  // 16-byte path only when both operands allow it
     const double2 *x2 = reinterpret_cast<const double2 *>(x), *y2 = reinterpret_cast<const double2 *>(y);
-    for (long long i = (long long)blockIdx.x * VEC_THREADS + threadIdx.x; i < n2; i += (long long)gridDim.x * VEC_THREADS) {
+    for (long long q = (long long)blockIdx.x * VEC_THREADS + threadIdx.x; q < n2; q += (long long)gridDim.x * VEC_THREADS) {
+        const long long i = reverse ? n2 - 1 - q : q;
         double2 a = x2[i], b = y2[i];
         acc += a.x * b.x;
         acc += a.y * b.y;
@@ -79,9 +83,11 @@ __global__ void __launch_bounds__(VEC_THREADS) dot_kernel(long long n, const dou
 // w += (sign * *alpha_dev or alpha_host) * v ; optionally out = dot(u, w_new)
 // (u == w gives the squared norm).  One pass: 32n bytes with the dot, 24n without.
 template <bool DOT>
+// reverse: walk the vectors from the end.  Consecutive MGS steps alternate the direction, so a step starts
+// with the ~L2-sized tail of w and of the basis vector that the previous step touched last.
 __global__ void __launch_bounds__(VEC_THREADS) axpy_dot_kernel(long long n, const double *alpha_dev, double alpha_host,
                                                                const double *__restrict__ v, double *w, const double *u,
-                                                               RedWs *ws, double *out) {
+                                                               RedWs *ws, double *out, int reverse) {
     const double alpha = alpha_dev ? alpha_host * (*alpha_dev) : alpha_host;
     double acc = 0.0;
     const long long n2 = (aligned16(v, w) && aligned16(u ? u : w, w)) ? n >> 1 : 0;
@@ -89,7 +95,8 @@ __global__ void __launch_bounds__(VEC_THREADS) axpy_dot_kernel(long long n, cons
     double2 *w2 = reinterpret_cast<double2 *>(w);
     const double2 *u2 = reinterpret_cast<const double2 *>(u);
     const bool self = (u == w);
-    for (long long i = (long long)blockIdx.x * VEC_THREADS + threadIdx.x; i < n2; i += (long long)gridDim.x * VEC_THREADS) {
+    for (long long q = (long long)blockIdx.x * VEC_THREADS + threadIdx.x; q < n2; q += (long long)gridDim.x * VEC_THREADS) {
+        const long long i = reverse ? n2 - 1 - q : q;
         double2 a = v2[i], b = w2[i];
         b.x += alpha * a.x;
         b.y += alpha * a.y;
@@ -168,24 +175,45 @@ using namespace ddilu;
 extern "C" long long ddilu_reduce_ws_bytes(void) { return (long long)sizeof(RedWs); }
 
 extern "C" int ddilu_dot(long long n, const double *x, const double *y, double *out, void *ws, void *stream) {
-    dot_kernel<<<red_grid(n), VEC_THREADS, 0, (cudaStream_t)stream>>>(n, x, y, (RedWs *)ws, out);
+    dot_kernel<<<red_grid(n), VEC_THREADS, 0, (cudaStream_t)stream>>>(n, x, y, (RedWs *)ws, out, 0);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* the same walking the vectors from the end when reverse != 0 (see ddilu_axpy_dot_dir) */
+extern "C" int ddilu_dot_dir(long long n, const double *x, const double *y, double *out, void *ws, int reverse,
+                             void *stream) {
+    dot_kernel<<<red_grid(n), VEC_THREADS, 0, (cudaStream_t)stream>>>(n, x, y, (RedWs *)ws, out, reverse);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+static int axpy_dot_launch(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
+                           const double *u, double *out, void *ws, int reverse, cudaStream_t st) {
+    if (u) {
+        if (!out || !ws) return DDILU_ERR_ARG;
+        axpy_dot_kernel<true><<<red_grid(n), VEC_THREADS, 0, st>>>(n, alpha_dev, alpha_host, v, w, u, (RedWs *)ws, out,
+                                                                  reverse);
+    } else {
+        if (n <= 0) return DDILU_OK;
+        axpy_dot_kernel<false><<<stream_grid(n, VEC_THREADS, 4), VEC_THREADS, 0, st>>>(n, alpha_dev, alpha_host, v, w,
+                                                                                       nullptr, nullptr, nullptr,
+                                                                                       reverse);
+    }
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
 
 extern "C" int ddilu_axpy_dot(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
                               const double *u, double *out, void *ws, void *stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (u) {
-        if (!out || !ws) return DDILU_ERR_ARG;
-        axpy_dot_kernel<true><<<red_grid(n), VEC_THREADS, 0, st>>>(n, alpha_dev, alpha_host, v, w, u, (RedWs *)ws, out);
-    } else {
-        if (n <= 0) return DDILU_OK;
-        axpy_dot_kernel<false><<<stream_grid(n, VEC_THREADS, 4), VEC_THREADS, 0, st>>>(n, alpha_dev, alpha_host, v, w,
-                                                                                       nullptr, nullptr, nullptr);
-    }
-    DDILU_LAUNCH_CHECK();
-    return DDILU_OK;
+    return axpy_dot_launch(n, alpha_dev, alpha_host, v, w, u, out, ws, 0, (cudaStream_t)stream);
+}
+
+/* the same, walking the vectors from the end when reverse != 0 (consecutive MGS steps alternate: the step
+ * starts with what the previous one left in L2) */
+extern "C" int ddilu_axpy_dot_dir(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
+                                  const double *u, double *out, void *ws, int reverse, void *stream) {
+    return axpy_dot_launch(n, alpha_dev, alpha_host, v, w, u, out, ws, reverse, (cudaStream_t)stream);
 }
 
 extern "C" int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt,
@@ -224,5 +252,37 @@ extern "C" int ddilu_scatter(long long n, const int *idx, const double *src, dou
     if (n <= 0) return DDILU_OK;
     scatter_kernel<<<stream_grid(n, VEC_THREADS, 2), VEC_THREADS, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
     DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* L2 residency hint for the Arnoldi work vector w (no reference equivalent): every MGS step reads and writes
+ * w while the basis vectors stream through once; with w pinned in the persisting part of L2 a step moves
+ * 16n + (1 - hit) 16n bytes from HBM instead of 32n.  bytes = 0 clears the window and the persisting lines. */
+extern "C" int ddilu_l2_persist_window(const void *ptr, long long bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, max_persist = 0, max_window = 0;
+    DDILU_CHECK(cudaGetDevice(&dev));
+    DDILU_CHECK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    DDILU_CHECK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    cudaStreamAttrValue attr;
+    memset(&attr, 0, sizeof(attr));
+    if (bytes <= 0 || !ptr || max_persist <= 0) {
+        attr.accessPolicyWindow.num_bytes = 0;
+        DDILU_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
+        DDILU_CHECK(cudaCtxResetPersistingL2Cache());
+        return DDILU_OK;
+    }
+    // leave a quarter of the allowed set-aside to everything else that wants L2
+    const long long set_aside = (long long)max_persist * 3 / 4;
+    DDILU_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)set_aside));
+    const long long win = bytes < max_window ? bytes : max_window;
+    double ratio = (double)set_aside / (double)win;
+    if (ratio > 1.0) ratio = 1.0;
+    attr.accessPolicyWindow.base_ptr = const_cast<void *>(ptr);
+    attr.accessPolicyWindow.num_bytes = (size_t)win;
+    attr.accessPolicyWindow.hitRatio = (float)ratio;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    DDILU_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
     return DDILU_OK;
 }

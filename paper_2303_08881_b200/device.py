@@ -558,11 +558,11 @@ class Reducer:
         nbytes = query("ddilu_reduce_ws_bytes")
         self.ws = torch.zeros(nbytes // 8 + 1, dtype=F64, device=dev())
 
-    def dot(self, n, x, y, out):
-        call("ddilu_dot", int(n), x, y, out, self.ws)
+    def dot(self, n, x, y, out, reverse=False):
+        call("ddilu_dot_dir", int(n), x, y, out, self.ws, int(reverse))
 
-    def axpy_dot(self, n, alpha_dev, alpha_host, v, w, u, out):
-        call("ddilu_axpy_dot", int(n), alpha_dev, float(alpha_host), v, w, u, out, self.ws)
+    def axpy_dot(self, n, alpha_dev, alpha_host, v, w, u, out, reverse=False):
+        call("ddilu_axpy_dot_dir", int(n), alpha_dev, float(alpha_host), v, w, u, out, self.ws, int(reverse))
 
 
 def axpy(n, alpha, v, w, alpha_dev=None):

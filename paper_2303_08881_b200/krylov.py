@@ -119,12 +119,16 @@ class Arnoldi:
         to_host = h is None
         if to_host:
             h = self.hdev
-        red.dot(n, V[0], w, h[0:1])
+        # consecutive passes walk the vectors in alternating directions (the SpMV that produced w ran forward):
+        # a pass starts with the tail of w and of the shared basis vector that the previous pass left in L2
+        # (126 MB against 3 x 134 MB per pass at 256^3)
+        alt = ALTERNATE_MGS
+        red.dot(n, V[0], w, h[0:1], reverse=alt)
         comm.allreduce_sum_(h[0:1])
         for i in range(j):
-            red.axpy_dot(n, h[i:i + 1], -1.0, V[i], w, V[i + 1], h[i + 1:i + 2])
+            red.axpy_dot(n, h[i:i + 1], -1.0, V[i], w, V[i + 1], h[i + 1:i + 2], reverse=alt and (i & 1) == 1)
             comm.allreduce_sum_(h[i + 1:i + 2])
-        red.axpy_dot(n, h[j:j + 1], -1.0, V[j], w, w, h[j + 1:j + 2])
+        red.axpy_dot(n, h[j:j + 1], -1.0, V[j], w, w, h[j + 1:j + 2], reverse=alt and (j & 1) == 1)
         comm.allreduce_sum_(h[j + 1:j + 2])
         return h[: j + 2].cpu().numpy() if to_host else None
 
@@ -142,6 +146,9 @@ class Arnoldi:
 
 DevOp = Callable[[torch.Tensor, torch.Tensor], None]  # op(x, out): out[:n] = Op x[:n]
 
+L2_PERSIST_W = False  # pin the Arnoldi work vector in the persisting part of L2 during a solve (measured: slower)
+ALTERNATE_MGS = True  # consecutive MGS steps traverse the vectors in alternating directions (L2 reuse)
+
 
 def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Tensor, x0: torch.Tensor | None,
                      cfg: KrylovConfig, flexible: bool, comm: Comm, pad: int = 0):
@@ -151,6 +158,9 @@ def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Ten
     m = cfg.restart
     ws = Arnoldi(n, m, comm, flexible, pad)
     V, Z, w = ws.V, ws.Z, ws.w
+    if L2_PERSIST_W and n * 8 > (32 << 20):
+        # w is read and written by every MGS step, the basis streams through once: keep w in persisting L2
+        D.call("ddilu_l2_persist_window", w, w.numel() * 8)
     bnorm = ws.norm2(b)
     scale = bnorm if bnorm > 0.0 else 1.0
     x = torch.zeros(ws.ld, dtype=D.F64, device=D.dev())
@@ -213,6 +223,8 @@ def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Ten
         final_rel = beta / scale
         if final_rel <= cfg.rtol:
             converged = True
+    if L2_PERSIST_W and n * 8 > (32 << 20):
+        D.call("ddilu_l2_persist_window", None, 0)
     report = SolveReport(iterations=its, converged=converged,
                          residual_history=np.array(history if cfg.record_history else []),
                          final_relres=final_rel)
