@@ -53,16 +53,18 @@ class _Owner(np.ndarray):
     """int64 owner array that remembers its device copy (avoids a re-upload)."""
 
     _dev = None
+    _p = None          # number of domains when the map came from partition() (values 0 .. _p-1 guaranteed)
     grid_hint = None   # dims of the structured grid the owner map was cut from (tiles the solves)
 
     def __array_finalize__(self, obj):
         if obj is not None:
-            self.grid_hint = getattr(obj, "grid_hint", None)
+            self.grid_hint = getattr(obj, "grid_hint", None)   # views / copies may be edited: no _dev, no _p
 
 
-def _wrap_owner(host: np.ndarray, dev_t: torch.Tensor | None, grid_hint=None) -> np.ndarray:
+def _wrap_owner(host: np.ndarray, dev_t: torch.Tensor | None, grid_hint=None, p: int | None = None) -> np.ndarray:
     out = host.view(_Owner)
     out._dev = dev_t
+    out._p = p
     out.grid_hint = tuple(int(d) for d in grid_hint) if grid_hint is not None else None
     return out
 
@@ -100,7 +102,7 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
                 sizes = np.outer(chunk, sizes).ravel()
             if np.max(np.abs(sizes - n / p)) <= max(1.0, 0.1 * n / p):
                 owner_d = D.box_owner(n, dims, factors)
-                return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint)
+                return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint, p)
     # unstructured fallback (ordering.py:192-198): greedy breadth-first growth over the symmetrised pattern
     base, rem = divmod(n, p)
     sizes = np.full(p, base, dtype=np.int32)
@@ -109,7 +111,7 @@ def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
     owner_d = D.empty_i32(n)
     work = D.empty_i32(2 * n)
     D.call("ddilu_grow_regions", n, adj.rp, adj.ci, p, torch.from_numpy(sizes).to(D.dev()), owner_d, work)
-    return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint)
+    return _wrap_owner(D.to_host_i64(owner_d), owner_d, hint, p)
 
 
 class DomainLayout:
@@ -172,9 +174,13 @@ def classify_and_order(a: CsrMatrix, owner, p: int | None = None, grid_hint=None
     owner_h = np.asarray(owner, dtype=np.int64) if not isinstance(owner, _Owner) else owner
     if owner_h.shape != (n,):
         raise ValueError("owner array has wrong length")
+    trusted = isinstance(owner, _Owner) and getattr(owner, "_dev", None) is not None and owner._p is not None
     if p is None:
-        p = int(owner_h.max()) + 1 if n else 1
-    if n and (owner_h.min() < 0 or owner_h.max() >= p):
+        p = owner._p if trusted else (int(owner_h.max()) + 1 if n else 1)
+    if trusted:
+        if owner._p > p:          # made by partition(): values are 0 .. _p-1 by construction, no host pass
+            raise ValueError("owner values out of range")
+    elif n and (owner_h.min() < 0 or owner_h.max() >= p):
         raise ValueError("owner values out of range")
     ad = a.device()
     owner_d = _owner_device(owner_h)
