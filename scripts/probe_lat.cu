@@ -22,34 +22,34 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
 #pragma unroll 8
     for (int i = 0; i < N; ++i) s -= a * s;
     t1 = clock64();
-    if (tid == 0) cyc[0] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[0] = (t1 - t0) / N;
     // (1) dependent DADD
     double s1 = s;
     t0 = clock64();
 #pragma unroll 8
     for (int i = 0; i < N; ++i) s1 = s1 - a;
     t1 = clock64();
-    if (tid == 0) cyc[1] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[1] = (t1 - t0) / N;
     // (2) dependent division
     double s2 = s1 + 3.0;
     t0 = clock64();
 #pragma unroll 4
     for (int i = 0; i < N; ++i) s2 = (s2 + 1.5) / a;
     t1 = clock64();
-    if (tid == 0) cyc[2] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[2] = (t1 - t0) / N;
     // (3) shared-memory pointer chase
     int p = lane;
     t0 = clock64();
 #pragma unroll 8
     for (int i = 0; i < N; ++i) p = chase[p];
     t1 = clock64();
-    if (tid == 0) cyc[3] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[3] = (t1 - t0) / N;
     // (4) named barrier, all warps
     __syncthreads();
     t0 = clock64();
     for (int i = 0; i < N; ++i) asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x) : "memory");
     t1 = clock64();
-    if (tid == 0) cyc[4] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[4] = (t1 - t0) / N;
     // (5) ring handoff: warp w waits for warp w-1 (bar ids 1..4), does one sts, passes on
     __syncthreads();
     const int nw = blockDim.x >> 5;
@@ -62,7 +62,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.arrive %0, %1;" ::"r"(8 + (l % nw)), "r"(64) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[5] = (t1 - t0) / (N * nw);   // per handoff
+    if (tid == 0 && blockIdx.x == 0) cyc[5] = (t1 - t0) / (N * nw);   // per handoff
     if (nw > 1 && warp == 0) asm volatile("bar.sync %0, %1;" ::"r"(8 + ((N * nw - 1) % nw)), "r"(64) : "memory");
     __syncthreads();
     // (6) volatile global store + barrier per iteration
@@ -72,7 +72,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[6] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[6] = (t1 - t0) / N;
     // (7) sts -> bar -> dependent lds of another thread's value -> dmul/dadd x3 -> sts  (one "level")
     double v = s2;
     t0 = clock64();
@@ -86,7 +86,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.sync 2, %0;" ::"r"((int)blockDim.x) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[7] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[7] = (t1 - t0) / N;
     // (8) like (6) but every store goes to a fresh line
     __syncthreads();
     t0 = clock64();
@@ -95,7 +95,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[8] = (t1 - t0) / N;
+    if (tid == 0 && blockIdx.x == 0) cyc[8] = (t1 - t0) / N;
     // (9) ring handoff with a level's work: sync, 3 lds, 3 mul/sub, sts, volatile global store (fresh line), arrive
     __syncthreads();
     t0 = clock64();
@@ -111,7 +111,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.arrive %0, %1;" ::"r"(8 + (l % nw)), "r"(64) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[9] = (t1 - t0) / (N * nw);
+    if (tid == 0 && blockIdx.x == 0) cyc[9] = (t1 - t0) / (N * nw);
     // (10) the same with a plain (weak) global store
     if (nw > 1 && warp == 0) asm volatile("bar.sync %0, %1;" ::"r"(8 + ((N * nw - 1) % nw)), "r"(64) : "memory");
     __syncthreads();
@@ -128,7 +128,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.arrive %0, %1;" ::"r"(8 + (l % nw)), "r"(64) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[10] = (t1 - t0) / (N * nw);
+    if (tid == 0 && blockIdx.x == 0) cyc[10] = (t1 - t0) / (N * nw);
     // (11) without any global store
     if (nw > 1 && warp == 0) asm volatile("bar.sync %0, %1;" ::"r"(8 + ((N * nw - 1) % nw)), "r"(64) : "memory");
     __syncthreads();
@@ -144,7 +144,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
         asm volatile("bar.arrive %0, %1;" ::"r"(8 + (l % nw)), "r"(64) : "memory");
     }
     t1 = clock64();
-    if (tid == 0) cyc[11] = (t1 - t0) / (N * nw);
+    if (tid == 0 && blockIdx.x == 0) cyc[11] = (t1 - t0) / (N * nw);
     if (nw > 1 && warp == 0) asm volatile("bar.sync %0, %1;" ::"r"(8 + ((N * nw - 1) % nw)), "r"(64) : "memory");
     // (12) the tiled kernel's protocol: every barrier B_l gets all 4 warps; the owner of level l syncs on
     // B_{l-1}, works, then arrives at B_l, B_{l+1}, B_{l+2}
@@ -167,7 +167,7 @@ __global__ void probe(double *out, long long *cyc, double seed, double *g) {
             for (int q = l; q <= last; ++q) asm volatile("bar.arrive %0, %1;" ::"r"(8 + (q & 3)), "r"(128) : "memory");
         }
         t1 = clock64();
-        if (tid == 0) cyc[12] = (t1 - t0) / (N * 4);
+        if (tid == 0 && blockIdx.x == 0) cyc[12] = (t1 - t0) / (N * 4);
     }
     __syncthreads();
     out[tid] = s + s1 + s2 + p + v;
@@ -183,9 +183,13 @@ int main() {
                              "ring handoff arrive->sync", "st.volatile + bar", "level: sts,bar,3 lds,3 mul/sub,bar",
                              "st.volatile fresh line + bar", "ring level + st.volatile", "ring level + weak st",
                              "ring level, no global st", "4-warp protocol level"};
+    const int grids[3] = {1, 148 * 4, 148 * 8};
+    for (int gi = 0; gi < 3; ++gi)
     for (int threads = 32; threads <= 128; threads *= 2) {
-        probe<<<1, threads>>>(out, cyc, 1.25, g);
-        probe<<<1, threads>>>(out, cyc, 1.25, g);
+        if (gi > 0 && threads != 128) continue;
+        printf("grid %d\n", grids[gi]);
+        probe<<<grids[gi], threads>>>(out, cyc, 1.25, g);
+        probe<<<grids[gi], threads>>>(out, cyc, 1.25, g);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("kernel failed: %s\n", cudaGetErrorString(e)); return 1; }
         cudaMemcpy(h, cyc, 104, cudaMemcpyDeviceToHost);
