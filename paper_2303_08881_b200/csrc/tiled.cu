@@ -594,7 +594,7 @@ __device__ __forceinline__ void tile_item_load(TileItem<KP> &r, const int4 *it, 
     r.K = A.w;
     const bool act = lane < (B.z & 0xff);
     const int s = A.x + lane;
-    r.saddr = smem_u32(xsk + s);
+    r.saddr = smem_u32(xsk + (act ? s : zslot + 1));   // idle lanes store into a scratch slot: no predicate on the chain
     r.row = act ? rows[s] : -1;
     r.rhs = act ? xsk[s] : 1.0;   // the feeder parked b[row] in the row's own x slot (idle lanes: keep the
                                   // division on its fast path)
@@ -620,7 +620,8 @@ __device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
 
-template <bool HAS_DIAG, int KP>
+// LONG: some row of the factor has more than KP dependencies (compiled out for 7-point ILU(0) factors)
+template <bool HAS_DIAG, int KP, bool LONG>
 __global__ void __launch_bounds__(TILE_HELPERS + TILE_NW * 32)
 sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char *__restrict__ blob, int stat_max,
              int tmax, int emax, long long *dbg, const double *__restrict__ b, double *x) {
@@ -789,14 +790,14 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 double sum = itm.rhs;
 #pragma unroll
                 for (int u = 0; u < KP; ++u) sum -= itm.a[u] * xv[u];
-                if (itm.K > KP) {   // long rows: the remaining entries straight from the static block
+                if (LONG && itm.K > KP) {   // long rows: the remaining entries straight from the static block
                     const unsigned short *cp = codes + itm.ent0 + lane;
                     const double *vp = vals + itm.ent0 + lane;
                     if (lane < (itm.flags & 0xff))
                         for (int kk = KP; kk < itm.K; ++kk) sum -= vp[kk * itm.w] * xsk[cp[kk * itm.w]];
                 }
                 if (HAS_DIAG) sum = exact_div(sum, itm.piv, itm.rinv);
-                if (lane < (itm.flags & 0xff)) sts_f64(itm.saddr, sum);
+                sts_f64(itm.saddr, sum);
                 // release this level and every level I skip right away; then the next item's prefetch,
                 // off everybody's critical path
                 if (itm.n_arr > 0) asm volatile("bar.arrive %0, %1;" ::"r"(itm.bar), "r"(NC) : "memory");
@@ -1264,14 +1265,15 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
     const size_t smem = (size_t)ddilu_tiled_smem_bytes(stat_max, tmax, emax);
     const int threads = TILE_HELPERS + TILE_NW * 32;
     // entries of a row held in registers: 3 covers 7-point factors, 6 everything else (+ a loop for the rest)
-    const int wide = kmax > 3 ? 1 : 0;
-    void *fns[2][2] = {{(void *)sptrsv_tiled<false, 3>, (void *)sptrsv_tiled<false, 6>},
-                       {(void *)sptrsv_tiled<true, 3>, (void *)sptrsv_tiled<true, 6>}};
-    void *fn = fns[has_diag ? 1 : 0][wide];
+    const int sel = kmax <= 3 ? 0 : (kmax <= 6 ? 1 : 2);   // 0: KP 3, 1: KP 6, 2: KP 6 + loop over the rest
+    void *fns[2][3] = {
+        {(void *)sptrsv_tiled<false, 3, false>, (void *)sptrsv_tiled<false, 6, false>, (void *)sptrsv_tiled<false, 6, true>},
+        {(void *)sptrsv_tiled<true, 3, false>, (void *)sptrsv_tiled<true, 6, false>, (void *)sptrsv_tiled<true, 6, true>}};
+    void *fn = fns[has_diag ? 1 : 0][sel];
     // occupancy of (kernel, smem) is looked up once per configuration
     struct Cfg { size_t smem; int occ; };
-    static Cfg cache[2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
-    Cfg &cf = cache[has_diag ? 1 : 0][wide];
+    static Cfg cache[2][3] = {{{0, 0}, {0, 0}, {0, 0}}, {{0, 0}, {0, 0}, {0, 0}}};
+    Cfg &cf = cache[has_diag ? 1 : 0][sel];
     if (cf.smem != smem) {
         DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int o = 0;
