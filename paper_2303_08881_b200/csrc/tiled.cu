@@ -800,7 +800,10 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 sts_f64(itm.saddr, sum);
                 // release this level and every level I skip right away; then the next item's prefetch,
                 // off everybody's critical path
-                if (itm.n_arr > 0) asm volatile("bar.arrive %0, %1;" ::"r"(itm.bar), "r"(NC) : "memory");
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.gt.s32 p, %2, 0;\n @p bar.arrive %0, %1;\n}" ::"r"(itm.bar), "r"(NC),
+                    "r"(itm.n_arr)
+                    : "memory");   // predicated: no branch between the store and the arrive
                 for (int j = 1; j < itm.n_arr; ++j) level_arrive(itm.level + j, NC);
                 // publish to L2 AFTER the arrives: a barrier operation issued behind a global store waits for
                 // the store (an L2 round trip); this warp's next barrier operation is >= 1 level away
