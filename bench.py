@@ -185,7 +185,8 @@ def run_ours(args):
     clocks = sampler.stop() if sampler else None
     prof, _lib.profile = _lib.profile, None
     # --- one extra UNTIMED step with events on the other hot kernels (or on every entry: --watch-all)
-    watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_spmv_csr_f64_tuned", "ddilu_axpy_dot_dir", "ddilu_dot_dir")
+    watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_spmv_csr_f64_tuned", "ddilu_axpy_dot_dir", "ddilu_dot_dir",
+             "ddilu_mgs_block")
     if args.watch_all:
         watch = tuple(k for k, (res, a) in _lib.SIGNATURES.items() if res is _lib._I and a and a[-1] is _lib._P)
     _lib.profile = {k: [] for k in watch}
@@ -278,6 +279,22 @@ def run_ours(args):
         line["roofline_mgs"] = {"kernel": "axpy_dot (fused w -= h v_i, <v_i+1, w>), outer basis", "achieved": 32 * s.n_loc / d_mg / 1e9,
                                 "peak": peak, "unit": "GB/s", "frac": 32 * s.n_loc / d_mg / 1e9 / peak,
                                 "algorithmic_bytes_per_launch": 32 * s.n_loc, "avg_launch_us": d_mg * 1e6}
+    # blocked Gram-Schmidt: every pass is tagged (n, kp, kn); bytes = w read (+ write if kp) + kp + kn basis vectors
+    mb = [(e0.elapsed_time(e1) * 1e-3, tag) for e0, e1, tag in prof_all.get("ddilu_mgs_block", [])
+          if tag is not None and tag[0] == s.n_loc]
+    if mb:
+        byts = float(sum(8 * t[0] * (1 + (1 if t[1] else 0) + t[1] + t[2]) for _, t in mb))
+        secs = float(sum(d for d, _ in mb))
+        full = [d for d, t in mb if t[1] == 4 and t[2] == 4]
+        line["roofline_mgs"] = {"kernel": "mgs_block (w -= sum of 4 h_l v_l, then <v_i, w> and <v_i, v_l> of the next 4), "
+                                          "all passes over the outer basis",
+                                "achieved": byts / secs / 1e9, "peak": peak, "unit": "GB/s",
+                                "frac": byts / secs / 1e9 / peak, "launches": len(mb), "total_s": secs,
+                                "algorithmic_bytes_per_step": byts,
+                                "full_pass_us": float(np.mean(full)) * 1e6 if full else None,
+                                "full_pass_gbs": 80 * s.n_loc / float(np.mean(full)) / 1e9 if full else None,
+                                "vector_by_vector_bytes_per_step": float(sum(
+                                    8 * s.n_loc * (4 * (j + 1) + 1) for j in _arnoldi_js(rec["its"])))}
     tr = sorted(e0.elapsed_time(e1) * 1e-3 for e0, e1, _ in prof_all.get(trsv_name, []))
     if tr and args.precond == "schur" and m._p.schur.n:
         small = tr[: len(tr) - int(round(len(tr) * share))]
@@ -291,6 +308,11 @@ def run_ours(args):
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, full_its=rec["its"])
     print(json.dumps(line), flush=True)
+
+
+def _arnoldi_js(its, restart=50):
+    """Arnoldi column index j of each of `its` outer iterations of a restarted solve."""
+    return [i % restart for i in range(its)]
 
 
 # ---------------------------------------------------------------------------

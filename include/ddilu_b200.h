@@ -215,6 +215,15 @@ int ddilu_axpy_dot(long long n, const double *alpha_dev, double alpha_host, cons
  * so that a step starts with the part of w and of the shared basis vector that is still in L2 */
 int ddilu_axpy_dot_dir(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
                        const double *u, double *out, void *ws, int reverse, void *stream);
+/* Blocked modified Gram-Schmidt (krylov.py:131-136, the loop `h[i,j] = vdot(V[i], w); w -= h[i,j] V[i]`): one pass
+ * (a) subtracts the previous block, w -= sum_{l<kp} h_l vprev[l*ld + :], with h solved from the raw sums of the
+ * previous pass (raw_prev = [d_0..d_{kp-1}, G_10, G_20, G_21, ...]: h_i = d_i - sum_{l<i} h_l G_il) and stored to
+ * hout[0..kp), and (b) writes the raw sums of vnext[0..kn) against the updated w to out; kn == 0: out[0] = <w, w>.
+ * kp, kn <= ddilu_mgs_max_block().  Same values as the vector-by-vector loop up to the rounding of the dots. */
+long long ddilu_mgs_ws_bytes(void);
+int ddilu_mgs_max_block(void);
+int ddilu_mgs_block(long long n, long long ld, int kp, const double *vprev, const double *raw_prev, double *hout,
+                    double *w, int kn, const double *vnext, double *out, void *ws, int reverse, void *stream);
 /* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
 int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
                 double *y, void *stream);

@@ -118,6 +118,172 @@ __global__ void __launch_bounds__(VEC_THREADS) axpy_dot_kernel(long long n, cons
     }
 }
 
+// ---- blocked modified Gram-Schmidt (krylov.py:131-136 restated for blocks of MGS_K basis vectors) ----------
+// MGS orthogonalises w against v_0..v_j one vector at a time: h_i = <v_i, w_i>, w_{i+1} = w_i - h_i v_i; every
+// step is a pass over w.  Inside a block of k vectors the same coefficients follow from ONE pass:
+//   d_i = <v_i, w_0>,  G_il = <v_i, v_l> (l < i)   =>   h_i = d_i - sum_{l<i} h_l G_il   ( = <v_i, w_i> ),
+// so a pass (a) subtracts the previous block, w -= sum h_l v_l in the MGS order, and (b) accumulates d and G of
+// the next block against the updated w.  Traffic per MGS step: (16/k + 16) n bytes instead of 32 n.
+// The raw sums [d_0..d_{k-1}, G_10, G_20, G_21, G_30, ...] go through the same deterministic two-stage
+// reduction as the dots (and through ONE allreduce with several ranks); the k x k recurrence is redone by every
+// thread of the consuming pass, whose first thread also stores the coefficients into the Hessenberg column.
+constexpr int MGS_K = 4;
+constexpr int MGS_NRED = MGS_K + MGS_K * (MGS_K - 1) / 2;
+
+struct MgsWs {
+    double partial[MGS_NRED][RED_MAX_BLOCKS];
+    unsigned int ticket;
+};
+
+template <int NA>
+__device__ __forceinline__ void finish_reduction_multi(const double (&acc)[NA], MgsWs *ws, double *out) {
+    __shared__ double sm[NA][VEC_THREADS / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+        double v = warp_sum(acc[a]);
+        if (lane == 0) sm[a][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC_THREADS / 32; ++q) t += sm[threadIdx.x][q];
+        ws->partial[threadIdx.x][blockIdx.x] = t;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = atomicAdd(&ws->ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        for (int a = warp; a < NA; a += VEC_THREADS / 32) {
+            double s = 0.0;
+            for (unsigned b = lane; b < gridDim.x; b += 32) s += ld_l2(&ws->partial[a][b]);
+            s = warp_sum(s);
+            if (lane == 0) out[a] = s;
+        }
+        if (threadIdx.x == 0) ws->ticket = 0;
+    }
+}
+
+// one pass: w -= sum_{l<KP} h_l vprev_l (h from raw_prev, stored to hout), then raw sums of vnext_0..KN-1 against
+// the updated w into out[0 .. KN + KN(KN-1)/2); KN == 0: out[0] = <w, w>.
+template <int KP, int KN>
+__global__ void __launch_bounds__(VEC_THREADS) mgs_block_kernel(long long n, long long ld,
+                                                                const double *__restrict__ vprev,
+                                                                const double *__restrict__ raw_prev, double *hout,
+                                                                double *w, const double *__restrict__ vnext, MgsWs *ws,
+                                                                double *out, int reverse) {
+    constexpr int KPA = KP > 0 ? KP : 1;
+    constexpr int NA = KN > 0 ? KN + KN * (KN - 1) / 2 : 1;
+    double nh[KPA];
+    if (KP > 0) {
+        double h[KPA];
+        int g = KP;
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+            double s = raw_prev[i];
+#pragma unroll
+            for (int l = 0; l < i; ++l) s -= h[l] * raw_prev[g++];
+            h[i] = s;
+            nh[i] = -s;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < KP; ++i) hout[i] = h[i];
+        }
+    }
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    const bool al = ((((uintptr_t)w | (uintptr_t)(KP > 0 ? vprev : w) | (uintptr_t)(KN > 0 ? vnext : w)) & 15) == 0) &&
+                    ((ld & 1) == 0);
+    const long long n2 = al ? n >> 1 : 0, ld2 = ld >> 1;
+    double2 *w2 = reinterpret_cast<double2 *>(w);
+    const double2 *p2 = reinterpret_cast<const double2 *>(vprev), *q2 = reinterpret_cast<const double2 *>(vnext);
+    for (long long q = (long long)blockIdx.x * VEC_THREADS + threadIdx.x; q < n2; q += (long long)gridDim.x * VEC_THREADS) {
+        const long long i = reverse ? n2 - 1 - q : q;
+        double2 b = w2[i];
+        if (KP > 0) {
+            double2 a[KPA];
+#pragma unroll
+            for (int l = 0; l < KP; ++l) a[l] = p2[l * ld2 + i];
+#pragma unroll
+            for (int l = 0; l < KP; ++l) {
+                b.x += nh[l] * a[l].x;
+                b.y += nh[l] * a[l].y;
+            }
+            w2[i] = b;
+        }
+        if (KN > 0) {
+            double2 c[KN > 0 ? KN : 1];
+#pragma unroll
+            for (int j = 0; j < KN; ++j) c[j] = q2[j * ld2 + i];
+            int g = KN;
+#pragma unroll
+            for (int j = 0; j < KN; ++j) {
+                acc[j] += c[j].x * b.x;
+                acc[j] += c[j].y * b.y;
+#pragma unroll
+                for (int l = 0; l < j; ++l) {
+                    acc[g] += c[j].x * c[l].x;
+                    acc[g] += c[j].y * c[l].y;
+                    ++g;
+                }
+            }
+        } else {
+            acc[0] += b.x * b.x;
+            acc[0] += b.y * b.y;
+        }
+    }
+    for (long long i = 2 * n2 + (long long)blockIdx.x * VEC_THREADS + threadIdx.x; i < n; i += (long long)gridDim.x * VEC_THREADS) {
+        double b = w[i];
+        if (KP > 0) {
+#pragma unroll
+            for (int l = 0; l < KP; ++l) b += nh[l] * vprev[l * ld + i];
+            w[i] = b;
+        }
+        if (KN > 0) {
+            double c[KN > 0 ? KN : 1];
+#pragma unroll
+            for (int j = 0; j < KN; ++j) c[j] = vnext[j * ld + i];
+            int g = KN;
+#pragma unroll
+            for (int j = 0; j < KN; ++j) {
+                acc[j] += c[j] * b;
+#pragma unroll
+                for (int l = 0; l < j; ++l) acc[g++] += c[j] * c[l];
+            }
+        } else {
+            acc[0] += b * b;
+        }
+    }
+    finish_reduction_multi<NA>(acc, ws, out);
+}
+
+template <int KP>
+static void mgs_launch_kn(int kn, int grid, cudaStream_t st, long long n, long long ld, const double *vprev,
+                          const double *raw_prev, double *hout, double *w, const double *vnext, MgsWs *ws, double *out,
+                          int reverse) {
+#define DDILU_MGS_CASE(KN)                                                                                           \
+    case KN:                                                                                                         \
+        mgs_block_kernel<KP, KN><<<grid, VEC_THREADS, 0, st>>>(n, ld, vprev, raw_prev, hout, w, vnext, ws, out, reverse); \
+        break;
+    switch (kn) {
+        DDILU_MGS_CASE(0)
+        DDILU_MGS_CASE(1)
+        DDILU_MGS_CASE(2)
+        DDILU_MGS_CASE(3)
+        DDILU_MGS_CASE(4)
+    }
+#undef DDILU_MGS_CASE
+}
+
 // y = x / s, y = x * s or y = copy, with s = *alpha_dev (optionally sqrt'ed) or alpha_host
 // mode: 0 divide, 1 multiply
 __global__ void __launch_bounds__(VEC_THREADS) scale_kernel(long long n, const double *__restrict__ x,
@@ -214,6 +380,30 @@ extern "C" int ddilu_axpy_dot(long long n, const double *alpha_dev, double alpha
 extern "C" int ddilu_axpy_dot_dir(long long n, const double *alpha_dev, double alpha_host, const double *v, double *w,
                                   const double *u, double *out, void *ws, int reverse, void *stream) {
     return axpy_dot_launch(n, alpha_dev, alpha_host, v, w, u, out, ws, reverse, (cudaStream_t)stream);
+}
+
+extern "C" long long ddilu_mgs_ws_bytes(void) { return (long long)sizeof(MgsWs); }
+extern "C" int ddilu_mgs_max_block(void) { return MGS_K; }
+
+/* one pass of the blocked modified Gram-Schmidt (see mgs_block_kernel) */
+extern "C" int ddilu_mgs_block(long long n, long long ld, int kp, const double *vprev, const double *raw_prev,
+                               double *hout, double *w, int kn, const double *vnext, double *out, void *ws,
+                               int reverse, void *stream) {
+    if (kp < 0 || kp > MGS_K || kn < 0 || kn > MGS_K || !w || !out || !ws) return DDILU_ERR_ARG;
+    if (kp > 0 && (!vprev || !raw_prev || !hout)) return DDILU_ERR_ARG;
+    if (kn > 0 && !vnext) return DDILU_ERR_ARG;
+    const int grid = red_grid(n);
+    cudaStream_t st = (cudaStream_t)stream;
+    MgsWs *m = (MgsWs *)ws;
+    switch (kp) {
+        case 0: mgs_launch_kn<0>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 1: mgs_launch_kn<1>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 2: mgs_launch_kn<2>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 3: mgs_launch_kn<3>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 4: mgs_launch_kn<4>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+    }
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
 }
 
 extern "C" int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt,

@@ -567,12 +567,23 @@ class Reducer:
     def __init__(self):
         nbytes = query("ddilu_reduce_ws_bytes")
         self.ws = torch.zeros(nbytes // 8 + 1, dtype=F64, device=dev())
+        self.mgs_ws = None
 
     def dot(self, n, x, y, out, reverse=False):
         call("ddilu_dot_dir", int(n), x, y, out, self.ws, int(reverse))
 
     def axpy_dot(self, n, alpha_dev, alpha_host, v, w, u, out, reverse=False):
         call("ddilu_axpy_dot_dir", int(n), alpha_dev, float(alpha_host), v, w, u, out, self.ws, int(reverse))
+
+    def mgs_block(self, n, ld, kp, vprev, raw_prev, hout, w, kn, vnext, out, reverse=False):
+        """One pass of the blocked modified Gram-Schmidt (`ddilu_mgs_block`)."""
+        if self.mgs_ws is None:
+            self.mgs_ws = torch.zeros(query("ddilu_mgs_ws_bytes") // 8 + 1, dtype=F64, device=dev())
+        if _lib.profile is not None:
+            _lib.profile_tag = (int(n), int(kp), int(kn))
+        call("ddilu_mgs_block", int(n), int(ld), int(kp), vprev, raw_prev, hout, w, int(kn), vnext, out, self.mgs_ws,
+             int(reverse))
+        _lib.profile_tag = None
 
 
 def axpy(n, alpha, v, w, alpha_dev=None):

@@ -1,0 +1,95 @@
+"""Blocked modified Gram-Schmidt (`ddilu_mgs_block`) against the reference's
+vector-by-vector loop (krylov.py:131-136).
+
+The oracle is the loop itself in numpy fp64 on the same vectors:
+`h_i = <v_i, w>; w -= h_i v_i` for i = 0..j, then |w|^2.  The blocked kernel
+recovers the same coefficients from one pass per block of 4 vectors
+(h_i = <v_i, w_0> - sum_{l<i} h_l <v_i, v_l>); they differ from the loop only
+by the rounding of the reductions.  Tolerances: coefficients to 1e-12 of
+|w_0|, the updated w to 1e-12 of |w_0| per entry, and -- the property that
+matters to GMRES -- the orthogonality of the result against the basis must not
+be worse than the loop's.  The basis is deliberately NOT orthonormal in the
+second case (Gram entries of order 0.1), where a classical Gram-Schmidt would
+be visibly wrong and the block recurrence must still follow MGS."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mgs_loop(V, w):
+    w = w.copy()
+    h = np.zeros(V.shape[0] + 1)
+    for i in range(V.shape[0]):
+        h[i] = float(np.dot(V[i], w))
+        w -= h[i] * V[i]
+    h[-1] = float(np.dot(w, w))
+    return h, w
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 100003, (1 << 20) + 5])
+@pytest.mark.parametrize("nv", [1, 2, 3, 4, 5, 8, 11])
+@pytest.mark.parametrize("orthonormal", [True, False])
+def test_blocked_mgs_matches_the_loop(n, nv, orthonormal):
+    import torch
+    from paper_2303_08881_b200 import krylov as K
+    from paper_2303_08881_b200.dist import Comm
+    rng = np.random.default_rng(1000 * nv + n % 997 + int(orthonormal))
+    ws = K.Arnoldi(n, max(nv, 2), Comm(), flexible=False, pad=3)
+    Vh = rng.standard_normal((nv, n))
+    if orthonormal and n >= nv:
+        Vh = np.linalg.qr(Vh.T)[0].T.copy()
+    else:
+        Vh /= np.linalg.norm(Vh, axis=1)[:, None]
+        if n > 1:
+            Vh[1:] += 0.1 * Vh[:-1]          # neighbouring basis vectors overlap
+    wh = rng.standard_normal(n) * 3.0
+    ws.V.zero_()
+    ws.V[:nv, :n] = torch.from_numpy(Vh).cuda()
+    results = {}
+    for block in (1, 4):
+        K.MGS_BLOCK = block
+        try:
+            ws.w.zero_()
+            ws.w[:n] = torch.from_numpy(wh).cuda()
+            col = ws.mgs(nv - 1)
+            results[block] = (col.copy(), ws.w[:n].cpu().numpy())
+        finally:
+            K.MGS_BLOCK = 4
+    h_ref, w_ref = _mgs_loop(Vh, wh)
+    scale = np.linalg.norm(wh)
+    for block, (col, wd) in results.items():
+        assert col.shape == (nv + 1,)
+        assert np.max(np.abs(col[:nv] - h_ref[:nv])) <= 1e-12 * scale, block
+        assert abs(col[nv] - h_ref[nv]) <= 1e-11 * scale * scale, block
+        assert np.max(np.abs(wd - w_ref)) <= 1e-12 * scale, block
+    # the pad / untouched tail of w stays zero
+    assert float(ws.w[n:].abs().max()) == 0.0 if ws.w.numel() > n else True
+    if orthonormal and n >= nv:
+        # orthogonality of the result against the basis: not worse than the one-vector-at-a-time loop
+        def loss(wd):
+            return np.max(np.abs(Vh @ wd)) / max(np.linalg.norm(wd), 1e-300)
+        assert loss(results[4][1]) <= max(4.0 * loss(results[1][1]), 1e-14)
+
+
+def test_blocked_mgs_column_stays_on_device():
+    """With a device buffer nothing is read back and the column lands in it (inner GMRES path)."""
+    import torch
+    from paper_2303_08881_b200 import krylov as K
+    from paper_2303_08881_b200.dist import Comm
+    n, nv = 5000, 6
+    rng = np.random.default_rng(3)
+    ws = K.Arnoldi(n, nv, Comm(), flexible=False)
+    Vh = np.linalg.qr(rng.standard_normal((n, nv)))[0].T.copy()
+    wh = rng.standard_normal(n)
+    ws.V.zero_()
+    ws.V[:nv, :n] = torch.from_numpy(Vh).cuda()
+    ws.w.zero_()
+    ws.w[:n] = torch.from_numpy(wh).cuda()
+    buf = torch.full((nv + 3,), -7.0, dtype=torch.float64, device="cuda")
+    assert ws.mgs(nv - 1, buf) is None
+    h_ref, _ = _mgs_loop(Vh, wh)
+    got = buf.cpu().numpy()
+    assert np.allclose(got[: nv + 1], h_ref, rtol=0, atol=1e-12 * np.linalg.norm(wh))
+    assert np.all(got[nv + 1:] == -7.0)
