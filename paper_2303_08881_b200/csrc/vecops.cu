@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(VEC_THREADS) axpy_dot_kernel(long long n, cons
     }
 }
 
-// ---- blocked modified Gram-Schmidt (krylov.py:131-136 restated for blocks of MGS_K basis vectors) ----------
+// ---- blocked modified Gram-Schmidt (krylov.py:131-136 restated for blocks of up to MGS_K basis vectors) ----------
 // MGS orthogonalises w against v_0..v_j one vector at a time: h_i = <v_i, w_i>, w_{i+1} = w_i - h_i v_i; every
 // step is a pass over w.  Inside a block of k vectors the same coefficients follow from ONE pass:
 //   d_i = <v_i, w_0>,  G_il = <v_i, v_l> (l < i)   =>   h_i = d_i - sum_{l<i} h_l G_il   ( = <v_i, w_i> ),
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(VEC_THREADS) axpy_dot_kernel(long long n, cons
 // The raw sums [d_0..d_{k-1}, G_10, G_20, G_21, G_30, ...] go through the same deterministic two-stage
 // reduction as the dots (and through ONE allreduce with several ranks); the k x k recurrence is redone by every
 // thread of the consuming pass, whose first thread also stores the coefficients into the Hessenberg column.
-constexpr int MGS_K = 4;
+constexpr int MGS_K = 8;
 constexpr int MGS_NRED = MGS_K + MGS_K * (MGS_K - 1) / 2;
 
 struct MgsWs {
@@ -280,6 +280,10 @@ static void mgs_launch_kn(int kn, int grid, cudaStream_t st, long long n, long l
         DDILU_MGS_CASE(2)
         DDILU_MGS_CASE(3)
         DDILU_MGS_CASE(4)
+        DDILU_MGS_CASE(5)
+        DDILU_MGS_CASE(6)
+        DDILU_MGS_CASE(7)
+        DDILU_MGS_CASE(8)
     }
 #undef DDILU_MGS_CASE
 }
@@ -401,6 +405,10 @@ extern "C" int ddilu_mgs_block(long long n, long long ld, int kp, const double *
         case 2: mgs_launch_kn<2>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
         case 3: mgs_launch_kn<3>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
         case 4: mgs_launch_kn<4>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 5: mgs_launch_kn<5>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 6: mgs_launch_kn<6>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 7: mgs_launch_kn<7>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
+        case 8: mgs_launch_kn<8>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
     }
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;

@@ -18,6 +18,7 @@ residual.  What changed is where the work runs:
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass
 from typing import Callable
@@ -146,7 +147,7 @@ class Arnoldi:
         nv = j + 1
         npass = (nv + kmax - 1) // kmax
         if self.raw is None or self.raw.shape[0] < npass:
-            self.raw = torch.zeros(((self.m + kmax) // kmax + 1, 16), dtype=D.F64, device=D.dev())
+            self.raw = torch.zeros(((self.m + kmax) // kmax + 1, 40), dtype=D.F64, device=D.dev())
         raw = self.raw
         alt = ALTERNATE_MGS
         ps, pk = 0, 0
@@ -176,7 +177,7 @@ class Arnoldi:
 DevOp = Callable[[torch.Tensor, torch.Tensor], None]  # op(x, out): out[:n] = Op x[:n]
 
 L2_PERSIST_W = False  # pin the Arnoldi work vector in the persisting part of L2 during a solve (measured: slower)
-MGS_BLOCK = 4  # basis vectors per pass of the blocked Gram-Schmidt (1: the vector-by-vector launches)
+MGS_BLOCK = int(os.environ.get("DDILU_MGS_BLOCK", "4"))  # basis vectors per pass of the blocked Gram-Schmidt (1: the vector-by-vector launches)
 ALTERNATE_MGS = True  # consecutive MGS steps traverse the vectors in alternating directions (L2 reuse)
 
 
