@@ -97,6 +97,14 @@ int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *start, const 
                             int upper, int unit_diag, int *err, void *stream);
 
 /* same sweep on the SELL arrays; sstart[d*n_levels+l] = first SCHEDULE SLOT of block d in level l */
+/* the same sweep with the block's part of x in a shared-memory window: scol_loc = block-local schedule position
+ * of every dependency (-1 padding), lbase = first position of (block, level), wmask + 1 = window size (a power
+ * of two, checked at setup against the furthest dependency), sdinv = RN(1/pivot) or 0 (see ddilu_fastdiv_selftest) */
+int ddilu_sptrsv_blockwin_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *lbase,
+                               const int *order, const int *goff, int uniform_width, const int *scol_loc,
+                               const double *sval,
+                               const double *sdiag, const double *sdinv, int wmask, const double *b, double *x,
+                               void *stream);
 int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *order,
                                  const int *goff, int uniform_width, const int *scol, const double *sval,
                                  const double *sdiag, const double *b, double *x, void *stream);

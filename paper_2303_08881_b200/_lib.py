@@ -39,6 +39,7 @@ SIGNATURES = {
     "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv_blockwin_sell": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P]),
     "ddilu_sptrsv_sell_trace": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_iluk_smem_bytes": (_L, [_I]),
     "ddilu_iluk_symbolic": (_I, [_I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

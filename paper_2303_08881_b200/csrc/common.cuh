@@ -96,4 +96,29 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// s / d with the pivot's reciprocal r = RN(1/d) precomputed at setup: one multiply and two
+// remainder/correction FMA pairs instead of the ~30-instruction division routine on every level's
+// critical path.  q1 = RN(s r) is within 2 ulp of s/d, q2 is faithful, and by Markstein's theorem
+// (r correctly rounded, the remainder s - d q2 exact) the last correction rounds exactly like the
+// IEEE division, so the result has the bits of the reference's `s / d` (sparse.py:271).  Operands
+// outside a safe exponent window (zero, subnormal, huge, inf/nan: the remainder would not be exact)
+// and pivots flagged r = 0 at setup take the real division.  Verified bit-for-bit on random and
+// adversarial operands by ddilu_fastdiv_selftest (tests/test_gpu_tiled.py).
+__device__ __forceinline__ double exact_div(double s, double d, double r) {
+    const unsigned es = ((unsigned)__double2hiint(s) >> 20) & 0x7ffu;
+    if (r != 0.0 && es - 623u <= 800u) {
+        const double q1 = s * r;
+        const double e1 = __fma_rn(-d, q1, s);
+        const double q2 = __fma_rn(e1, r, q1);
+        const double e2 = __fma_rn(-d, q2, s);
+        return __fma_rn(e2, r, q2);
+    }
+    return s / d;
+}
+// reciprocal to store for a pivot, 0 = "always divide" (pivot outside the safe exponent window)
+__device__ __forceinline__ double safe_reciprocal(double d) {
+    const unsigned ed = ((unsigned)__double2hiint(d) >> 20) & 0x7ffu;
+    return (ed - 623u <= 800u) ? 1.0 / d : 0.0;
+}
+
 }  // namespace ddilu

@@ -678,6 +678,117 @@ __global__ void __launch_bounds__(BL_THREADS) sptrsv_blocklocal_sell(int n_level
     }
 }
 
+// Block-local sweep with the block's part of x in a SHARED-MEMORY window.  The rows of a block in schedule
+// order (level by level) get block-local positions 0, 1, 2, ...; `scol_loc` holds the position of every
+// dependency, and result p lives in xs[p & wmask] until position p + W is written.  Setup checks that no row
+// reads further back than the window (device.enable_block_window), so a level costs a shared-memory round
+// trip + one CTA barrier instead of the L2 round trip of the variant above (0.77 us per level).  The pivot
+// division uses the reciprocal prepared at setup (exact_div: bits of the IEEE quotient).
+struct BwRow {
+    int row;
+    int c[SELL_CHUNK];
+    double a[SELL_CHUNK];
+    double rhs, piv, rinv;
+    long long off;
+    int w, lane;
+};
+
+template <bool HAS_DIAG>
+__device__ __forceinline__ void bw_load(BwRow &r, int row, bool active, int slot,
+                                        const int *__restrict__ goff, int uw,
+                                        const int *__restrict__ scol, const double *__restrict__ sval,
+                                        const double *__restrict__ sdiag, const double *__restrict__ sdinv,
+                                        const double *__restrict__ b) {
+    r.row = active ? row : -1;
+    r.lane = slot & 31;
+    r.off = 0;
+    r.w = 0;
+    if (active) {
+        const long long g = slot >> 5;
+        r.off = goff ? goff[g] : g * 32LL * uw;
+        r.w = goff ? (goff[g + 1] - (int)r.off) >> 5 : uw;
+    }
+    r.rhs = 0.0;
+    r.piv = 1.0;
+    r.rinv = 1.0;
+    if (active && r.row >= 0) {
+        r.rhs = b[r.row];
+        if (HAS_DIAG) {
+            r.piv = sdiag[slot];
+            r.rinv = sdinv[slot];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_CHUNK; ++u) {
+        const bool in = u < r.w;
+        r.c[u] = in ? scol[r.off + 32 * u + r.lane] : -1;
+        r.a[u] = in ? sval[r.off + 32 * u + r.lane] : 0.0;
+    }
+}
+
+template <bool HAS_DIAG>
+__device__ __forceinline__ void bw_finish(const BwRow &r, const int *__restrict__ scol,
+                                          const double *__restrict__ sval, double *xs, int wmask, int pos, double *x) {
+    if (r.row < 0) return;
+    double s = r.rhs;
+#pragma unroll
+    for (int u = 0; u < SELL_CHUNK; ++u)
+        if (r.c[u] >= 0) s -= r.a[u] * xs[r.c[u] & wmask];
+    for (int k = SELL_CHUNK; k < r.w; ++k) {
+        const int j = scol[r.off + 32 * k + r.lane];
+        if (j >= 0) s -= sval[r.off + 32 * k + r.lane] * xs[j & wmask];
+    }
+    if (HAS_DIAG) s = exact_div(s, r.piv, r.rinv);
+    xs[pos & wmask] = s;
+    x[r.row] = s;
+}
+
+template <bool HAS_DIAG>
+__global__ void __launch_bounds__(BL_THREADS) sptrsv_blockwin_sell(int n_levels, const int *__restrict__ sstart,
+                                                                   const int *__restrict__ cnt,
+                                                                   const int *__restrict__ lbase,
+                                                                   const int *__restrict__ order,
+                                                                   const int *__restrict__ goff, int uw,
+                                                                   const int *__restrict__ scol,
+                                                                   const double *__restrict__ sval,
+                                                                   const double *__restrict__ sdiag,
+                                                                   const double *__restrict__ sdinv, int wmask,
+                                                                   const double *__restrict__ b, double *x) {
+    extern __shared__ double xs_win[];
+    const int *st = sstart + (long long)blockIdx.x * n_levels;
+    const int *ct = cnt + (long long)blockIdx.x * n_levels;
+    const int *lb = lbase + (long long)blockIdx.x * n_levels;
+    const int tid = threadIdx.x;
+    int c_cur = n_levels > 0 ? ct[0] : 0, c_n = n_levels > 1 ? ct[1] : 0;
+    int s_cur = n_levels > 0 ? st[0] : 0, s_n = n_levels > 1 ? st[1] : 0;
+    int p_cur = n_levels > 0 ? lb[0] : 0, p_n = n_levels > 1 ? lb[1] : 0;
+    int row0 = tid < c_cur ? order[s_cur + tid] : -1;
+    int row_n = tid < c_n ? order[s_n + tid] : -1;
+    BwRow cur, nxt;
+    bw_load<HAS_DIAG>(nxt, row0, tid < c_cur, s_cur + tid, goff, uw, scol, sval, sdiag, sdinv, b);
+    for (int l = 0; l < n_levels; ++l) {
+        cur = nxt;
+        const int c = c_cur, s0 = s_cur, p0 = p_cur;
+        int c_nn = 0, s_nn = 0, p_nn = 0, row_nn = -1;
+        if (l + 2 < n_levels) {
+            c_nn = ct[l + 2];
+            s_nn = st[l + 2];
+            p_nn = lb[l + 2];
+            if (tid < c_nn) row_nn = order[s_nn + tid];
+        }
+        if (l + 1 < n_levels) bw_load<HAS_DIAG>(nxt, row_n, tid < c_n, s_n + tid, goff, uw, scol, sval, sdiag, sdinv, b);
+        bw_finish<HAS_DIAG>(cur, scol, sval, xs_win, wmask, p0 + tid, x);
+        for (int t = tid + BL_THREADS; t < c; t += BL_THREADS) {  // levels wider than the CTA
+            BwRow extra;
+            bw_load<HAS_DIAG>(extra, order[s0 + t], true, s0 + t, goff, uw, scol, sval, sdiag, sdinv, b);
+            bw_finish<HAS_DIAG>(extra, scol, sval, xs_win, wmask, p0 + t, x);
+        }
+        __syncthreads();
+        c_cur = c_n; s_cur = s_n; p_cur = p_n;
+        c_n = c_nn; s_n = s_nn; p_n = p_nn; row_n = row_nn;
+    }
+}
+
 template <typename K>
 static int coop_grid(K kernel, int threads, int blocks_per_sm_cap, long long work_items) {
     int occ = 0;
@@ -883,6 +994,35 @@ extern "C" int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *st
     else
         sptrsv_blocklocal<false><<<n_blocks, BL_THREADS, 0, st>>>(n_levels, start, cnt, level_rows, row_ptr, col_idx,
                                                                  values, b, x, unit_diag, err);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* block-local sweep with x in a shared-memory window of wmask + 1 doubles */
+extern "C" int ddilu_sptrsv_blockwin_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt,
+                                          const int *lbase, const int *order, const int *goff, int uniform_width,
+                                          const int *scol_loc,
+                                          const double *sval, const double *sdiag, const double *sdinv, int wmask,
+                                          const double *b, double *x, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_blocks <= 0 || n_levels <= 0) return DDILU_OK;
+    if (x == b || wmask < 0 || ((wmask + 1) & wmask) || (sdiag && !sdinv)) return DDILU_ERR_ARG;
+    const size_t smem = sizeof(double) * (size_t)(wmask + 1);
+    if (smem > 200 * 1024) return DDILU_ERR_ARG;
+    void *fn = sdiag ? (void *)sptrsv_blockwin_sell<true> : (void *)sptrsv_blockwin_sell<false>;
+    static size_t attr[2] = {0, 0};
+    if (attr[sdiag ? 1 : 0] < smem) {
+        DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[sdiag ? 1 : 0] = smem;
+    }
+    if (sdiag)
+        sptrsv_blockwin_sell<true><<<n_blocks, BL_THREADS, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
+                                                                      uniform_width, scol_loc, sval, sdiag, sdinv, wmask,
+                                                                      b, x);
+    else
+        sptrsv_blockwin_sell<false><<<n_blocks, BL_THREADS, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
+                                                                       uniform_width, scol_loc, sval, sdiag, sdinv,
+                                                                       wmask, b, x);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

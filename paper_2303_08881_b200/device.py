@@ -10,6 +10,7 @@ the reference's int64 arrays (sparse.py:95-96); nnz < 2^31 is enforced here.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -367,6 +368,7 @@ def sptrsv_tiled(ts: TileSched, b: torch.Tensor, out: torch.Tensor, check: bool 
 USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)
 UNIFORM_SELL = True
 USE_GWAIT = True
+USE_BLOCK_WINDOW = os.environ.get("DDILU_BLOCK_WINDOW", "0") == "1"   # interface factors: CTA-per-block sweep, x window in shared memory
 USE_BLOCK_LOCAL = False   # "sell" | "csr": CTA-per-block sweeps (measured slower: 0.77 us/level floor)
 
 
@@ -399,6 +401,83 @@ def build_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> S
 
 
 BLOCK_LOCAL_MAX_WIDTH = 1024   # average rows per level per block up to which the CTA-per-block sweep is used
+
+
+BLOCK_WINDOW_MAX = 16384   # doubles of shared memory per block (128 KB)
+
+
+@dataclass
+class BlockWindow:
+    """Plan of the block-local sweep with x in a shared-memory window (`ddilu_sptrsv_blockwin_sell`)."""
+
+    lbase: torch.Tensor        # [n_blocks * n_levels] block-local position of the first row of (block, level)
+    scol_loc: torch.Tensor     # sell.scol with block-local positions instead of row ids
+    sdinv: torch.Tensor | None  # RN(1 / pivot), 0 where the kernel must divide
+    wmask: int
+
+
+def enable_block_window(t: DeviceCsr, sched: Schedule, seg_ptr, upper: bool, unit_diag: bool) -> "BlockWindow | None":
+    """Block-diagonal factor with narrow levels (interface factors: one block per subdomain): number the rows of a
+    block in schedule order and check that every dependency lies less than a shared-memory window behind the end
+    of the level that reads it.  Returns None when the factor does not qualify."""
+    if sched.n == 0 or not enable_block_local(sched, seg_ptr):
+        return None
+    sell = get_sell(t, sched, upper, unit_diag)
+    bl, L, n = sched.blocks, sched.n_levels, sched.n
+    nb = bl.n_blocks
+    cnt = bl.cnt.view(nb, L).to(torch.int64)
+    base = torch.cumsum(cnt, 1) - cnt                       # block-local position of the first row of a level
+    flat_cnt = cnt.reshape(-1)
+    seg = torch.repeat_interleave(torch.arange(nb * L, device=dev()), flat_cnt)     # (block, level) of element e
+    first = torch.cumsum(flat_cnt, 0) - flat_cnt
+    within = torch.arange(int(flat_cnt.sum().item()), device=dev()) - first[seg]
+    q = bl.start.to(torch.int64)[seg] + within                                       # position in level_rows
+    rows = sched.level_rows.to(torch.int64)[q]
+    lp = torch.empty(n, dtype=torch.int64, device=dev())
+    lend = torch.empty(n, dtype=torch.int64, device=dev())
+    lp[rows] = base.reshape(-1)[seg] + within
+    lend[rows] = (base + cnt).reshape(-1)[seg]
+    G = sched.n_slots // 32
+    if sell.goff is None:
+        n_ent = G * sell.width * 32
+        e = torch.arange(n_ent, device=dev())
+        grp = e // (32 * sell.width)
+    else:
+        n_ent = int(sell.goff[G].item())
+        e = torch.arange(n_ent, device=dev())
+        grp = torch.searchsorted(sell.goff[: G + 1].to(torch.int64), e, right=True) - 1
+    dep = sell.scol[:n_ent].to(torch.int64)
+    valid = dep >= 0
+    qd = lp[dep.clamp(min=0)]
+    slot_rows = sched.order.to(torch.int64)[grp * 32 + (e & 31)]      # entries of a group are lane-minor
+    row_end = lend[slot_rows.clamp(min=0)]
+    need = torch.where(valid & (slot_rows >= 0), row_end - qd, torch.zeros_like(qd))
+    max_need = int(need.max().item()) if need.numel() else 1
+    w = 1
+    while w < max(max_need, 32):
+        w <<= 1
+    if os.environ.get("DDILU_DEBUG_WINDOW"):
+        print("block window: need", max_need, "window", w, "blocks", nb, "levels", L, flush=True)
+    if w > BLOCK_WINDOW_MAX:
+        return None
+    scol_loc = torch.full((max(1, sell.scol.numel()),), -1, dtype=I32, device=dev())
+    scol_loc[:n_ent] = torch.where(valid, qd, torch.full_like(qd, -1)).to(I32)
+    sdinv = None
+    if sell.sdiag is not None:
+        d = sell.sdiag
+        a = d.abs()
+        ok = (a >= 2.0 ** -400) & (a < 2.0 ** 401)          # the exponent window of exact_div (csrc/common.cuh)
+        sdinv = torch.where(ok, 1.0 / d, torch.zeros_like(d)).contiguous()
+    return BlockWindow(base.to(I32).reshape(-1).contiguous(), scol_loc, sdinv, w - 1)
+
+
+def sptrsv_block_window(t: DeviceCsr, sched: Schedule, bw: BlockWindow, b: torch.Tensor, out: torch.Tensor, upper: bool,
+                        unit_diag: bool):
+    bl = sched.blocks
+    sell = get_sell(t, sched, upper, unit_diag)
+    call("ddilu_sptrsv_blockwin_sell", bl.n_blocks, sched.n_levels, bl.sstart, bl.cnt, bw.lbase, sched.order,
+         sell.goff, sell.width, bw.scol_loc, sell.sval, sell.sdiag, bw.sdinv, bw.wmask, b, out)
+    return out
 
 
 def enable_block_local(sched: Schedule, seg_ptr) -> bool:

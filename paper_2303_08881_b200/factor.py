@@ -84,6 +84,7 @@ class DevFactors:
         if sched_l is not None:
             self._levs[False] = (sched_l.lev, sched_l.n_levels)
         self._tl = self._tu = None  # tiled layouts (D.TileSched) when the factor tiles
+        self._bw = None             # (L, U) shared-memory-window plans of the block-local sweep
         self._tmp = None
 
     @property
@@ -126,6 +127,10 @@ class DevFactors:
                     self._tu = ts
                 else:
                     self._tl = ts
+        if seg_ptr is not None and D.USE_BLOCK_WINDOW and self.n:
+            bwl = D.enable_block_window(self.lower, self.sched_l, seg_ptr, False, True)
+            bwu = D.enable_block_window(self.upper, self.sched_u, seg_ptr, True, False) if bwl is not None else None
+            self._bw = (bwl, bwu) if bwu is not None else None
         if seg_ptr is not None and (self._tl is None or self._tu is None):
             D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
         if self._tl is None:
@@ -137,11 +142,15 @@ class DevFactors:
         return self
 
     def lower_solve(self, b, out):
+        if self._bw is not None:
+            return D.sptrsv_block_window(self.lower, self.sched_l, self._bw[0], b, out, False, True)
         if self._tl is not None:
             return D.sptrsv_tiled(self._tl, b, out)
         return D.sptrsv(self.lower, self.sched_l, b, out, False, True)
 
     def upper_solve(self, b, out):
+        if self._bw is not None:
+            return D.sptrsv_block_window(self.upper, self.sched_u, self._bw[1], b, out, True, False)
         if self._tu is not None:
             return D.sptrsv_tiled(self._tu, b, out)
         return D.sptrsv(self.upper, self.sched_u, b, out, True, False)

@@ -7,12 +7,14 @@ estimate-based in-cycle break, convergence declared only on the recomputed true
 residual.  What changed is where the work runs:
 
 * vectors (V, Z, w, x, r) never leave HBM,
-* one MGS step is j+2 launches of a fused kernel (w -= h_i v_i together with
-  the next dot product; 32n bytes per step instead of the reference's 40n),
-  the h coefficients stay on the device between them,
+* the MGS loop runs in blocks of 4 basis vectors (`ddilu_mgs_block`: one pass
+  subtracts the previous block and accumulates the next block's dots and Gram
+  entries, from which the SAME coefficients h_i = <v_i, w_i> follow; 20n bytes
+  per basis vector instead of the reference's 40n), the coefficients stay on
+  the device between the passes,
 * the host sees one small copy per Arnoldi step (the new Hessenberg column),
   which it needs for the rotation / stopping logic,
-* with several ranks every dot is followed by a scalar allreduce.
+* with several ranks every block of dots is followed by one small allreduce.
 """
 
 from __future__ import annotations

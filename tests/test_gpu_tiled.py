@@ -179,3 +179,47 @@ def _strict_lower(a):
                 ci.append(int(a.col_idx[k])); v.append(float(a.values[k]))
         rp.append(len(ci))
     return np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int64), np.array(v)
+
+
+@pytest.mark.parametrize("dims,p", [((20, 20, 20), 8), ((24, 16, 12), 4), ((40, 40), 4)])
+def test_block_window_sweep_bit_exact(P, orc, dims, p):
+    """Interface factors solved by the CTA-per-block sweep with x in a shared-memory window
+    (`ddilu_sptrsv_blockwin_sell`): same bits as the oracle's serial solves, L and U."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    a = P.aniso3d(*dims) if len(dims) == 3 else P.aniso2d(*dims)
+    layout = P.classify_and_order(a, P.partition(a, p, dims), p)
+    m = P.make_preconditioner("schur", a, layout)
+    f, s = m._p.schur, m.system
+    assert f.n > 0
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal(f.n)
+    bd = D.to_device_f64(b)
+    for upper, t, sched in ((False, f.lower, f.sched_l), (True, f.upper, f.sched_u)):
+        bw = D.enable_block_window(t, sched, s.ext_ptr, upper, not upper)
+        assert bw is not None, "interface factor did not qualify for the window sweep"
+        assert (bw.wmask + 1) & bw.wmask == 0 and bw.wmask + 1 <= D.BLOCK_WINDOW_MAX
+        out = D.empty_f64(f.n)
+        D.sptrsv_block_window(t, sched, bw, bd, out, upper, not upper)
+        torch.cuda.synchronize()
+        h = P.CsrMatrix.from_device(t)
+        oc = orc.Csr(h.n_rows, h.n_cols, h.row_ptr, h.col_idx, h.values)
+        ref = orc.tri_solve_upper(oc, b) if upper else orc.tri_solve_lower(oc, b, True)
+        assert np.array_equal(out.cpu().numpy(), ref), ("U" if upper else "L")
+
+
+def test_block_window_refuses_far_dependencies(P):
+    """A factor whose rows reach further back than the largest window must not get a plan."""
+    from paper_2303_08881_b200 import device as D
+    n = 3 * D.BLOCK_WINDOW_MAX
+    # bidiagonal-plus-first-column lower factor: every row depends on row 0 -> distance up to n
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci, va = [], []
+    for i in range(n):
+        cols = [0, i - 1, i] if i > 1 else ([0, 1] if i == 1 else [0])
+        ci += cols
+        va += [0.5] * (len(cols) - 1) + [1.0]
+        rp[i + 1] = len(ci)
+    lo = P.CsrMatrix(n, n, rp, np.array(ci, dtype=np.int64), np.array(va)).device()
+    sched = D.build_schedule(lo, False)
+    assert D.enable_block_window(lo, sched, np.array([0, n]), False, True) is None
