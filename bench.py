@@ -293,6 +293,7 @@ def run_ours(args):
                                 "algorithmic_bytes_per_step": byts,
                                 "full_pass_us": float(np.mean(full)) * 1e6 if full else None,
                                 "full_pass_gbs": 80 * s.n_loc / float(np.mean(full)) / 1e9 if full else None,
+                                "full_pass_traffic": _traffic(f"mgs_block_4_4_{args.n}"),
                                 "vector_by_vector_bytes_per_step": float(sum(
                                     8 * s.n_loc * (4 * (j + 1) + 1) for j in _arnoldi_js(rec["its"])))}
     tr = sorted(e0.elapsed_time(e1) * 1e-3 for e0, e1, _ in prof_all.get(trsv_name, []))
@@ -308,6 +309,14 @@ def run_ours(args):
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, full_its=rec["its"])
     print(json.dumps(line), flush=True)
+
+
+def _traffic(key):
+    """dram bytes per launch from the committed ncu capture (profiles/traffic.json), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+    except Exception:
+        return None
 
 
 def _arnoldi_js(its, restart=50):
