@@ -34,6 +34,7 @@ struct TrsvTuning {
     unsigned sleep_ns = 0;
     int pipe = 0;            // 1: software-pipelined SELL kernel, 0: plain SELL kernel
     int pipe_warps_per_sm = 8;
+    int win_threads = 0;   // CTA size of the window sweep (0: BL_THREADS)
     int stage_mask = -1;     // -1: by level width (measured: narrow levels -> 3, wide levels -> 4)
                              // bit0: far stage (sleep-poll 3 levels back), bit1: mid stage (spin 2 levels
                              // back), bit2: near stage (spin on the group's own latest dependency)
@@ -778,7 +779,7 @@ __global__ void __launch_bounds__(BL_THREADS) sptrsv_blockwin_sell(int n_levels,
         }
         if (l + 1 < n_levels) bw_load<HAS_DIAG>(nxt, row_n, tid < c_n, s_n + tid, goff, uw, scol, sval, sdiag, sdinv, b);
         bw_finish<HAS_DIAG>(cur, scol, sval, xs_win, wmask, p0 + tid, x);
-        for (int t = tid + BL_THREADS; t < c; t += BL_THREADS) {  // levels wider than the CTA
+        for (int t = tid + (int)blockDim.x; t < c; t += (int)blockDim.x) {  // levels wider than the CTA
             BwRow extra;
             bw_load<HAS_DIAG>(extra, order[s0 + t], true, s0 + t, goff, uw, scol, sval, sdiag, sdinv, b);
             bw_finish<HAS_DIAG>(extra, scol, sval, xs_win, wmask, p0 + t, x);
@@ -815,6 +816,7 @@ extern "C" int ddilu_set_tuning(const char *key, int value) {
     else if (!strcmp(key, "trsv_stage_mask")) g_trsv.stage_mask = value;
     else if (!strcmp(key, "trsv_far_sleep_ns")) g_trsv.far_sleep_ns = value;
     else if (!strcmp(key, "trsv_pipe_warps_per_sm")) g_trsv.pipe_warps_per_sm = value;
+    else if (!strcmp(key, "win_threads")) g_trsv.win_threads = value;
     else return DDILU_ERR_ARG;
     return DDILU_OK;
 }
@@ -1015,12 +1017,13 @@ extern "C" int ddilu_sptrsv_blockwin_sell(int n_blocks, int n_levels, const int 
         DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[sdiag ? 1 : 0] = smem;
     }
+    const int threads = g_trsv.win_threads > 0 ? g_trsv.win_threads : BL_THREADS;
     if (sdiag)
-        sptrsv_blockwin_sell<true><<<n_blocks, BL_THREADS, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
+        sptrsv_blockwin_sell<true><<<n_blocks, threads, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
                                                                       uniform_width, scol_loc, sval, sdiag, sdinv, wmask,
                                                                       b, x);
     else
-        sptrsv_blockwin_sell<false><<<n_blocks, BL_THREADS, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
+        sptrsv_blockwin_sell<false><<<n_blocks, threads, smem, st>>>(n_levels, sstart, cnt, lbase, order, goff,
                                                                        uniform_width, scol_loc, sval, sdiag, sdinv,
                                                                        wmask, b, x);
     DDILU_LAUNCH_CHECK();

@@ -47,9 +47,13 @@ def main():
         rec[which + "_tiled_us"] = timed(tiled, flush)
         if bw is not None:
             win = lambda: D.sptrsv_block_window(t, sched, bw, r, x1, upper, not upper)
-            rec[which + "_window_us"] = timed(win, flush)
-            rec[which + "_window_warm_us"] = timed(win, torch.empty(1, dtype=torch.float64, device="cuda"))
-            rec[which + "_same_bits"] = bool(torch.equal(x0, x1))
+            from paper_2303_08881_b200._lib import query
+            for thr in (1024, 512, 384, 256, 128):
+                query("ddilu_set_tuning", b"win_threads", thr)
+                rec[which + f"_window_{thr}_us"] = timed(win, flush)
+                rec[which + f"_window_{thr}_warm_us"] = timed(win, torch.empty(1, dtype=torch.float64, device="cuda"))
+                rec[which + f"_same_bits_{thr}"] = bool(torch.equal(x0, x1))
+            query("ddilu_set_tuning", b"win_threads", 0)
             rec[which + "_window"] = bw.wmask + 1
     print(json.dumps(rec), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
