@@ -55,6 +55,10 @@ struct TiledTuning {
     long long *debug = nullptr;  // optional device buffer: 8 int64 per CTA of cycle counters (scripts/probe_tiled.py)
 };
 static TiledTuning g_tiled;
+// timing probes of the rotating kernel (scripts/probe_tiled.py --probe): 1 = right-hand side read from CONTIGUOUS
+// (wrong) addresses, 2 = every result stored to L2 twice, 4 = right-hand side gathered twice.  Flags 2 and 4 keep the
+// results intact; flag 1 does not (timing only).  They measure how much the scattered 8-byte accesses cost.
+__device__ int d_tile_probe = 0;
 
 
 #define GRID_STRIDE_Q(i, n) \
@@ -645,12 +649,21 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
             const int T = hdr[H_T];
             const int *rows = (const int *)(blk + hdr[H_OFF_ROWS]);
             double *xsk = xs + (size_t)(j & 1) * xstride;   // slot s holds b[row] until the row is solved
+            const int probe = d_tile_probe;
+            const long long fake0 = ((long long)blockIdx.x + (long long)j * G) * 448;
             for (int s0 = 0; s0 < T; s0 += 256) {
                 double v[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int s = s0 + u * 32 + lane;
-                    v[u] = s < T ? __ldg(b + rows[s]) : 0.0;
+                    v[u] = s < T ? __ldg(b + ((probe & 1) ? fake0 + s : (long long)rows[s])) : 0.0;
+                }
+                if (probe & 4) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int s = s0 + u * 32 + lane;
+                        if (s < T) v[u] += 0.0 * ld_l2(b + rows[s]);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -712,6 +725,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
         // per-level critical path is  wake-up -> x loads -> multiply/subtract chain -> store -> arrive.
         const int cw = warp - TILE_HELPERS / 32;
         constexpr int NC = TILE_NW * 32;
+        const bool probe2 = (d_tile_probe & 2) != 0;
         long long t_start = 0, t_wait_tile = 0, t_wait_ext = 0, t_levels = 0, n_lv = 0;
         if (dbg) t_start = clock64();
         for (int k = 0; k < nk; ++k) {
@@ -783,6 +797,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
                 // publish to L2 AFTER the arrives: a barrier operation issued behind a global store waits for
                 // the store (an L2 round trip); this warp's next barrier operation is >= 1 level away
                 if (itm.row >= 0) st_l2(x + itm.row, scrub_sentinel(sum));
+                if (probe2 && itm.row >= 0) st_l2(x + itm.row, scrub_sentinel(sum));
                 if (q + 1 < n_it)
                     tile_item_load<HAS_DIAG, KP>(itm, items + 2 * (q + 1), lane, xsk, zslot, piv, rows, codes, vals);
             }
@@ -1101,6 +1116,8 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
         g_tiled.ctas_per_sm = value;
     } else if (eq("grid_cap")) {
         g_tiled.grid_cap = value;
+    } else if (eq("probe")) {
+        DDILU_CHECK(cudaMemcpyToSymbol(d_tile_probe, &value, sizeof(int)));
 
     } else {
         return DDILU_ERR_ARG;

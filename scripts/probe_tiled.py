@@ -49,17 +49,19 @@ def main():
     ap.add_argument("--kernel", default="")
     ap.add_argument("--slab", default="")
     ap.add_argument("--wpb", type=int, default=0)
+    ap.add_argument("--probe", type=int, default=0, help="timing probes of the rotating kernel (csrc/tiled.cu d_tile_probe)")
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
 
     def emit(**kw):
-        kw.update(n=args.n, p=args.p)
+        kw.update(n=args.n, p=args.p, probe=args.probe)
         print(json.dumps(kw), flush=True)
         out.write(json.dumps(kw) + "\n")
         out.flush()
 
     query("ddilu_tiled_set_tuning", b"grid_cap", args.grid_cap)
+    query("ddilu_tiled_set_tuning", b"probe", args.probe)
     if args.nap >= 0:
         query("ddilu_tiled_set_tuning", b"nap_ns", args.nap)
     if args.slab:
@@ -142,6 +144,8 @@ def main():
                 t = timed(sell_t, flush=flush)
                 rec.update(sell_us=t * 1e6, sell_frac=nbytes / t / 1e9 / PEAK)
             emit(**rec)
+    if args.probe:
+        return   # probe 1 reads wrong right-hand sides: timings only
     b = P.default_rhs(a)
     x, rep = P.fgmres(a, b, m=m.apply)
     emit(what="solve", pc=args.pc, its=rep.iterations, solve_s=rep.solve_seconds, relres=rep.final_relres,
