@@ -135,6 +135,53 @@ def spmv(a: DeviceCsr, x: torch.Tensor, out: torch.Tensor, b: torch.Tensor | Non
 
 
 @dataclass
+class CompactRows:
+    """The non-empty rows of a very sparse coupling block (Z: interior x exterior has entries in the rows next to
+    the interface only): `vec[rows] -= A[rows, :] x` touches those rows instead of streaming all of them."""
+
+    rows: torch.Tensor      # int32 indices of the non-empty rows
+    csr: DeviceCsr          # the same entries (col_idx / values shared) with a compacted row_ptr
+    t_in: torch.Tensor
+    t_out: torch.Tensor
+    zeros: torch.Tensor = None
+
+
+def compact_rows(a: DeviceCsr, max_fraction: float = 0.25) -> "CompactRows | None":
+    if a.n_rows == 0 or a.nnz == 0:
+        return None
+    cnt = a.rp[1:] - a.rp[:-1]
+    rows = torch.nonzero(cnt > 0).reshape(-1)
+    k = int(rows.numel())
+    if k == 0 or k > max_fraction * a.n_rows:
+        return None
+    rp = zeros_i32(k + 1)
+    rp[1:] = torch.cumsum(cnt[rows], 0).to(I32)      # empty rows hold no entries: col_idx / values stay as they are
+    return CompactRows(rows.to(I32).contiguous(), DeviceCsr(k, a.n_cols, rp, a.ci, a.val, a.nnz), empty_f64(k), empty_f64(k))
+
+
+def sub_compact(c: CompactRows, x: torch.Tensor, vec: torch.Tensor):
+    """vec[rows] = vec[rows] - A[rows, :] x, the same row arithmetic as `spmv(..., b=vec, mode=1)`; the other rows of
+    `b - A x` equal b bit for bit (b - 0.0)."""
+    k = c.csr.n_rows
+    gather(k, c.rows, vec, c.t_in)
+    spmv(c.csr, x, c.t_out, b=c.t_in, mode=1)
+    scatter(k, c.rows, c.t_out, vec)
+
+
+def spmv_compact(c: CompactRows, x: torch.Tensor, out: torch.Tensor, n_rows: int, negate: bool = False):
+    """out[:n_rows] = A x for a matrix whose non-empty rows are `c.rows` (the empty rows give +0.0, as the row loop does)."""
+    k = c.csr.n_rows
+    out[:n_rows].zero_()
+    if negate:   # 0 - A x: negation commutes with every later operation bit for bit (only the sign of exact zeros differs)
+        if c.zeros is None:
+            c.zeros = torch.zeros(k, dtype=F64, device=dev())
+        spmv(c.csr, x, c.t_out, b=c.zeros, mode=1)
+    else:
+        spmv(c.csr, x, c.t_out)
+    scatter(k, c.rows, c.t_out, out)
+
+
+@dataclass
 class Schedule:
     """Level schedule of a triangular factor (SURVEY.md 8c definition)."""
 

@@ -405,6 +405,9 @@ class BjIluPrecond(_DDPrecond):
         self._f.solve(r, z)
 
 
+COMPACT_Z = True   # schur apply: update only the rows of Z that have entries (the full pass streamed 20 n bytes)
+
+
 class SchurIluPrecond(_DDPrecond):
     """precond.py:221-267."""
 
@@ -429,6 +432,7 @@ class SchurIluPrecond(_DDPrecond):
         self._ybuf = D.empty_f64(max(1, ne + nh))
         self._partial = None
         self._coupling_host = None
+        self._zc = D.compact_rows(self._p.z) if COMPACT_Z else None   # Z has entries next to the interface only
 
     # host views
     @property
@@ -497,8 +501,12 @@ class SchurIluPrecond(_DDPrecond):
         D.spmv(p.w, self._fp, self._g, b=r[ni:], mode=1)              # ghat = r_ext - W fp
         self._schur_solve(self._g, self._rhs)                         # S~^-1 ghat
         self._inner.solve(self._reduced_matvec, self._rhs, self._y, n_global=s.n_ext_global)
-        D.spmv(p.z, self._y, self._t1, b=self._fp, mode=1)            # fp - Z y
-        p.interior.upper_solve(self._t1, z[:ni])
+        if self._zc is not None:
+            D.sub_compact(self._zc, self._y, self._fp)                # fp - Z y on the rows that have entries, in place
+            p.interior.upper_solve(self._fp, z[:ni])
+        else:
+            D.spmv(p.z, self._y, self._t1, b=self._fp, mode=1)        # fp - Z y
+            p.interior.upper_solve(self._t1, z[:ni])
         if ne:
             z[ni:ni + ne].copy_(self._y[:ne])
 
@@ -524,6 +532,7 @@ class RapIluPrecond(_DDPrecond):
         l_b, u_b, w, z, l_s, u_s = d_carve(coarse, s.n_int)
         self._interior = DevFactors(l_b, u_b).prepare(part=s.tile_part_interior())
         self._w, self._zt = w, z
+        self._ztc = D.compact_rows(z) if COMPACT_Z else None
         self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))
         self._coarse_kind = coarse
         ni, ne, nh = s.n_int, s.n_ext, s.n_halo
@@ -591,9 +600,14 @@ class RapIluPrecond(_DDPrecond):
         """out = [-U_B^-1 (Z v); v]  (precond.py:337-346)."""
         s = self.system
         ni, ne = s.n_int, s.n_ext
-        D.spmv(self._zt, v, self._ti)
-        self._interior.upper_solve(self._ti, self._ti2)
-        D.ewise(ni, self._ti2, None, 2, out)
+        if self._ztc is not None:
+            # Z has entries next to the interface only; U_B^-1 (-(Z v)) = -(U_B^-1 (Z v)) bit for bit
+            D.spmv_compact(self._ztc, v, self._ti, ni, negate=True)
+            self._interior.upper_solve(self._ti, out)
+        else:
+            D.spmv(self._zt, v, self._ti)
+            self._interior.upper_solve(self._ti, self._ti2)
+            D.ewise(ni, self._ti2, None, 2, out)
         if ne:
             out[ni:ni + ne].copy_(v[:ne])
 
