@@ -241,3 +241,46 @@ def test_known_answers_from_reference_tests(P):
     t = P.csr_from_dense(np.array([[4.0, 0.0, 0.0], [0.0, 4.0, 0.0], [1.0, 1.0, 4.0]]))
     f = P.ilut(t, 0.0, 1)
     assert np.array_equal(f.lower.col_idx[f.lower.row_ptr[2]:f.lower.row_ptr[3]], [0])
+
+
+def test_compact_row_updates_match_the_full_pass(P):
+    """Coupling blocks with few non-empty rows (Z of the two-level preconditioners): the compact-row update must give
+    the bits of the full `b - A x` / `A x` passes it replaces (precond.py:262, 343 of the reference)."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    rng = np.random.default_rng(21)
+    n_rows, n_cols = 5000, 300
+    rows = np.sort(rng.choice(n_rows, size=400, replace=False))
+    rp = np.zeros(n_rows + 1, dtype=np.int64)
+    ci, va = [], []
+    for r in rows:
+        k = int(rng.integers(1, 4))
+        cols = np.sort(rng.choice(n_cols, size=k, replace=False))
+        ci += list(cols)
+        va += list(rng.standard_normal(k))
+        rp[r + 1] = k
+    rp = np.cumsum(rp)
+    a = P.CsrMatrix(n_rows, n_cols, rp, np.array(ci, dtype=np.int64), np.array(va)).device()
+    c = D.compact_rows(a)
+    assert c is not None and c.csr.n_rows == len(rows)
+    x = D.to_device_f64(rng.standard_normal(n_cols))
+    b = rng.standard_normal(n_rows)
+    b[rows[0]] = -0.0
+    b[5] = -0.0 if 5 not in rows else b[5]
+    full = D.empty_f64(n_rows)
+    D.spmv(a, x, full, b=D.to_device_f64(b), mode=1)
+    upd = D.to_device_f64(b)
+    D.sub_compact(c, x, upd)
+    assert np.array_equal(full.cpu().numpy().view(np.int64), upd.cpu().numpy().view(np.int64))   # bits, signs of zero included
+    prod, prod_c, neg_c = D.empty_f64(n_rows), D.empty_f64(n_rows + 7), D.empty_f64(n_rows)
+    D.spmv(a, x, prod)
+    prod_c.fill_(3.0)
+    D.spmv_compact(c, x, prod_c, n_rows)
+    assert np.array_equal(prod.cpu().numpy().view(np.int64), prod_c[:n_rows].cpu().numpy().view(np.int64))
+    assert float((prod_c[n_rows:] - 3.0).abs().max()) == 0.0          # nothing written behind the rows
+    D.spmv_compact(c, x, neg_c, n_rows, negate=True)
+    assert np.array_equal(neg_c.cpu().numpy(), -prod.cpu().numpy())   # values; the sign of exact zeros may differ
+    # a matrix with most rows non-empty is left to the streaming kernel
+    dense_rp = np.arange(n_rows + 1, dtype=np.int64)
+    d = P.CsrMatrix(n_rows, n_cols, dense_rp, np.zeros(n_rows, dtype=np.int64), np.ones(n_rows)).device()
+    assert D.compact_rows(d) is None
