@@ -181,6 +181,26 @@ int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigne
 int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
                        int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 
+/* ---- lattice triangular solve (csrc/lattice.cu): the fast path of sparse.py:228-272 for factors whose box
+ * tiles are lattices with one-way axes and <= 3 dependencies per row (7-point ILU(0) factors).  One warp per
+ * tile, results of a step handed to the next through the warp's shared-memory line buffer, row records streamed
+ * through a per-warp cp.async ring, per-tile completion flags instead of a sentinel preset of x.
+ * ddilu_lattice_build: fill = 0 checks the lattice property and sizes the blocks (blk16[q] in 16-byte units,
+ * stats = {failed, max boundary values, max steps, first bad pivot row, max producer tiles, max block bytes,
+ * max rows}); fill = 1 writes
+ * the per-tile table `tab` (32 int4 per tile) and the blocks at blob + 16 * blk16[q] (scanned offsets).
+ * nodes[row] = grid node of a row, dims3 / tdims3 = grid and tile dimensions (x fastest, padded with 1). */
+int ddilu_lattice_build(int fill, int n_tiles, const int *tsched, const int *tile_pos, const int *tile_ptr,
+                        const int *trows, const int *tile_of, const int *row_ptr, const int *col_idx,
+                        const double *values, const int *nodes, const int *dims3, const int *tdims3, int upper,
+                        int has_diag, void *tab, int *blk16, int *stats, unsigned char *blob, void *stream);
+int ddilu_lattice_max_ext(void);
+int ddilu_lattice_set_tuning(const char *key, int value);
+long long ddilu_lattice_smem_bytes(int blkmax, int tmax, int xemax);
+int ddilu_lattice_set_debug(long long *buf);
+int ddilu_sptrsv_lattice(int n_tiles, const void *tab, const unsigned char *blob, int *flags, int n_slots,
+                         int has_diag, int blkmax, int tmax, int xemax, const double *b, double *x, void *stream);
+
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,
                       double *rownorm, void *stream);

@@ -53,6 +53,47 @@ def lib():
     return _lib
 
 
+# ---------------------------------------------------------------------------
+# optional threading (bench.py --impl reference only).  The reference is strictly
+# serial; threads = 1 (the default) IS the pinned oracle.  With threads > 1 the
+# per-domain loops of the preconditioners run side by side (independent work,
+# same bits), SpMV rows and axpy are split over threads (same bits), and the dot
+# product is summed in `threads` contiguous chunks (NOT the reference's
+# left-to-right order: results agree to rounding, iteration counts may move by
+# one).  Tests never enable it.
+
+_threads = 1
+_pool = None
+
+
+def set_threads(n: int) -> int:
+    """Use up to n host threads for the timed reference arm; returns the count in effect."""
+    global _threads, _pool
+    n = max(1, int(n))
+    if _pool is not None:
+        _pool.shutdown()
+        _pool = None
+    _threads = n
+    lib().orc_set_threads(ctypes.c_int(n))
+    if n > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        _pool = ThreadPoolExecutor(max_workers=n)
+    return _threads
+
+
+def _pmap(fn, items):
+    """[fn(x) for x in items]; independent domain work, spread over the pool when threading is on."""
+    items = list(items)
+    if _pool is None or len(items) < 2:
+        return [fn(x) for x in items]
+    # the C kernels run single-threaded inside a domain task (the domains already fill the cores)
+    lib().orc_set_threads(ctypes.c_int(1))
+    try:
+        return list(_pool.map(fn, items))
+    finally:
+        lib().orc_set_threads(ctypes.c_int(_threads))
+
+
 def _p(a):
     return _P(a.ctypes.data) if a is not None else _P(0)
 
@@ -760,16 +801,14 @@ def fixed_gmres(apply_a, b, iters, apply_m=None, happy_tol=1e-14):
 
 def domain_orderings(a: Csr, layout, use_rcm=True):
     """precond.py:137-147: RCM on the interior block only; exteriors keep index order."""
-    out = []
-    for d in range(layout.p):
+    def one(d):
         ints = layout.interior_of[d]
         if use_rcm and len(ints) > 1:
             _, inv = rcm(extract_block(a, ints, ints))
             ints = ints[inv]
         exts = layout.exterior_of[d]
-        out.append(SimpleNamespace(interior_nodes=ints, exterior_nodes=exts,
-                                   nodes=np.concatenate([ints, exts])))
-    return out
+        return SimpleNamespace(interior_nodes=ints, exterior_nodes=exts, nodes=np.concatenate([ints, exts]))
+    return _pmap(one, range(layout.p))
 
 
 def strip_diagonal_blocks(m: Csr, block_of):
@@ -804,20 +843,24 @@ class BjPrecond:
     def __init__(self, a, layout, rule=Rule("ilu0"), use_rcm=True, l1=False):
         self.layout, self.rule = layout, rule
         self.domains = domain_orderings(a, layout, use_rcm)
-        self.factors = []
-        for d, dom in enumerate(self.domains):
+        def one(d):
+            dom = self.domains[d]
             local = take_submatrix(a, dom.nodes, dom.nodes)
             if l1:  # precond.py:207-212
                 shifts = np.empty(len(dom.nodes))
                 lib().orc_l1_row_shifts(_p(a.row_ptr), _p(a.col_idx), _p(a.values), _p(layout.owner),
                                         _I(len(dom.nodes)), _p(_i64(dom.nodes)), _I(d), _p(shifts))
                 local = add_to_diagonal(local, shifts)
-            self.factors.append(factorize(local, rule))
+            return factorize(local, rule)
+        self.factors = _pmap(one, range(len(self.domains)))
 
     def apply(self, r):
         z = np.empty_like(r)
-        for dom, f in zip(self.domains, self.factors):
-            z[dom.nodes] = f.solve(r[dom.nodes])
+
+        def one(d):
+            dom = self.domains[d]
+            z[dom.nodes] = self.factors[d].solve(r[dom.nodes])
+        _pmap(one, range(len(self.domains)))
         return z
 
 
@@ -827,8 +870,8 @@ class SchurPrecond:
     def __init__(self, a, layout, rule=Rule("ilu0"), inner_iters=3, schur_drop_tol=0.0, use_rcm=True):
         self.layout, self.rule, self.inner_iters = layout, rule, inner_iters
         self.domains = domain_orderings(a, layout, use_rcm)
-        self.partial = [partial_ilu(take_submatrix(a, d.nodes, d.nodes), len(d.interior_nodes), rule,
-                                    schur_drop_tol=schur_drop_tol) for d in self.domains]
+        self.partial = _pmap(lambda d: partial_ilu(take_submatrix(a, d.nodes, d.nodes), len(d.interior_nodes), rule,
+                                                   schur_drop_tol=schur_drop_tol), self.domains)
         ext_all = (np.concatenate([d.exterior_nodes for d in self.domains])
                    if layout.n_exterior else np.empty(0, dtype=np.int64))
         block_of = np.repeat(np.arange(layout.p), np.diff(layout.exterior_starts))
@@ -837,8 +880,10 @@ class SchurPrecond:
     def _schur_solve(self, t):
         out = np.empty_like(t)
         s = self.layout.exterior_starts
-        for d, pf in enumerate(self.partial):
-            out[s[d]:s[d + 1]] = pf.schur.solve(t[s[d]:s[d + 1]])
+
+        def one(d):
+            out[s[d]:s[d + 1]] = self.partial[d].schur.solve(t[s[d]:s[d + 1]])
+        _pmap(one, range(len(self.partial)))
         return out
 
     def reduced_matvec(self, y):
@@ -846,18 +891,23 @@ class SchurPrecond:
 
     def apply(self, r):
         s = self.layout.exterior_starts
-        fps = []
         ghat = np.empty(self.layout.n_exterior)
-        for d, (dom, pf) in enumerate(zip(self.domains, self.partial)):
+
+        def forward(d):
+            dom, pf = self.domains[d], self.partial[d]
             fp = tri_solve_lower(pf.interior.lower, r[dom.interior_nodes], unit_diag=True)
-            fps.append(fp)
             ghat[s[d]:s[d + 1]] = r[dom.exterior_nodes] - spmv(pf.w_block, fp)
+            return fp
+        fps = _pmap(forward, range(len(self.domains)))
         y = fixed_gmres(self.reduced_matvec, self._schur_solve(ghat), self.inner_iters)
         z = np.empty_like(r)
-        for d, (dom, pf) in enumerate(zip(self.domains, self.partial)):
+
+        def backward(d):
+            dom, pf = self.domains[d], self.partial[d]
             yd = y[s[d]:s[d + 1]]
             z[dom.interior_nodes] = tri_solve_upper(pf.interior.upper, fps[d] - spmv(pf.z_block, yd))
             z[dom.exterior_nodes] = yd
+        _pmap(backward, range(len(self.domains)))
         return z
 
 
@@ -867,13 +917,13 @@ class RapPrecond:
     def __init__(self, a, layout, modified=True, inner_iters=3, use_rcm=True):
         self.layout, self.inner_iters, self.modified = layout, inner_iters, modified
         self.domains = domain_orderings(a, layout, use_rcm)
-        self.smoother, self.blocks = [], []
-        for dom in self.domains:
+        def one(dom):
             local = take_submatrix(a, dom.nodes, dom.nodes)
             plain = ilu0(local)
-            self.smoother.append(plain)
             coarse = milu0(local) if modified else plain
-            self.blocks.append(extract_two_level_blocks(coarse, len(dom.interior_nodes)))
+            return plain, extract_two_level_blocks(coarse, len(dom.interior_nodes))
+        both = _pmap(one, self.domains)
+        self.smoother, self.blocks = [b[0] for b in both], [b[1] for b in both]
         order = np.concatenate([d.interior_nodes for d in self.domains]
                                + [d.exterior_nodes for d in self.domains])
         self.perm_forward, self.perm_inverse = perm_from_order(order)
@@ -893,17 +943,23 @@ class RapPrecond:
 
     def interpolate(self, v):
         out = np.empty(self.layout.n)
-        for d, blk in enumerate(self.blocks):
+
+        def one(d):
+            blk = self.blocks[d]
             vd = v[self._csl(d)]
             out[self._isl(d)] = -tri_solve_upper(blk.interior.upper, spmv(blk.z_tilde, vd))
             out[self._esl(d)] = vd
+        _pmap(one, range(len(self.blocks)))
         return out
 
     def restrict(self, t):
         out = np.empty(self.layout.n_exterior)
-        for d, blk in enumerate(self.blocks):
+
+        def one(d):
+            blk = self.blocks[d]
             s = tri_solve_lower(blk.interior.lower, t[self._isl(d)], unit_diag=True)
             out[self._csl(d)] = t[self._esl(d)] - spmv(blk.w_tilde, s)
+        _pmap(one, range(len(self.blocks)))
         return out
 
     def coarse_matvec(self, v):
@@ -911,18 +967,22 @@ class RapPrecond:
 
     def _coarse_precond(self, t):
         out = np.empty_like(t)
-        for d, blk in enumerate(self.blocks):
-            out[self._csl(d)] = blk.schur.solve(t[self._csl(d)])
+
+        def one(d):
+            out[self._csl(d)] = self.blocks[d].schur.solve(t[self._csl(d)])
+        _pmap(one, range(len(self.blocks)))
         return out
 
     def apply(self, r):
         b = r[self.perm_inverse]
         xhat = np.empty(self.layout.n)
-        for d, f in enumerate(self.smoother):
+
+        def smooth(d):
             isl, esl = self._isl(d), self._esl(d)
-            sol = f.solve(np.concatenate([b[isl], b[esl]]))
+            sol = self.smoother[d].solve(np.concatenate([b[isl], b[esl]]))
             n1 = isl.stop - isl.start
             xhat[isl], xhat[esl] = sol[:n1], sol[n1:]
+        _pmap(smooth, range(len(self.smoother)))
         res = b - spmv(self.a_perm, xhat)
         v = fixed_gmres(self.coarse_matvec, self.restrict(res), self.inner_iters,
                         apply_m=self._coarse_precond)

@@ -61,6 +61,12 @@ SIGNATURES = {
     "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_fastdiv_selftest": (_I, [_L, ctypes.c_ulonglong, _P, _P]),
     "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_lattice_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
+    "ddilu_lattice_max_ext": (_I, []),
+    "ddilu_lattice_set_tuning": (_I, [_S, _I]),
+    "ddilu_lattice_smem_bytes": (_L, [_I, _I, _I]),
+    "ddilu_lattice_set_debug": (_I, [_P]),
+    "ddilu_sptrsv_lattice": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),

@@ -34,6 +34,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include <mutex>
 #include "ddilu_b200.h"
 
 namespace ddilu {
@@ -1265,18 +1266,32 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
         {(void *)sptrsv_tiled<false, 3, false>, (void *)sptrsv_tiled<false, 6, false>, (void *)sptrsv_tiled<false, 6, true>},
         {(void *)sptrsv_tiled<true, 3, false>, (void *)sptrsv_tiled<true, 6, false>, (void *)sptrsv_tiled<true, 6, true>}};
     void *fn = fns[has_diag ? 1 : 0][sel];
-    // occupancy of (kernel, smem) is looked up once per configuration
+    // occupancy is looked up once per (kernel, shared-memory size): a solve alternates between factors of
+    // different tile sizes (L_B / L_S share an instance), so the cache holds a few sizes per instance and the
+    // opt-in shared-memory attribute only ever grows.  Guarded: the Python host may call from several threads.
     struct Cfg { size_t smem; int occ; };
-    static Cfg cache[2][3] = {{{0, 0}, {0, 0}, {0, 0}}, {{0, 0}, {0, 0}, {0, 0}}};
-    Cfg &cf = cache[has_diag ? 1 : 0][sel];
-    if (cf.smem != smem) {
-        DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int o = 0;
-        DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
-        cf.smem = smem;
-        cf.occ = o;
+    struct Inst { size_t attr; int n; Cfg c[8]; };
+    static Inst cache[2][3];
+    static std::mutex cache_mu;
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> lock(cache_mu);
+        Inst &in = cache[has_diag ? 1 : 0][sel];
+        int hit = -1;
+        for (int i = 0; i < in.n; ++i)
+            if (in.c[i].smem == smem) hit = i;
+        if (hit < 0) {
+            if (in.attr < smem) {
+                DDILU_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                in.attr = smem;
+            }
+            int o = 0;
+            DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+            hit = in.n < 8 ? in.n++ : 7;
+            in.c[hit] = {smem, o};
+        }
+        occ = in.c[hit].occ;
     }
-    int occ = cf.occ;
     if (occ < 1) return DDILU_ERR_ARG;
     if (g_tiled.ctas_per_sm > 0 && occ > g_tiled.ctas_per_sm) occ = g_tiled.ctas_per_sm;
     long long grid = (long long)occ * device_info().sm_count;

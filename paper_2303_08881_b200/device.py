@@ -272,6 +272,7 @@ class TilePartition:
     tile_ptr: torch.Tensor    # int32[n_tiles + 1]
     trows: torch.Tensor       # int32[n] rows grouped by tile, ascending inside a tile
     max_rows: int
+    geom: tuple = None        # (grid node of every row, grid dims, tile dims) when the tiles are grid boxes
 
 
 @dataclass
@@ -339,13 +340,10 @@ def tile_partition(keys: torch.Tensor, key_range: int) -> TilePartition | None:
     return TilePartition(n, n_tiles, tile_of, tpos, tile_ptr, rows, max_rows)
 
 
-def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: bool, unit_diag: bool) -> TileSched | None:
-    """Tile schedule + static blocks of a triangular factor; None when the tile
-    graph is cyclic / too deep or a tile does not fit the shared-memory budget
-    (the caller then uses the sync-free solve)."""
+def tile_schedule(t: DeviceCsr, part: TilePartition, upper: bool):
+    """(tsched, n_tile_levels): the tiles in a topological order of the tile graph (cross-tile dependencies of
+    the factor, relaxed to tile levels on the device); None when the graph is cyclic or too deep."""
     n = t.n_rows
-    if part is None or n == 0 or part.n != n:
-        return None
     cnt = zeros_i32(n + 1)
     call("ddilu_tile_edges_count", n, t.rp, t.ci, int(upper), part.tile_of, cnt)
     exclusive_scan_(cnt, n)
@@ -370,6 +368,99 @@ def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: boo
     n_tile_levels = int(tlev.max().item()) + 1
     tsched = torch.arange(nt, dtype=I32, device=dev())
     sort_pairs_(tlev, tsched, max(1, int(n_tile_levels - 1).bit_length()))
+    return tsched, n_tile_levels
+
+
+@dataclass
+class LatticeSched:
+    """Layout of the lattice solve (csrc/lattice.cu): per tile a 32-entry table and a block of boundary columns
+    + row records in (step, slot, lane) order; tiles in schedule order."""
+
+    n: int
+    n_tiles: int
+    n_tile_levels: int
+    tab: torch.Tensor         # int32[n_tiles * 32 * 4]
+    blob: torch.Tensor        # uint8
+    flags: torch.Tensor       # int32[n_tiles] per-tile completion flags of the running solve
+    n_slots: int              # 1: <= 32 lines per tile, 2: <= 64
+    has_diag: bool
+    bad_row: int
+    blkmax: int = 0           # largest tile block (bytes), row count, boundary-value count: size the shared memory
+    tmax: int = 0
+    xemax: int = 0
+    kind: str = "lattice"
+
+
+USE_LATTICE = os.environ.get("DDILU_LATTICE", "1") == "1"
+
+
+def build_lattice(t: DeviceCsr, part: TilePartition, upper: bool, unit_diag: bool, sched=None) -> "LatticeSched | None":
+    """Lattice layout of a triangular factor whose tiles are boxes of a structured grid (part.geom = (grid node
+    of every row, grid dims, tile dims)); None when some tile is not a lattice with one-way axes, a row has more
+    than 3 dependencies, or the tile graph is cyclic -- the caller then uses the general tiled solve."""
+    geom = getattr(part, "geom", None)
+    n = t.n_rows
+    if not USE_LATTICE or geom is None or n == 0 or part.n != n:
+        return None
+    nodes, dims, tdims = geom
+    d3 = [int(v) for v in dims] + [1] * (3 - len(dims))
+    t3 = [int(v) for v in tdims] + [1] * (3 - len(tdims))
+    if t3[1] * t3[2] > 64 or t3[0] + t3[1] + t3[2] - 2 > 32 or t3[0] * t3[1] * t3[2] > 1024:
+        return None
+    sched = sched if sched is not None else tile_schedule(t, part, upper)
+    if sched is None:
+        return None
+    tsched, n_tile_levels = sched
+    nt = part.n_tiles
+    pos = empty_i32(nt)
+    pos[tsched.long()] = torch.arange(nt, dtype=I32, device=dev())
+    arr = ctypes.c_int * 3
+    dd, tt = arr(*d3), arr(*t3)
+    has_diag = not unit_diag
+    blk = zeros_i32(nt + 1)
+    stats = torch.tensor([0, 0, 0, INT_MAX, 0, 0, 0], dtype=I32, device=dev())
+    args = (nt, tsched, pos, part.tile_ptr, part.trows, part.tile_of, t.rp, t.ci, t.val, nodes,
+            ctypes.addressof(dd), ctypes.addressof(tt), int(upper), int(has_diag))
+    call("ddilu_lattice_build", 0, *args, None, blk, stats, None)
+    st = [int(v) for v in stats.cpu().numpy()]
+    if st[0] or st[1] > query("ddilu_lattice_max_ext"):
+        return None
+    exclusive_scan_(blk, nt)
+    total16 = int(blk[-1].item())
+    blob = torch.empty(max(16, 16 * total16), dtype=torch.uint8, device=dev())
+    tab = torch.empty(nt * 32 * 4, dtype=I32, device=dev())
+    call("ddilu_lattice_build", 1, *args, tab, blk, stats, blob)
+    st = [int(v) for v in stats.cpu().numpy()]
+    if st[0]:
+        return None
+    blkmax, tmax, xemax = (st[5] + 15) & ~15, st[6], st[1]
+    if query("ddilu_lattice_smem_bytes", blkmax, tmax, xemax) > 226 * 1024:
+        return None
+    return LatticeSched(n, nt, n_tile_levels, tab, blob, zeros_i32(nt), 2 if t3[1] * t3[2] > 32 else 1, has_diag, st[3],
+                        blkmax, tmax, xemax)
+
+
+def sptrsv_lattice(ls: LatticeSched, b: torch.Tensor, out: torch.Tensor, check: bool = False):
+    if check and ls.bad_row != INT_MAX:
+        raise TriSolveError(f"zero or missing diagonal at row {ls.bad_row}")
+    call("ddilu_sptrsv_lattice", ls.n_tiles, ls.tab, ls.blob, ls.flags, ls.n_slots, int(ls.has_diag), ls.blkmax,
+         ls.tmax, ls.xemax, b, out)
+    return out
+
+
+def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: bool, unit_diag: bool,
+                sched=None) -> TileSched | None:
+    """Tile schedule + static blocks of a triangular factor; None when the tile
+    graph is cyclic / too deep or a tile does not fit the shared-memory budget
+    (the caller then uses the sync-free solve)."""
+    n = t.n_rows
+    if part is None or n == 0 or part.n != n:
+        return None
+    sched = sched if sched is not None else tile_schedule(t, part, upper)
+    if sched is None:
+        return None
+    tsched, n_tile_levels = sched
+    nt = part.n_tiles
     has_diag = not unit_diag
     args = (nt, tsched, part.tile_ptr, part.trows, part.tile_of, part.tpos, t.rp, t.ci, t.val, lev, int(upper),
             int(has_diag))
@@ -403,7 +494,9 @@ def build_tiles(t: DeviceCsr, lev: torch.Tensor, part: TilePartition, upper: boo
     return TileSched(n, nt, n_tile_levels, blk, blob, stat_max, tmax, emax, kmax, has_diag, bad, kind)
 
 
-def sptrsv_tiled(ts: TileSched, b: torch.Tensor, out: torch.Tensor, check: bool = False):
+def sptrsv_tiled(ts, b: torch.Tensor, out: torch.Tensor, check: bool = False):
+    if ts.kind == "lattice":
+        return sptrsv_lattice(ts, b, out, check)
     if check and ts.bad_row != INT_MAX:
         raise TriSolveError(f"zero or missing diagonal at row {ts.bad_row}")
     entry = {"lean": "ddilu_sptrsv_lean", "warp": "ddilu_sptrsv_warptile", "rot": "ddilu_sptrsv_tiled"}[ts.kind]

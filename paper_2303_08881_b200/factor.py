@@ -117,6 +117,18 @@ class DevFactors:
             # part: one TilePartition for both factors, or a callable (lev, n_levels) -> TilePartition for
             # partitions that depend on the factor's own levels (wavefront-slab tiles)
             for upper in (False, True):
+                fac = self.upper if upper else self.lower
+                if not callable(part) and getattr(part, "geom", None) is not None and part.n == self.n:
+                    # box tiles of a structured grid: the lattice solve if every tile qualifies
+                    sched = D.tile_schedule(fac, part, upper)
+                    ts = D.build_lattice(fac, part, upper, not upper, sched) if sched is not None else None
+                    if ts is None and sched is not None:
+                        ts = D.build_tiles(fac, self._lev(upper)[0], part, upper, not upper, sched)
+                    if upper:
+                        self._tu = ts
+                    else:
+                        self._tl = ts
+                    continue
                 lev, nlev = self._lev(upper)
                 pt = part(lev, nlev) if callable(part) else part
                 ts = D.build_tiles(self.upper if upper else self.lower, lev, pt, upper, not upper) \

@@ -268,9 +268,13 @@ class InnerGmres:
     """krylov.py:213-268 `fixed_gmres` with a persistent device workspace (the
     two-level preconditioners call it once per outer iteration)."""
 
-    def __init__(self, n: int, iters: int, comm: Comm, pad: int = 0, happy_tol: float = 1e-14):
+    def __init__(self, n: int, iters: int, comm: Comm, pad: int = 0, happy_tol: float = 1e-14,
+                 n_global: int | None = None):
         self.n, self.iters, self.comm, self.happy_tol = int(n), int(iters), comm, happy_tol
-        self.m = max(1, min(self.iters, max(self.n, 1)))
+        # the step count follows the GLOBAL system size (krylov.py:232: m = min(iters, n)); a rank with few
+        # (or no) interface unknowns still runs every step, so its workspace is sized from the global count
+        ng = self.n if n_global is None else int(n_global)
+        self.m = max(1, min(self.iters, max(ng, 1)))
         self.ws = Arnoldi(self.n, self.m, comm, flexible=False, pad=pad)
         self.z = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
         self.u = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
@@ -289,7 +293,7 @@ class InnerGmres:
         if ng == 0 or self.iters <= 0:
             out[:n].zero_()
             return out
-        m = min(self.iters, ng)
+        m = min(self.iters, ng, self.m)
         if self.hcols is None:
             self.hcols = torch.zeros((self.m + 1, self.m + 2), dtype=D.F64, device=D.dev())
         H = self.hcols

@@ -65,13 +65,19 @@ def _wrap_owner(host: np.ndarray, dev_t: torch.Tensor | None, grid_hint=None, p:
     out = host.view(_Owner)
     out._dev = dev_t
     out._p = p
+    if dev_t is not None:
+        # the cached device copy is only valid while the host array is untouched: hand it out read-only
+        # (`owner.copy()` is writable and carries no cache); classify_and_order re-checks the flag
+        out.setflags(write=False)
     out.grid_hint = tuple(int(d) for d in grid_hint) if grid_hint is not None else None
     return out
 
 
 def _owner_device(owner) -> torch.Tensor:
     d = getattr(owner, "_dev", None)
-    return d if d is not None else D.to_device_i32(owner)
+    if d is not None and not owner.flags.writeable:
+        return d
+    return D.to_device_i32(np.asarray(owner))
 
 
 def partition(a: CsrMatrix, p: int, grid_hint=None) -> np.ndarray:
@@ -174,7 +180,8 @@ def classify_and_order(a: CsrMatrix, owner, p: int | None = None, grid_hint=None
     owner_h = np.asarray(owner, dtype=np.int64) if not isinstance(owner, _Owner) else owner
     if owner_h.shape != (n,):
         raise ValueError("owner array has wrong length")
-    trusted = isinstance(owner, _Owner) and getattr(owner, "_dev", None) is not None and owner._p is not None
+    trusted = (isinstance(owner, _Owner) and getattr(owner, "_dev", None) is not None and owner._p is not None
+               and not owner.flags.writeable)        # made writable again => may have been edited: re-validate, re-upload
     if p is None:
         p = owner._p if trusted else (int(owner_h.max()) + 1 if n else 1)
     if trusted:

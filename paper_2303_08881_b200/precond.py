@@ -168,6 +168,8 @@ class LocalSystem:
         if which == "int" and self.n_int:
             keys, nk = self._tile_keys(0, self.n_int, self._int_tdims())
             part = D.tile_partition(keys, nk * p)
+            if part is not None:     # box tiles of the grid: candidates for the lattice solve
+                part.geom = (self.nodes[: self.n_int], tuple(lay.grid_hint), tuple(self._int_tdims()))
         elif which == "ext" and self.n_ext:
             part, self._ext_tdims = self._ext_partition(D.TILE_MAX_ROWS, 0, 0)
         elif which == "all":
@@ -421,7 +423,7 @@ class SchurIluPrecond(_DDPrecond):
         self._p.schur.prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))   # interface factors: one block per subdomain
         self._coupling = s.coupling()
         ne, nh = s.n_ext, s.n_halo
-        self._inner = InnerGmres(ne, inner_iters, s.comm, pad=nh)
+        self._inner = InnerGmres(ne, inner_iters, s.comm, pad=nh, n_global=s.n_ext_global)
         self._fp = D.empty_f64(max(1, s.n_int))
         self._t1 = D.empty_f64(max(1, s.n_int))
         self._g = D.empty_f64(max(1, ne))
@@ -536,7 +538,7 @@ class RapIluPrecond(_DDPrecond):
         self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))
         self._coarse_kind = coarse
         ni, ne, nh = s.n_int, s.n_ext, s.n_halo
-        self._inner = InnerGmres(ne, inner_iters, s.comm)
+        self._inner = InnerGmres(ne, inner_iters, s.comm, n_global=s.n_ext_global)
         self._xhat = D.empty_f64(max(1, s.n_loc + nh))
         self._pv = D.empty_f64(max(1, s.n_loc + nh))
         self._res = D.empty_f64(max(1, s.n_loc))

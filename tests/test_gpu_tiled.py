@@ -32,14 +32,16 @@ def _factor_pairs(m):
     return out
 
 
-@pytest.fixture(params=["rot", "warp"])
+@pytest.fixture(params=["lattice", "rot", "warp"])
 def tile_kernel(request):
-    """Run with the production CTA-per-tile kernel and with the warp-per-tile alternatives."""
+    """Run with the production kernels (lattice solve where the tiles qualify, CTA-per-tile kernel elsewhere),
+    with the CTA-per-tile kernel alone and with the warp-per-tile alternatives."""
     from paper_2303_08881_b200 import device as D
-    old = D.TILE_KERNEL
-    D.TILE_KERNEL = request.param
+    old, old_lat = D.TILE_KERNEL, D.USE_LATTICE
+    D.TILE_KERNEL = "rot" if request.param == "lattice" else request.param
+    D.USE_LATTICE = request.param == "lattice"
     yield request.param
-    D.TILE_KERNEL = old
+    D.TILE_KERNEL, D.USE_LATTICE = old, old_lat
 
 
 @pytest.mark.parametrize("dims,p", [((20, 20, 20), 8), ((24, 17, 9), 4), ((40, 40), 4), ((33, 33, 33), 1)])
@@ -56,7 +58,12 @@ def test_tiled_solves_bit_exact(P, orc, dims, p, tile_kernel):
             if f.n == 0:
                 continue
             assert f._tl is not None and f._tu is not None, (pc, name, "factor did not tile")
-            if tile_kernel == "rot":
+            if tile_kernel == "lattice":
+                # purely interior factors of a 3D grid are lattices of 7-point rows; everything else stays "rot"
+                want = "lattice" if (len(dims) == 3 and name in ("interior", "rap-interior")) or \
+                    (len(dims) == 3 and p == 1 and name in ("bj", "smoother")) else "rot"
+                assert f._tl.kind == want and f._tu.kind == want, (pc, name, f._tl.kind, f._tu.kind)
+            elif tile_kernel == "rot":
                 assert f._tl.kind == "rot" and f._tu.kind == "rot"
             else:
                 assert f._tl.kind in ("lean", "warp") and f._tu.kind in ("lean", "warp")
@@ -223,3 +230,49 @@ def test_block_window_refuses_far_dependencies(P):
     lo = P.CsrMatrix(n, n, rp, np.array(ci, dtype=np.int64), np.array(va)).device()
     sched = D.build_schedule(lo, False)
     assert D.enable_block_window(lo, sched, np.array([0, n]), False, True) is None
+
+
+@pytest.mark.parametrize("dims,p,tile", [((40, 37, 29), 8, (8, 8, 8)), ((33, 33, 33), 1, (16, 8, 8)),
+                                         ((21, 20, 19), 2, (8, 8, 4)), ((36, 36, 36), 8, (4, 4, 4))])
+def test_lattice_solves_bit_exact(P, orc, dims, p, tile):
+    """csrc/lattice.cu on ragged boxes, partial tiles and several tile shapes: bit-exact against the oracle's
+    serial solves (sparse.py:228-272), L and U (the U solve runs every axis in the opposite direction)."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    from paper_2303_08881_b200.precond import LocalSystem
+    old = LocalSystem.TILE_DIMS_3D
+    LocalSystem.TILE_DIMS_3D = tile
+    try:
+        a = P.aniso3d(*dims)
+        layout = P.classify_and_order(a, P.partition(a, p, dims), p)
+        m = P.make_preconditioner("schur", a, layout)
+    finally:
+        LocalSystem.TILE_DIMS_3D = old
+    f = m._p.interior
+    assert f._tl.kind == "lattice" and f._tu.kind == "lattice"
+    rng = np.random.default_rng(11)
+    lo, up = P.CsrMatrix.from_device(f.lower), P.CsrMatrix.from_device(f.upper)
+    for rep in range(3):       # repeated solves reuse the per-tile flags
+        b = rng.standard_normal(f.n)
+        bd = D.to_device_f64(b)
+        xl, xu = D.empty_f64(f.n), D.empty_f64(f.n)
+        f.lower_solve(bd, xl)
+        f.upper_solve(bd, xu)
+        torch.cuda.synchronize()
+        ref_l = orc.tri_solve_lower(orc.Csr(lo.n_rows, lo.n_cols, lo.row_ptr, lo.col_idx, lo.values), b, True)
+        ref_u = orc.tri_solve_upper(orc.Csr(up.n_rows, up.n_cols, up.row_ptr, up.col_idx, up.values), b)
+        assert np.array_equal(xl.cpu().numpy(), ref_l), ("L", rep)
+        assert np.array_equal(xu.cpu().numpy(), ref_u), ("U", rep)
+
+
+def test_lattice_refuses_wide_rows(P):
+    """A 27-point factor has up to 13 dependencies per row: no lattice layout, the general kernels take it."""
+    from paper_2303_08881_b200 import device as D
+    dims = (12, 12, 12)
+    a = P.convdiff27(*dims)
+    layout = P.classify_and_order(a, P.partition(a, 1, dims), 1)
+    m = P.make_preconditioner("bj", a, layout)
+    assert m._f._tl is None or m._f._tl.kind != "lattice"
+    b = P.default_rhs(a)
+    x, rep = P.fgmres(a, b, m=m.apply)
+    assert rep.converged
