@@ -181,6 +181,39 @@ int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigne
 int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
                        int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 
+/* ---- block sweep (csrc/sweep.cu): L^-1, U^-1 or U^-1 L^-1 on a block-diagonal factor pair with narrow levels --
+ * the interface factors L_S / U_S, one diagonal block per subdomain (precond.py:239-249 `_schur_solve` inside
+ * `reduced_matvec`, precond.py:361-366 `_coarse_precond`; arithmetic of sparse.py:228-272, bit-exact).  One CTA
+ * per block, the block's x in a shared-memory window, the rows' operands streamed as 256-row pages in schedule
+ * order through a TMA ring, L and U back to back in one launch.
+ * ddilu_sweep_fill: operands of a factor into its pages (k = operand slots per row, gpos / lpos = global padded /
+ * block-local schedule position of every row, gpos_u = position of the row in the U schedule (lower factor only),
+ * window = shared-memory window in doubles, a power of two).
+ * ddilu_sweep_rhs: right-hand side in schedule order, out[i] = base[row] (row_ptr NULL), (A y)[row] (mode 0),
+ * base[row] - (A y)[row] (mode 1: `r_ext - W fp`, precond.py:242-243) or base + A y (mode 2), row = rowof[i],
+ * 0 where rowof[i] < 0 (page padding); with add_out also add_out[i] = add[rowof_u[i]], the vector the U phase
+ * adds to its results, in U schedule order.
+ * ddilu_sweep_solve: phases 1 = L, 2 = U, 3 = L then U; blocks = 8 ints per block {rows, first page, L levels,
+ * U levels, offset into levtab, 0, 0, 0}; stages = ring depth (power of two), sets x nct compute threads that own
+ * rows_per_thread (1, 2, 4) rows of a level each; out[row] = x (+ add[U position of the row]: `y + S^-1 E y`,
+ * precond.py:249). */
+int ddilu_sweep_page_rows(void);
+int ddilu_sweep_helper_threads(void);   /* threads of a CTA that do not compute (TMA issuer, gate, writers) */
+int ddilu_sweep_set_tuning(int writer_sleep_ns, int flags);   /* diagnostics */
+int ddilu_sweep_set_debug(long long *buf);   /* diagnostics: 64 int64 cycle counters per block, NULL = off */
+long long ddilu_sweep_page_bytes(int k, int upper);
+long long ddilu_sweep_smem_bytes(int k, int stages, int window, int max_lev);
+int ddilu_sweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
+                     const int *gpos, const int *lpos, const int *gpos_u, int window, unsigned char *pages,
+                     int *bad_row, void *stream);
+int ddilu_sweep_rhs(int npad, const int *rowof, const int *row_ptr, const int *col_idx, const double *values,
+                    const double *y, const double *base, int mode, double *out, const int *rowof_u, const double *add,
+                    double *add_out, void *stream);
+int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const unsigned char *pages_l,
+                      const unsigned char *pages_u, int k, int window, int stages, int sets, int nct,
+                      int rows_per_thread, int max_lev, int phases, const double *rhs, double *tmp, double *out,
+                      const double *add, void *stream);
+
 /* ---- lattice triangular solve (csrc/lattice.cu): the fast path of sparse.py:228-272 for factors whose box
  * tiles are lattices with one-way axes and <= 3 dependencies per row (7-point ILU(0) factors).  One warp per
  * tile, results of a step handed to the next through the warp's shared-memory line buffer, row records streamed

@@ -17,25 +17,86 @@
  * Index type is int64 like the reference (sparse.py:95-96).
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 typedef int64_t i64;
 
+/* Optional host threading for the TIMED reference arm of bench.py only (`bench.py --impl reference`): the
+ * reference is strictly serial and g_threads = 1 (the default) IS the pinned oracle.  With more threads SpMV
+ * rows and axpy entries are split (same bits) and the dot product is summed in g_threads chunks. */
+#define ORC_MAX_THREADS 256
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : (n > ORC_MAX_THREADS ? ORC_MAX_THREADS : n); }
+
+/* fork-join over contiguous index ranges (pthreads: the image has no libgomp); a call costs ~20 us per thread,
+ * it is used on vectors of >= 65536 entries only */
+typedef struct {
+    void (*fn)(i64 lo, i64 hi, int t, void *ctx);
+    void *ctx;
+    i64 lo, hi;
+    int t;
+} orc_task;
+static void *orc_task_run(void *p)
+{
+    orc_task *k = (orc_task *)p;
+    k->fn(k->lo, k->hi, k->t, k->ctx);
+    return NULL;
+}
+static void orc_parallel(i64 n, int nt, void (*fn)(i64, i64, int, void *), void *ctx)
+{
+    pthread_t th[ORC_MAX_THREADS];
+    orc_task task[ORC_MAX_THREADS];
+    int started[ORC_MAX_THREADS];
+    if (nt < 1)
+        nt = 1;
+    if (nt > ORC_MAX_THREADS)
+        nt = ORC_MAX_THREADS;
+    memset(task, 0, sizeof(orc_task));
+    for (int t = 0; t < nt; ++t) {
+        task[t].fn = fn;
+        task[t].ctx = ctx;
+        task[t].lo = n * t / nt;
+        task[t].hi = n * (t + 1) / nt;
+        task[t].t = t;
+        started[t] = t > 0 && pthread_create(&th[t], NULL, orc_task_run, &task[t]) == 0;
+    }
+    orc_task_run(&task[0]);
+    for (int t = 1; t < nt; ++t) {
+        if (started[t])
+            pthread_join(th[t], NULL);
+        else
+            orc_task_run(&task[t]);
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* sparse core                                                          */
 
 /* sparse.py:219-225 (_spmv): row-serial, left-to-right sum. */
+typedef struct { const i64 *rp, *ci; const double *v, *x; double *out; } spmv_ctx;
+static void spmv_rows(i64 lo, i64 hi, int t, void *p)
+{
+    const spmv_ctx *c = (const spmv_ctx *)p;
+    (void)t;
+    for (i64 i = lo; i < hi; ++i) {
+        double s = 0.0;
+        for (i64 k = c->rp[i]; k < c->rp[i + 1]; ++k)
+            s += c->v[k] * c->x[c->ci[k]];
+        c->out[i] = s;
+    }
+}
 void orc_spmv(i64 n_rows, const i64 *rp, const i64 *ci, const double *v,
               const double *x, double *out)
 {
-    for (i64 i = 0; i < n_rows; ++i) {
-        double s = 0.0;
-        for (i64 k = rp[i]; k < rp[i + 1]; ++k)
-            s += v[k] * x[ci[k]];
-        out[i] = s;
-    }
+    spmv_ctx c = {rp, ci, v, x, out};
+    /* rows are independent: splitting them over threads keeps every bit */
+    if (g_threads > 1 && n_rows > 65536)
+        orc_parallel(n_rows, g_threads, spmv_rows, &c);
+    else
+        spmv_rows(0, n_rows, 0, &c);
 }
 
 /* sparse.py:228-249 (_lower_solve): returns -1 or the failing row. */
@@ -93,8 +154,29 @@ i64 orc_upper_solve(i64 n, const i64 *rp, const i64 *ci, const double *v,
 }
 
 /* sparse.py:275-280 (_vdot). */
+typedef struct { const double *a, *b; double *part; } dot_ctx;
+static void dot_chunk(i64 lo, i64 hi, int t, void *p)
+{
+    const dot_ctx *c = (const dot_ctx *)p;
+    double s = 0.0;
+    for (i64 i = lo; i < hi; ++i)
+        s += c->a[i] * c->b[i];
+    c->part[t] = s;
+}
 double orc_vdot(i64 n, const double *a, const double *b)
 {
+    if (g_threads > 1 && n > 65536) {
+        /* timed reference arm only: g_threads contiguous chunks, partial sums added in chunk order (NOT the
+         * reference's single left-to-right sum; agrees to rounding) */
+        double part[ORC_MAX_THREADS];
+        const int nt = g_threads;
+        dot_ctx c = {a, b, part};
+        orc_parallel(n, nt, dot_chunk, &c);
+        double s = 0.0;
+        for (int t = 0; t < nt; ++t)
+            s += part[t];
+        return s;
+    }
     double s = 0.0;
     for (i64 i = 0; i < n; ++i)
         s += a[i] * b[i];
@@ -102,10 +184,21 @@ double orc_vdot(i64 n, const double *a, const double *b)
 }
 
 /* krylov.py:74-77 (_axpy): w += alpha * v. */
+typedef struct { double alpha; const double *v; double *w; } axpy_ctx;
+static void axpy_range(i64 lo, i64 hi, int t, void *p)
+{
+    const axpy_ctx *c = (const axpy_ctx *)p;
+    (void)t;
+    for (i64 i = lo; i < hi; ++i)
+        c->w[i] += c->alpha * c->v[i];
+}
 void orc_axpy(i64 n, double alpha, const double *v, double *w)
 {
-    for (i64 i = 0; i < n; ++i)
-        w[i] += alpha * v[i];
+    axpy_ctx c = {alpha, v, w};
+    if (g_threads > 1 && n > 65536)
+        orc_parallel(n, g_threads, axpy_range, &c);
+    else
+        axpy_range(0, n, 0, &c);
 }
 
 /* sort one CSR row segment by column (columns are unique, so any sort gives

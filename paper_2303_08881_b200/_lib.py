@@ -61,6 +61,15 @@ SIGNATURES = {
     "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_fastdiv_selftest": (_I, [_L, ctypes.c_ulonglong, _P, _P]),
     "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_sweep_page_rows": (_I, []),
+    "ddilu_sweep_helper_threads": (_I, []),
+    "ddilu_sweep_set_debug": (_I, [_P]),
+    "ddilu_sweep_set_tuning": (_I, [_I, _I]),
+    "ddilu_sweep_page_bytes": (_L, [_I, _I]),
+    "ddilu_sweep_smem_bytes": (_L, [_I, _I, _I, _I]),
+    "ddilu_sweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
+    "ddilu_sweep_rhs": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
+    "ddilu_sweep_solve": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "ddilu_lattice_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
     "ddilu_lattice_max_ext": (_I, []),
     "ddilu_lattice_set_tuning": (_I, [_S, _I]),

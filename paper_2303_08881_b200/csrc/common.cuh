@@ -104,6 +104,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // outside a safe exponent window (zero, subnormal, huge, inf/nan: the remainder would not be exact)
 // and pivots flagged r = 0 at setup take the real division.  Verified bit-for-bit on random and
 // adversarial operands by ddilu_fastdiv_selftest (tests/test_gpu_tiled.py).
+// the rare real division, kept out of line: inlined, the compiler starts its reciprocal iteration (six dependent
+// FMAs) speculatively on every call, in front of the corrections below
+static __device__ __noinline__ double exact_div_slow(double s, double d) { return s / d; }
+
 __device__ __forceinline__ double exact_div(double s, double d, double r) {
     // the corrections start at once; the operand check runs beside them and only a failing check branches
     // (the check-then-branch form put ~25 cycles in front of the five dependent operations on every level)
@@ -115,7 +119,7 @@ __device__ __forceinline__ double exact_div(double s, double d, double r) {
     const unsigned es = ((unsigned)__double2hiint(s) >> 20) & 0x7ffu;
     const unsigned rh = (unsigned)__double2hiint(r) & 0x7fffffffu;   // r == +-0.0 <=> no exponent / mantissa bits
     const bool ok = ((rh | (unsigned)__double2loint(r)) != 0u) && (es - 623u <= 800u);
-    if (!ok) q = s / d;
+    if (!ok) q = exact_div_slow(s, d);
     return q;
 }
 // reciprocal to store for a pivot, 0 = "always divide" (pivot outside the safe exponent window)

@@ -391,7 +391,7 @@ class LatticeSched:
     kind: str = "lattice"
 
 
-USE_LATTICE = os.environ.get("DDILU_LATTICE", "1") == "1"
+USE_LATTICE = os.environ.get("DDILU_LATTICE", "0") == "1"   # measured 2-4x slower than the rotating kernel
 
 
 def build_lattice(t: DeviceCsr, part: TilePartition, upper: bool, unit_diag: bool, sched=None) -> "LatticeSched | None":
@@ -617,6 +617,167 @@ def sptrsv_block_window(t: DeviceCsr, sched: Schedule, bw: BlockWindow, b: torch
     sell = get_sell(t, sched, upper, unit_diag)
     call("ddilu_sptrsv_blockwin_sell", bl.n_blocks, sched.n_levels, bl.sstart, bl.cnt, bw.lbase, sched.order,
          sell.goff, sell.width, bw.scol_loc, sell.sval, sell.sdiag, bw.sdinv, bw.wmask, b, out)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# block sweep (csrc/sweep.cu): interface factors, one CTA per subdomain block
+
+USE_SWEEP = os.environ.get("DDILU_SWEEP", "1") == "1"
+SWEEP_MAX_AVG_WIDTH = 512      # average rows per level of a block up to which one CTA per block is the right shape
+SWEEP_SMEM_BUDGET = 200 * 1024
+SWEEP_MAX_LEVELS = 6144        # level table of a block in shared memory (L + U)
+SWEEP_MAX_THREADS = 416        # compute threads per set (wider levels loop)
+SWEEP_ROWS_PER_THREAD = 1      # rows of a level per thread (1, 2, 4); measured at 256^3 / 128^3: 1 row, 3 sets is the fastest shape
+SWEEP_SETS = 3                 # compute sets taking the levels in turn (2, 3)
+
+
+@dataclass
+class SweepPlan:
+    """Layout of `ddilu_sweep_solve` for a block-diagonal factor pair: rows of a block in schedule order
+    (level-major), operands in 256-row pages, positions padded to whole pages per block."""
+
+    n: int
+    n_blocks: int
+    k: int                     # operand slots per row
+    window: int                # shared-memory window (doubles, power of two)
+    stages: int                # ring depth (power of two)
+    sets: int                  # compute sets taking the levels in turn
+    nct: int                   # compute threads per set
+    rpt: int                   # rows of a level per thread
+    max_lev: int
+    npad: int                  # padded position space (n_pages * 256)
+    blocks: torch.Tensor       # int32[n_blocks * 8]
+    levtab: torch.Tensor
+    pages_l: torch.Tensor
+    pages_u: torch.Tensor
+    rowof_l: torch.Tensor      # int32[npad]: row at a position of the L schedule, -1 = padding
+    rowof_u: torch.Tensor
+    rhs: torch.Tensor          # f64[npad] right-hand side in schedule order
+    tmp: torch.Tensor          # f64[npad] U-phase right-hand side written by the L phase
+    addbuf: torch.Tensor       # f64[npad] vector added to the results, in U schedule order
+    bad_row: int
+    n_levels: tuple = (0, 0)
+
+
+def build_sweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l: int, lev_u: torch.Tensor,
+                nlev_u: int, seg_ptr) -> "SweepPlan | None":
+    """Plan of the block sweep for the factor pair (L strictly lower, U with its diagonal) whose independent
+    diagonal blocks are the row ranges seg_ptr (host ints); None when the pair does not qualify (a dependency
+    leaves its block, rows with more than 8 dependencies, levels too wide or too many, window too large)."""
+    n = lower.n_rows
+    nb = len(seg_ptr) - 1
+    if not USE_SWEEP or n == 0 or nb < 1 or nlev_l == 0 or nlev_u == 0:
+        return None
+    P = query("ddilu_sweep_page_rows")
+    d = dev()
+    i64 = torch.int64
+    seg = torch.tensor([int(v) for v in seg_ptr], dtype=i64, device=d)
+    if int(seg[-1].item()) != n or int(seg[0].item()) != 0:
+        return None
+    rows = torch.arange(n, dtype=i64, device=d)
+    blk = torch.bucketize(rows, seg[1:], right=True)
+    sizes = seg[1:] - seg[:-1]
+    n_pages_b = (sizes + P - 1) // P
+    page0 = torch.cumsum(n_pages_b, 0) - n_pages_b
+    n_pages = int(n_pages_b.sum().item())
+    npad = n_pages * P
+    # dependency counts -> operand slots per row
+    kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
+    ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
+    kmax = max(kl, ku, 1)
+    k = next((c for c in (2, 3, 4, 8) if kmax <= c), None)
+    if k is None:
+        return None
+    plans = []
+    for fac, lev, nlev, up in ((lower, lev_l, nlev_l, False), (upper, lev_u, nlev_u, True)):
+        key = blk * nlev + lev[:n].to(i64)
+        order = torch.argsort(key, stable=True)
+        cnt = torch.bincount(key, minlength=nb * nlev).view(nb, nlev)
+        lpos = torch.empty(n, dtype=i64, device=d)
+        lpos[order] = rows - seg[blk[order]]
+        gpos = page0[blk] * P + lpos
+        lev_end = torch.cumsum(cnt, 1)
+        # dependencies: same block, and not further back than the window behind the end of the reader's level
+        nnz = fac.nnz
+        rlen = (fac.rp[1:] - fac.rp[:-1]).to(i64)
+        erow = torch.repeat_interleave(rows, rlen)
+        ecol = fac.ci[:nnz].to(i64)
+        dep = ecol != erow
+        if bool((blk[ecol] != blk[erow]).any().item()):
+            return None
+        row_end = lev_end.reshape(-1)[key]
+        need = torch.where(dep, row_end[erow] - lpos[ecol], torch.zeros_like(ecol))
+        max_need = int(need.max().item()) if nnz else 1
+        nz = cnt > 0
+        plans.append((fac, up, lpos, gpos, lev_end[nz], nz.sum(1), int(cnt.max().item()), max_need))
+    window = 32
+    while window < max(p[7] for p in plans):
+        window <<= 1
+    width_max = max(p[6] for p in plans)
+    nlev_b = plans[0][5] + plans[1][5]
+    max_lev = int(nlev_b.max().item())
+    avg_width = float(n) / max(1, int(plans[0][5].sum().item()))
+    if window > 16384 or max_lev > SWEEP_MAX_LEVELS or avg_width > SWEEP_MAX_AVG_WIDTH:
+        return None
+    rpt, sets = SWEEP_ROWS_PER_THREAD, SWEEP_SETS
+    helpers = query("ddilu_sweep_helper_threads")
+    nct = min(SWEEP_MAX_THREADS, ((1024 - helpers) // sets) & ~31, max(32, ((width_max + rpt - 1) // rpt + 31) & ~31))
+    stages = 0
+    for st in (16, 8, 4):
+        if query("ddilu_sweep_smem_bytes", k, st, window, max_lev) <= SWEEP_SMEM_BUDGET:
+            stages = st
+            break
+    if stages < 4 or width_max > (stages - 2) * P:
+        return None
+    # level tables: per block its L levels then its U levels
+    lev_off = torch.cumsum(nlev_b, 0) - nlev_b
+    lt_l, lt_u = plans[0][4], plans[1][4]
+    nl, nu = plans[0][5], plans[1][5]
+    levtab = torch.empty(int(nlev_b.sum().item()), dtype=i64, device=d)
+    off_l = torch.repeat_interleave(lev_off, nl) + (torch.arange(lt_l.numel(), device=d) -
+                                                    torch.repeat_interleave(torch.cumsum(nl, 0) - nl, nl))
+    off_u = torch.repeat_interleave(lev_off + nl, nu) + (torch.arange(lt_u.numel(), device=d) -
+                                                         torch.repeat_interleave(torch.cumsum(nu, 0) - nu, nu))
+    levtab[off_l] = lt_l
+    levtab[off_u] = lt_u
+    blocks = torch.zeros((nb, 8), dtype=i64, device=d)
+    blocks[:, 0], blocks[:, 1], blocks[:, 2], blocks[:, 3], blocks[:, 4] = sizes, page0, nl, nu, lev_off
+    bad = torch.full((1,), INT_MAX, dtype=I32, device=d)
+    gpos_u32 = plans[1][3].to(I32).contiguous()
+    pages, rowof = [], []
+    for fac, up, lpos, gpos, _, _, _, _ in plans:
+        pg = torch.zeros(n_pages * query("ddilu_sweep_page_bytes", k, int(up)), dtype=torch.uint8, device=d)
+        call("ddilu_sweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos.to(I32).contiguous(),
+             lpos.to(I32).contiguous(), None if up else gpos_u32, window, pg, bad)
+        ro = torch.full((npad,), -1, dtype=I32, device=d)
+        ro[gpos] = rows.to(I32)
+        pages.append(pg)
+        rowof.append(ro)
+    return SweepPlan(n, nb, k, window, stages, sets, nct, rpt, max_lev, npad, blocks.to(I32).contiguous().view(-1),
+                     levtab.to(I32).contiguous(), pages[0], pages[1], rowof[0], rowof[1], zeros_f64(npad),
+                     zeros_f64(npad), zeros_f64(npad), int(bad.item()), (int(nl.max().item()), int(nu.max().item())))
+
+
+def sweep_rhs(sp: SweepPlan, upper: bool, b: torch.Tensor | None, mat: "DeviceCsr | None" = None,
+              y: torch.Tensor | None = None, mode: int = 0, add: torch.Tensor | None = None):
+    """sp.rhs <- right-hand side in the schedule order of L (or U): b gathered, or (mode 0) mat y,
+    (mode 1) b - mat y, (mode 2) b + mat y; with `add` also sp.addbuf <- add in U schedule order."""
+    ro = sp.rowof_u if upper else sp.rowof_l
+    extra = (sp.rowof_u, add, sp.addbuf) if add is not None else (None, None, None)
+    if mat is None:
+        call("ddilu_sweep_rhs", sp.npad, ro, None, None, None, None, b, 0, sp.rhs, *extra)
+    else:
+        call("ddilu_sweep_rhs", sp.npad, ro, mat.rp, mat.ci, mat.val, y, b, mode, sp.rhs, *extra)
+
+
+def sweep_solve(sp: SweepPlan, phases: int, out: torch.Tensor, add: bool = False, check: bool = False):
+    """out[row] = x (+ add[row], staged by sweep_rhs) with x = L^-1 rhs (phases 1), U^-1 rhs (2) or
+    U^-1 L^-1 rhs (3), rhs = sp.rhs."""
+    if check and (phases & 2) and sp.bad_row != INT_MAX:
+        raise TriSolveError(f"zero or missing diagonal at row {sp.bad_row}")
+    call("ddilu_sweep_solve", sp.n_blocks, sp.blocks, sp.levtab, sp.pages_l, sp.pages_u, sp.k, sp.window, sp.stages,
+         sp.sets, sp.nct, sp.rpt, sp.max_lev, phases, sp.rhs, sp.tmp, out, sp.addbuf if add else None)
     return out
 
 

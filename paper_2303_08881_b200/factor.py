@@ -85,6 +85,7 @@ class DevFactors:
             self._levs[False] = (sched_l.lev, sched_l.n_levels)
         self._tl = self._tu = None  # tiled layouts (D.TileSched) when the factor tiles
         self._bw = None             # (L, U) shared-memory-window plans of the block-local sweep
+        self._sw = None             # D.SweepPlan: one CTA per diagonal block (interface factors)
         self._tmp = None
 
     @property
@@ -113,6 +114,12 @@ class DevFactors:
         rows (structured problems) -> tiled solve, with the sync-free SELL solve as the
         fallback when the tile graph is not one-way.  seg_ptr: row ranges of independent
         diagonal blocks (one per subdomain), if known."""
+        if seg_ptr is not None and D.USE_SWEEP and self.n:
+            # small, deep, block-diagonal (the interface factors): one CTA per block walks the levels in shared
+            # memory, L and U in one launch (csrc/sweep.cu); the other layouts are then built only on demand
+            self._sw = D.build_sweep(self.lower, self.upper, *self._lev(False), *self._lev(True), seg_ptr)
+            if self._sw is not None:
+                return self
         if part is not None and D.USE_TILED and self.n:
             # part: one TilePartition for both factors, or a callable (lev, n_levels) -> TilePartition for
             # partitions that depend on the factor's own levels (wavefront-slab tiles)
@@ -154,6 +161,9 @@ class DevFactors:
         return self
 
     def lower_solve(self, b, out):
+        if self._sw is not None:
+            D.sweep_rhs(self._sw, False, b)
+            return D.sweep_solve(self._sw, 1, out)
         if self._bw is not None:
             return D.sptrsv_block_window(self.lower, self.sched_l, self._bw[0], b, out, False, True)
         if self._tl is not None:
@@ -161,6 +171,9 @@ class DevFactors:
         return D.sptrsv(self.lower, self.sched_l, b, out, False, True)
 
     def upper_solve(self, b, out):
+        if self._sw is not None:
+            D.sweep_rhs(self._sw, True, b)
+            return D.sweep_solve(self._sw, 2, out)
         if self._bw is not None:
             return D.sptrsv_block_window(self.upper, self.sched_u, self._bw[1], b, out, True, False)
         if self._tu is not None:
@@ -169,10 +182,24 @@ class DevFactors:
 
     def solve(self, b, out):
         """out = U^-1 L^-1 b (factor.py:124-126)."""
+        if self._sw is not None:
+            D.sweep_rhs(self._sw, False, b)
+            return D.sweep_solve(self._sw, 3, out)
         if self._tmp is None:
             self._tmp = D.empty_f64(max(self.n, 1))
         self.lower_solve(b, self._tmp)
         return self.upper_solve(self._tmp, out)
+
+
+def solve_with_product(f: DevFactors, mat: D.DeviceCsr, y, base, mode: int, out, add=None):
+    """out = (add +) U^-1 L^-1 (mat y | base - mat y | base + mat y) for mode 0 | 1 | 2: the product feeds the
+    sweep's right-hand side directly and the sum is folded into its result stores (precond.py:242-249:
+    `S^-1 (r_ext - W fp)`, `y + S^-1 (E_off y)`).  Needs the factor pair's sweep plan (callers keep the
+    separate-kernel sequence for factors without one)."""
+    if f._sw is None:
+        raise RuntimeError("solve_with_product needs a sweep plan (DevFactors.prepare(seg_ptr=...))")
+    D.sweep_rhs(f._sw, False, base, mat, y, mode, add=add)
+    return D.sweep_solve(f._sw, 3, out, add=add is not None)
 
 
 def d_level0_split(a: D.DeviceCsr, n_elim: int):

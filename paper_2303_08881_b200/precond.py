@@ -25,7 +25,7 @@ import torch
 from . import device as D
 from .dist import Comm, domains_of_rank, get_comm
 from .factor import (DevFactors, DevPartial, FillRule, IluFactors, MiluVectors, PartialIluFactors, TwoLevelBlocks,
-                     d_carve, d_factor_level0, d_factorize, d_partial_ilu)
+                     d_carve, d_factor_level0, d_factorize, d_partial_ilu, solve_with_product)
 from .krylov import InnerGmres, KrylovConfig, restarted_device
 from .ordering import DomainLayout
 from .sparse import CsrMatrix, Permutation
@@ -474,6 +474,10 @@ class SchurIluPrecond(_DDPrecond):
             self._ybuf[: s.n_ext].copy_(y[: s.n_ext])
             y = self._ybuf
         s.exchange_halo(y[: s.n_ext], y[s.n_ext:])
+        if self._p.schur._sw is not None:
+            # E_off y feeds the sweep's right-hand side, `y +` rides on its result stores: two launches
+            solve_with_product(self._p.schur, self._coupling, y, None, 0, out, add=y)
+            return
         D.spmv(self._coupling, y, self._c)
         self._schur_solve(self._c, self._sv)
         D.ewise(s.n_ext, y, self._sv, 0, out)
@@ -500,8 +504,11 @@ class SchurIluPrecond(_DDPrecond):
         s, p = self.system, self._p
         ni, ne = s.n_int, s.n_ext
         p.interior.lower_solve(r[:ni], self._fp)                      # fp = L_B^-1 r_int
-        D.spmv(p.w, self._fp, self._g, b=r[ni:], mode=1)              # ghat = r_ext - W fp
-        self._schur_solve(self._g, self._rhs)                         # S~^-1 ghat
+        if p.schur._sw is not None:
+            solve_with_product(p.schur, p.w, self._fp, r[ni:], 1, self._rhs)   # S~^-1 (r_ext - W fp)
+        else:
+            D.spmv(p.w, self._fp, self._g, b=r[ni:], mode=1)          # ghat = r_ext - W fp
+            self._schur_solve(self._g, self._rhs)                     # S~^-1 ghat
         self._inner.solve(self._reduced_matvec, self._rhs, self._y, n_global=s.n_ext_global)
         if self._zc is not None:
             D.sub_compact(self._zc, self._y, self._fp)                # fp - Z y on the rows that have entries, in place

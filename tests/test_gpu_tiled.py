@@ -37,11 +37,12 @@ def tile_kernel(request):
     """Run with the production kernels (lattice solve where the tiles qualify, CTA-per-tile kernel elsewhere),
     with the CTA-per-tile kernel alone and with the warp-per-tile alternatives."""
     from paper_2303_08881_b200 import device as D
-    old, old_lat = D.TILE_KERNEL, D.USE_LATTICE
+    old, old_lat, old_sw = D.TILE_KERNEL, D.USE_LATTICE, D.USE_SWEEP
     D.TILE_KERNEL = "rot" if request.param == "lattice" else request.param
     D.USE_LATTICE = request.param == "lattice"
+    D.USE_SWEEP = False        # the interface factors go through the tiled kernels here (tests/test_gpu_sweep.py covers the sweep)
     yield request.param
-    D.TILE_KERNEL, D.USE_LATTICE = old, old_lat
+    D.TILE_KERNEL, D.USE_LATTICE, D.USE_SWEEP = old, old_lat, old_sw
 
 
 @pytest.mark.parametrize("dims,p", [((20, 20, 20), 8), ((24, 17, 9), 4), ((40, 40), 4), ((33, 33, 33), 1)])
@@ -240,14 +241,15 @@ def test_lattice_solves_bit_exact(P, orc, dims, p, tile):
     import torch
     from paper_2303_08881_b200 import device as D
     from paper_2303_08881_b200.precond import LocalSystem
-    old = LocalSystem.TILE_DIMS_3D
+    old, old_lat = LocalSystem.TILE_DIMS_3D, D.USE_LATTICE
     LocalSystem.TILE_DIMS_3D = tile
+    D.USE_LATTICE = True       # off by default: measured slower than the rotating-warp kernel
     try:
         a = P.aniso3d(*dims)
         layout = P.classify_and_order(a, P.partition(a, p, dims), p)
         m = P.make_preconditioner("schur", a, layout)
     finally:
-        LocalSystem.TILE_DIMS_3D = old
+        LocalSystem.TILE_DIMS_3D, D.USE_LATTICE = old, old_lat
     f = m._p.interior
     assert f._tl.kind == "lattice" and f._tu.kind == "lattice"
     rng = np.random.default_rng(11)

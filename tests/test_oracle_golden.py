@@ -269,3 +269,31 @@ def test_iteration_counts_baseline_shapes():
         out, rep, _ = orc.run(a, dims, rec["p"], rec["precond"], orc.Rule.parse(rec["fill"]))
         assert rep.iterations == rec["its"], rec
         assert rep.final_relres == rec["final_relres"], rec
+
+
+def test_oracle_library_exports_what_the_wrapper_calls():
+    """Every orc_* entry the Python half calls exists in the C half (a stale or partial build must not reach
+    bench.py's reference arm)."""
+    import re
+    from oracle import ddilu_oracle as orc
+    lib = orc.lib()
+    src = open(orc.__file__).read()
+    for name in sorted(set(re.findall(r"orc_[a-z0-9_]+", src))):
+        assert hasattr(lib, name), name
+
+
+def test_threaded_reference_arm_keeps_the_serial_results():
+    """bench.py --impl reference may use host threads: SpMV rows and axpy keep every bit, the chunked dot
+    agrees to rounding, and threads = 1 is the pinned serial oracle again afterwards."""
+    from oracle import ddilu_oracle as orc
+    a = orc.aniso((48, 48, 48), (1.0, 1.0, 0.01))
+    rng = np.random.default_rng(5)
+    x, y = rng.standard_normal(a.n_rows), rng.standard_normal(a.n_rows)
+    ref_mv, ref_dot = orc.spmv(a, x), orc.vdot(x, y)
+    try:
+        assert orc.set_threads(4) == 4
+        assert np.array_equal(orc.spmv(a, x), ref_mv)
+        assert abs(orc.vdot(x, y) - ref_dot) <= 1e-12 * np.sqrt(a.n_rows)
+    finally:
+        orc.set_threads(1)
+    assert orc.vdot(x, y) == ref_dot
