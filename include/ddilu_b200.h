@@ -23,10 +23,6 @@
 extern "C" {
 #endif
 
-/* ---- tuning knobs (no reference equivalent): "trsv_blocks_per_sm", "trsv_depth",
- * "trsv_stage_mask", "trsv_far_sleep_ns", "trsv_pipe", "trsv_pipe_warps_per_sm", "trsv_sleep_ns" */
-int ddilu_set_tuning(const char *key, int value);
-
 /* ---- primitives used by the count -> scan -> fill setup passes (the reference
  * uses np.cumsum: e.g. sparse.py:449, factor.py:254-257) */
 long long ddilu_scan_tmp_elems(long long n);
@@ -86,35 +82,6 @@ int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const 
                       const int *scol, const double *sval, const double *sdiag, const int *gwait, const int *gfar1,
                       const int *gfar2, double avg_width, const double *b, double *x, void *stream);
 
-/* Block-local variant for small, deep, block-diagonal factors (interface factors L_S/U_S:
- * precond.py:239-245 `_schur_solve`, :361-366 `_coarse_precond`): one CTA per independent row
- * block seg_ptr[d]..seg_ptr[d+1], levels separated by a CTA barrier.  start/cnt[d*n_levels+l]
- * = first position / number of rows of block d in level l inside level_rows. */
-int ddilu_blocklocal_table(int n, int n_blocks, const int *seg_ptr, int n_levels, const int *lev,
-                           const int *level_rows, int *start, int *cnt, void *stream);
-int ddilu_sptrsv_blocklocal(int n_blocks, int n_levels, const int *start, const int *cnt, const int *level_rows,
-                            const int *row_ptr, const int *col_idx, const double *values, const double *b, double *x,
-                            int upper, int unit_diag, int *err, void *stream);
-
-/* same sweep on the SELL arrays; sstart[d*n_levels+l] = first SCHEDULE SLOT of block d in level l */
-/* the same sweep with the block's part of x in a shared-memory window: scol_loc = block-local schedule position
- * of every dependency (-1 padding), lbase = first position of (block, level), wmask + 1 = window size (a power
- * of two, checked at setup against the furthest dependency), sdinv = RN(1/pivot) or 0 (see ddilu_fastdiv_selftest) */
-int ddilu_sptrsv_blockwin_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *lbase,
-                               const int *order, const int *goff, int uniform_width, const int *scol_loc,
-                               const double *sval,
-                               const double *sdiag, const double *sdinv, int wmask, const double *b, double *x,
-                               void *stream);
-int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const int *sstart, const int *cnt, const int *order,
-                                 const int *goff, int uniform_width, const int *scol, const double *sval,
-                                 const double *sdiag, const double *b, double *x, void *stream);
-
-/* diagnostics: same solve with per-group timestamps (8 int64 per group: start, spin done, deps
- * loaded, stored [globaltimer ns], SM id, spin count, re-poll rounds, warp id) */
-int ddilu_sptrsv_sell_trace(int n, int n_slots, int blocks_per_sm, const int *order, const int *goff,
-                            int uniform_width, const int *scol, const double *sval, const double *sdiag,
-                            const int *gwait, const double *b, double *x, long long *stamps, void *stream);
-
 /* ---- factor.py:270-369 `_iluk_symbolic`: level-of-fill pattern (levels <= klevel), rows >= n_elim keep
  * their trailing block un-eliminated.  Row slabs of row_cap entries: p_* = pivot (L) part, k_* = kept
  * (U / Schur) part with fill levels; *status != 0: a row outgrew row_cap (retry with a larger one).
@@ -141,16 +108,8 @@ int ddilu_prefill(int n, const int *a_rp, const int *a_ci, const double *a_v, co
  *                   stats[0..2] = max rows, max externals, max bytes, stats[4] = longest row (kmax); fill = 1: blk16 holds the
  *                   scanned offsets, blocks are written to blob, stats[3] = first bad pivot row
  *   sptrsv_tiled  : x = T^-1 b; one cooperative launch */
-int ddilu_tiled_set_tuning(const char *key, int value);
-/* diagnostics: 8 int64 per CTA (life, wait static/rhs, wait boundary, tile time [cycles], levels, tiles); NULL = off */
-int ddilu_tiled_set_debug(long long *device_buf);
 int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *owner,
                         int *keys, long long *n_keys_h, void *stream);
-/* "wavefront slab" tiles: key = (owner, box of the first two grid coordinates, lev[i] / delta) with lev =
- * the factor's level of row i; *n_keys_h = size of the key range */
-int ddilu_tile_slab_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h, const int *lev,
-                         int n_levels, int delta, const int *owner, int n_owners, int *keys, long long *n_keys_h,
-                         void *stream);
 int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream);
 int ddilu_tile_assign(int n, const int *sorted_keys, const int *head_scan, const int *sorted_rows, int *tile_of,
                       int *tpos, int *tile_ptr, void *stream);
@@ -165,16 +124,6 @@ int ddilu_tile_build(int fill, int n_tiles, const int *tsched, const int *tile_p
                      const double *values, const int *glev, int upper, int has_diag, int item_warps, int *blk16,
                      int *stats, unsigned char *blob, void *stream);
 long long ddilu_tiled_smem_bytes(int stat_max, int tmax, int emax);
-/* warp-per-tile variant of the same solve (static blocks built with item_warps = 1): every warp owns a
- * stream of tiles, no named barriers, no helper warps; as many independent warps per SM as shared
- * memory allows */
-long long ddilu_warptile_smem_per_warp(int stat_max, int tmax, int emax);
-/* lean variant for rows with <= 3 dependencies (static blocks built with item_warps = 0: pre-digested
- * 16-byte row records, ~40 instructions per level) */
-int ddilu_sptrsv_lean(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
-                      int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
-int ddilu_sptrsv_warptile(int n, int n_tiles, const int *blk_off16, const unsigned char *blob, int stat_max, int tmax,
-                          int emax, int kmax, int has_diag, const double *b, double *x, void *stream);
 /* self-check of the division the U solves use (pivot reciprocal + two FMA corrections) against the
  * IEEE division on n pseudo-random / adversarial operand pairs; *mismatch = pairs whose bits differ */
 int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigned long long *mismatch, void *stream);
@@ -199,8 +148,6 @@ int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned 
  * precond.py:249). */
 int ddilu_sweep_page_rows(void);
 int ddilu_sweep_helper_threads(void);   /* threads of a CTA that do not compute (TMA issuer, gate, writers) */
-int ddilu_sweep_set_tuning(int writer_sleep_ns, int flags);   /* diagnostics */
-int ddilu_sweep_set_debug(long long *buf);   /* diagnostics: 64 int64 cycle counters per block, NULL = off */
 long long ddilu_sweep_page_bytes(int k, int upper);
 long long ddilu_sweep_smem_bytes(int k, int stages, int window, int max_lev);
 int ddilu_sweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
@@ -213,26 +160,6 @@ int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const 
                       const unsigned char *pages_u, int k, int window, int stages, int sets, int nct,
                       int rows_per_thread, int max_lev, int phases, const double *rhs, double *tmp, double *out,
                       const double *add, void *stream);
-
-/* ---- lattice triangular solve (csrc/lattice.cu): the fast path of sparse.py:228-272 for factors whose box
- * tiles are lattices with one-way axes and <= 3 dependencies per row (7-point ILU(0) factors).  One warp per
- * tile, results of a step handed to the next through the warp's shared-memory line buffer, row records streamed
- * through a per-warp cp.async ring, per-tile completion flags instead of a sentinel preset of x.
- * ddilu_lattice_build: fill = 0 checks the lattice property and sizes the blocks (blk16[q] in 16-byte units,
- * stats = {failed, max boundary values, max steps, first bad pivot row, max producer tiles, max block bytes,
- * max rows}); fill = 1 writes
- * the per-tile table `tab` (32 int4 per tile) and the blocks at blob + 16 * blk16[q] (scanned offsets).
- * nodes[row] = grid node of a row, dims3 / tdims3 = grid and tile dimensions (x fastest, padded with 1). */
-int ddilu_lattice_build(int fill, int n_tiles, const int *tsched, const int *tile_pos, const int *tile_ptr,
-                        const int *trows, const int *tile_of, const int *row_ptr, const int *col_idx,
-                        const double *values, const int *nodes, const int *dims3, const int *tdims3, int upper,
-                        int has_diag, void *tab, int *blk16, int *stats, unsigned char *blob, void *stream);
-int ddilu_lattice_max_ext(void);
-int ddilu_lattice_set_tuning(const char *key, int value);
-long long ddilu_lattice_smem_bytes(int blkmax, int tmax, int xemax);
-int ddilu_lattice_set_debug(long long *buf);
-int ddilu_sptrsv_lattice(int n_tiles, const void *tab, const unsigned char *blob, int *flags, int n_slots,
-                         int has_diag, int blkmax, int tmax, int xemax, const double *b, double *x, void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,
@@ -335,6 +262,16 @@ int ddilu_sort_rows_i32(int n, const int *rp, int *ci, void *stream);
 /* ---- ordering.py:97-127 `_grow_regions` (serial greedy BFS growth; work = 2n ints) */
 int ddilu_grow_regions(int n, const int *adj_rp, const int *adj_ci, int n_dom, const int *sizes, int *owner,
                        int *work, void *stream);
+/* ---- sparse.py:333-370, 487-505 `sparse_matmul`: C = A B with the exact structural pattern (cancelled entries
+ * kept), values bit-identical to the reference's marker/accumulator loop.  bound[i] = products of row i (scan it
+ * into off[n_rows + 1]); expand writes the products of a row, stably sorted by column, into s_col / s_val at
+ * off[i] and the number of distinct columns into counts[i] (scan it into out_rp); compact sums the runs. */
+int ddilu_spgemm_bound(int n_rows, const int *a_rp, const int *a_ci, const int *b_rp, int *bound, void *stream);
+int ddilu_spgemm_expand(int n_rows, const int *a_rp, const int *a_ci, const double *a_v, const int *b_rp,
+                        const int *b_ci, const double *b_v, const int *off, int *s_col, double *s_val, int *counts,
+                        void *stream);
+int ddilu_spgemm_compact(int n_rows, const int *off, const int *s_col, const double *s_val, const int *out_rp,
+                         int *out_ci, double *out_v, void *stream);
 /* ---- precond.py:84-125 `_l1_row_shifts`, `_add_to_diagonal` (l1 block Jacobi) */
 int ddilu_l1_row_shifts(int n_sel, const int *rows, const int *rp, const int *ci, const double *v, const int *owner,
                         double *out, void *stream);
@@ -363,5 +300,12 @@ int ddilu_widen_i32(long long n, const int *in, long long *out, void *stream);
 
 #ifdef __cplusplus
 }
+#endif
+
+/* Measured-slower alternative kernels, tuning knobs and diagnostics are NOT part of the product ABI: they are
+ * compiled only with -DDDILU_EXPERIMENTS (DDILU_EXPERIMENTS=1 python -m paper_2303_08881_b200.build) and declared
+ * in ddilu_b200_experiments.h. */
+#ifdef DDILU_EXPERIMENTS
+#include "ddilu_b200_experiments.h"
 #endif
 #endif /* DDILU_B200_H */

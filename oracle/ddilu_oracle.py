@@ -216,6 +216,36 @@ def csr_transpose(a: Csr):
     return Csr(a.n_cols, a.n_rows, rp, ci, v)
 
 
+def sparse_matmul(a: Csr, b: Csr):
+    """sparse.py:333-370, 487-505 (`_spgemm_count`, `_spgemm_fill`): marker / accumulator loops, the first
+    product of a column assigned, later ones added in traversal order, rows emitted in ascending column order
+    with cancelled entries kept.  Pure-Python loops: small matrices only."""
+    if a.n_cols != b.n_rows:
+        raise ValueError("inner dimensions do not match")
+    rp = np.zeros(a.n_rows + 1, dtype=np.int64)
+    cols_out, vals_out = [], []
+    marker_arr = np.full(b.n_cols, -1, dtype=np.int64)
+    acc = np.zeros(b.n_cols)
+    for i in range(a.n_rows):
+        row_cols = []
+        for ka in range(a.row_ptr[i], a.row_ptr[i + 1]):
+            k = a.col_idx[ka]
+            av = a.values[ka]
+            for kb in range(b.row_ptr[k], b.row_ptr[k + 1]):
+                j = b.col_idx[kb]
+                if marker_arr[j] != i:
+                    marker_arr[j] = i
+                    acc[j] = av * b.values[kb]
+                    row_cols.append(j)
+                else:
+                    acc[j] += av * b.values[kb]
+        row_cols.sort()
+        cols_out += row_cols
+        vals_out += [acc[j] for j in row_cols]
+        rp[i + 1] = len(cols_out)
+    return Csr(a.n_rows, b.n_cols, rp, np.array(cols_out, dtype=np.int64), np.array(vals_out, dtype=np.float64))
+
+
 def permute_symmetric(a: Csr, fwd):
     """sparse.py:431-442."""
     fwd = _i64(fwd)

@@ -22,7 +22,6 @@ _S = ctypes.c_char_p
 
 # name -> (restype, argtypes); must stay in sync with include/ddilu_b200.h
 SIGNATURES = {
-    "ddilu_set_tuning": (_I, [_S, _I]),
     "ddilu_scan_tmp_elems": (_L, [_L]),
     "ddilu_exclusive_scan_i32": (_I, [_P, _P, _L, _P, _P]),
     "ddilu_sort_tmp_elems": (_L, [_L]),
@@ -36,19 +35,11 @@ SIGNATURES = {
     "ddilu_sell_fill": (_I, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
     "ddilu_compose_wait": (_I, [_I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),
-    "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
-    "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
-    "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
-    "ddilu_sptrsv_blockwin_sell": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P]),
-    "ddilu_sptrsv_sell_trace": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_iluk_smem_bytes": (_L, [_I]),
     "ddilu_iluk_symbolic": (_I, [_I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_compact_cols": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "ddilu_prefill": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
-    "ddilu_tiled_set_tuning": (_I, [_S, _I]),
-    "ddilu_tiled_set_debug": (_I, [_P]),
     "ddilu_tile_box_keys": (_I, [_I, _P, _I, _P, _P, _P, _P, _P, _P]),
-    "ddilu_tile_slab_keys": (_I, [_I, _P, _I, _P, _P, _P, _I, _I, _P, _I, _P, _P, _P]),
     "ddilu_tile_heads": (_I, [_I, _P, _P, _P]),
     "ddilu_tile_assign": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_tile_edges_count": (_I, [_I, _P, _P, _I, _P, _P, _P]),
@@ -56,26 +47,15 @@ SIGNATURES = {
     "ddilu_tile_relax": (_I, [_L, _P, _I, _P, _P, _I, _P]),
     "ddilu_tile_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P]),
     "ddilu_tiled_smem_bytes": (_L, [_I, _I, _I]),
-    "ddilu_warptile_smem_per_warp": (_L, [_I, _I, _I]),
-    "ddilu_sptrsv_lean": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
-    "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_fastdiv_selftest": (_I, [_L, ctypes.c_ulonglong, _P, _P]),
     "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_sweep_page_rows": (_I, []),
     "ddilu_sweep_helper_threads": (_I, []),
-    "ddilu_sweep_set_debug": (_I, [_P]),
-    "ddilu_sweep_set_tuning": (_I, [_I, _I]),
     "ddilu_sweep_page_bytes": (_L, [_I, _I]),
     "ddilu_sweep_smem_bytes": (_L, [_I, _I, _I, _I]),
     "ddilu_sweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "ddilu_sweep_rhs": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sweep_solve": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
-    "ddilu_lattice_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
-    "ddilu_lattice_max_ext": (_I, []),
-    "ddilu_lattice_set_tuning": (_I, [_S, _I]),
-    "ddilu_lattice_smem_bytes": (_L, [_I, _I, _I]),
-    "ddilu_lattice_set_debug": (_I, [_P]),
-    "ddilu_sptrsv_lattice": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),
@@ -112,6 +92,9 @@ SIGNATURES = {
     "ddilu_sym_adj_fill": (_I, [_I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sort_rows_i32": (_I, [_I, _P, _P, _P]),
     "ddilu_grow_regions": (_I, [_I, _P, _P, _I, _P, _P, _P, _P]),
+    "ddilu_spgemm_bound": (_I, [_I, _P, _P, _P, _P, _P]),
+    "ddilu_spgemm_expand": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_spgemm_compact": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_l1_row_shifts": (_I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_add_to_diagonal": (_I, [_I, _P, _P, _P, _P, _P, _P]),
     "ddilu_drop_small_count": (_I, [_I, _P, _P, _P, _D, _P, _P]),
@@ -125,7 +108,33 @@ SIGNATURES = {
     "ddilu_widen_i32": (_I, [_L, _P, _P, _P]),
 }
 
+# entries that exist only in a -DDDILU_EXPERIMENTS build (include/ddilu_b200_experiments.h): measured-slower
+# alternative kernels, tuning knobs, diagnostics.  Bound when the library has them.
+EXPERIMENT_SIGNATURES = {
+    "ddilu_set_tuning": (_I, [_S, _I]),
+    "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "ddilu_sptrsv_blocklocal_sell": (_I, [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_sptrsv_blockwin_sell": (_I, [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P]),
+    "ddilu_sptrsv_sell_trace": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_tiled_set_tuning": (_I, [_S, _I]),
+    "ddilu_tiled_set_debug": (_I, [_P]),
+    "ddilu_tile_slab_keys": (_I, [_I, _P, _I, _P, _P, _P, _I, _I, _P, _I, _P, _P, _P]),
+    "ddilu_warptile_smem_per_warp": (_L, [_I, _I, _I]),
+    "ddilu_sptrsv_lean": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_sweep_set_debug": (_I, [_P]),
+    "ddilu_sweep_set_tuning": (_I, [_I, _I]),
+    "ddilu_lattice_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
+    "ddilu_lattice_max_ext": (_I, []),
+    "ddilu_lattice_set_tuning": (_I, [_S, _I]),
+    "ddilu_lattice_smem_bytes": (_L, [_I, _I, _I]),
+    "ddilu_lattice_set_debug": (_I, [_P]),
+    "ddilu_sptrsv_lattice": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+}
+
 _lib = None
+_experiments = False
 launches = 0  # kernels-launching C-ABI calls made so far (bench.py reports the delta)
 
 # Optional per-entry timing with CUDA events on the launching stream (bench.py):
@@ -151,8 +160,29 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        global _experiments
+        _experiments = hasattr(lib, next(iter(EXPERIMENT_SIGNATURES)))
+        if _experiments:
+            for name, (res, args) in EXPERIMENT_SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
         _lib = lib
     return _lib
+
+
+def has_experiments() -> bool:
+    """Whether the loaded library was built with -DDDILU_EXPERIMENTS (alternative kernels, knobs, diagnostics)."""
+    load()
+    return _experiments
+
+
+def _entry(name: str):
+    lib = load()
+    if name in EXPERIMENT_SIGNATURES and not _experiments:
+        raise DdiluError(f"{name} is an experiments-only entry: rebuild with DDILU_EXPERIMENTS=1 "
+                         "python -m paper_2303_08881_b200.build")
+    return getattr(lib, name)
 
 
 def require_cuda() -> None:
@@ -176,7 +206,7 @@ def call(name: str, *args):
     """Call a status-returning entry point with torch tensors / scalars; the
     current torch stream is appended as the last argument."""
     global launches
-    fn = getattr(load(), name)
+    fn = _entry(name)
     if profile is not None and name in profile:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -192,4 +222,4 @@ def call(name: str, *args):
 
 def query(name: str, *args):
     """Call a size-query entry point (no stream, returns a number)."""
-    return getattr(load(), name)(*args)
+    return _entry(name)(*args)

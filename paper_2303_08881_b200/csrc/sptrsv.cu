@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(SELL_THREADS) sptrsv_sell(int n_groups, const 
 // group after that.  The startup chain (descriptor -> entries -> x) is thus off
 // the critical path and a SMALL number of resident warps is enough, which keeps
 // the L2 polling traffic (the thing that inflates every dependency hop) low.
+#ifdef DDILU_EXPERIMENTS   // measured-slower alternatives: pipelined SELL solve, CTA-per-block sweeps
 struct SellRow {
     int row, w;
     long long off;
@@ -790,6 +791,7 @@ __global__ void __launch_bounds__(BL_THREADS) sptrsv_blockwin_sell(int n_levels,
     }
 }
 
+#endif  // DDILU_EXPERIMENTS
 template <typename K>
 static int coop_grid(K kernel, int threads, int blocks_per_sm_cap, long long work_items) {
     int occ = 0;
@@ -806,6 +808,7 @@ static int coop_grid(K kernel, int threads, int blocks_per_sm_cap, long long wor
 
 using namespace ddilu;
 
+#ifdef DDILU_EXPERIMENTS   // tuning knobs of the probes
 extern "C" int ddilu_set_tuning(const char *key, int value) {
     if (!key) return DDILU_ERR_ARG;
     if (!strcmp(key, "trsv_blocks_per_sm")) g_trsv.blocks_per_sm = value;
@@ -821,6 +824,7 @@ extern "C" int ddilu_set_tuning(const char *key, int value) {
     return DDILU_OK;
 }
 
+#endif  // DDILU_EXPERIMENTS
 extern "C" int ddilu_levels(int n, const int *row_ptr, const int *col_idx, int upper, int *lev, int *max_lev,
                             void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -927,6 +931,7 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
     const int *w2 = (mask & 1) ? gfar2 : nullptr;
     unsigned far_sleep = (unsigned)g_trsv.far_sleep_ns;
     void *args[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &w0, &w1, &w2, &far_sleep, &b, &x};
+#ifdef DDILU_EXPERIMENTS
     if (g_trsv.pipe) {
         void *pargs[] = {&n_groups, &order, &goff, &uniform_width, &scol, &sval, &sdiag, &b, &x};
         // few resident warps: pipe_warps_per_sm warps on every SM, 4 warps per CTA
@@ -944,6 +949,7 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
         DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, 128, pargs, 0, st));
         return DDILU_OK;
     }
+#endif  // DDILU_EXPERIMENTS
     // dependencies polled per round: 4 for stencil-length rows, 8 / 16 for long rows (ILUT / ILU(k) /
     // 27-point factors); avg_width = average padded entries per lane of the layout
     if (avg_width <= 0.0) avg_width = uniform_width;
@@ -971,6 +977,7 @@ extern "C" int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *or
     return DDILU_OK;
 }
 
+#ifdef DDILU_EXPERIMENTS
 extern "C" int ddilu_blocklocal_table(int n, int n_blocks, const int *seg_ptr, int n_levels, const int *lev,
                                       const int *level_rows, int *start, int *cnt, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -1046,3 +1053,4 @@ extern "C" int ddilu_sptrsv_blocklocal_sell(int n_blocks, int n_levels, const in
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
+#endif  // DDILU_EXPERIMENTS

@@ -545,6 +545,7 @@ int launch_sweep(int rows_per_thread, int n_blocks, const SweepArgs &a, size_t s
 }
 }  // namespace
 
+#ifdef DDILU_EXPERIMENTS   // diagnostics of scripts/probe_sweep.py
 /* diagnostics: 64 int64 cycle counters per block */
 extern "C" int ddilu_sweep_set_debug(long long *buf) {
     g_sweep_dbg = buf;
@@ -557,6 +558,7 @@ extern "C" int ddilu_sweep_set_tuning(int writer_sleep_ns, int flags) {
     return DDILU_OK;
 }
 
+#endif  // DDILU_EXPERIMENTS
 /* phases: 1 = x = L^-1 rhs, 2 = x = U^-1 rhs, 3 = x = U^-1 L^-1 rhs; rhs in the schedule order of the first
  * phase (ddilu_sweep_rhs), results by row: out[row] = x (+ add[U position of the row], phases 2 and 3) */
 extern "C" int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const unsigned char *pages_l,

@@ -79,6 +79,7 @@ __global__ void tile_box_keys(int n, const int *__restrict__ nodes, int d0, int 
 // "Wavefront slab" tiles: footprint box in the first two grid coordinates x a range of `delta` consecutive
 // LEVELS of the factor.  On a wavefront-ordered stencil factor every level of such a tile holds the whole
 // footprint (t0*t1 rows), so a tile of t0*t1*delta rows has only delta levels (a t^3 box has 3t-2).
+#ifdef DDILU_EXPERIMENTS   // wavefront-slab tiles
 __global__ void tile_slab_keys(int n, const int *__restrict__ nodes, int d0, int d1, int t0, int t1, int nb0, int nb1,
                                const int *__restrict__ lev, int delta, int n_slabs, const int *__restrict__ owner,
                                int *__restrict__ keys) {
@@ -91,6 +92,7 @@ __global__ void tile_slab_keys(int n, const int *__restrict__ nodes, int d0, int
     }
 }
 
+#endif  // DDILU_EXPERIMENTS
 __global__ void tile_heads(int n, const int *__restrict__ skeys, int *__restrict__ flags) {
     GRID_STRIDE_Q(q, n) flags[q] = (q == 0 || skeys[q] != skeys[q - 1]) ? 1 : 0;
 }
@@ -826,6 +828,7 @@ sptrsv_tiled(int n_tiles, const int *__restrict__ blk_off16, const unsigned char
     }
 }
 
+#ifdef DDILU_EXPERIMENTS   // warp-per-tile and lean kernels: measured slower
 // ---------------------------------------------------------------------------
 // Warp-per-tile variant (tiles whose levels are mostly <= 32 rows wide: 8x8x4 interior boxes, 16x16
 // interface patches).  Every WARP owns a stream of tiles and is completely independent of the other
@@ -1100,11 +1103,13 @@ sptrsv_lean(int n_tiles, const int *__restrict__ blk_off16, const unsigned char 
     }
 }
 
+#endif  // DDILU_EXPERIMENTS
 }  // namespace ddilu
 
 using namespace ddilu;
 #define ST(s) ((cudaStream_t)(s))
 
+#ifdef DDILU_EXPERIMENTS
 extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
     if (!key) return DDILU_ERR_ARG;
     const char *k = key;
@@ -1126,6 +1131,7 @@ extern "C" int ddilu_tiled_set_tuning(const char *key, int value) {
     return DDILU_OK;
 }
 
+#endif  // DDILU_EXPERIMENTS
 extern "C" int ddilu_fastdiv_selftest(long long n_samples, unsigned long long seed, unsigned long long *mismatch,
                                       void *stream) {
     DDILU_CHECK(cudaMemsetAsync(mismatch, 0, sizeof(unsigned long long), ST(stream)));
@@ -1135,11 +1141,13 @@ extern "C" int ddilu_fastdiv_selftest(long long n_samples, unsigned long long se
     return DDILU_OK;
 }
 
+#ifdef DDILU_EXPERIMENTS
 extern "C" int ddilu_tiled_set_debug(long long *device_buf) {
     g_tiled.debug = device_buf;
     return DDILU_OK;
 }
 
+#endif  // DDILU_EXPERIMENTS
 extern "C" int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h,
                                    const int *owner, int *keys, long long *n_keys_h, void *stream) {
     if (nd < 1 || nd > 3) return DDILU_ERR_ARG;
@@ -1162,6 +1170,7 @@ extern "C" int ddilu_tile_box_keys(int n, const int *nodes, int nd, const int *d
     return DDILU_OK;
 }
 
+#ifdef DDILU_EXPERIMENTS
 extern "C" int ddilu_tile_slab_keys(int n, const int *nodes, int nd, const int *dims_h, const int *tdims_h,
                                     const int *lev, int n_levels, int delta, const int *owner, int n_owners, int *keys,
                                     long long *n_keys_h, void *stream) {
@@ -1179,6 +1188,7 @@ extern "C" int ddilu_tile_slab_keys(int n, const int *nodes, int nd, const int *
     return DDILU_OK;
 }
 
+#endif  // DDILU_EXPERIMENTS
 extern "C" int ddilu_tile_heads(int n, const int *sorted_keys, int *flags, void *stream) {
     if (n <= 0) return DDILU_OK;
     tile_heads<<<stream_grid(n, 256), 256, 0, ST(stream)>>>(n, sorted_keys, flags);
@@ -1304,6 +1314,7 @@ extern "C" int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, cons
     return DDILU_OK;
 }
 
+#ifdef DDILU_EXPERIMENTS
 extern "C" long long ddilu_warptile_smem_per_warp(int stat_max, int tmax, int emax) {
     long long b = 2LL * stat_max + 8LL * (tmax + emax + 2) + 16;
     return (b + 127) & ~127LL;
@@ -1371,3 +1382,4 @@ extern "C" int ddilu_sptrsv_lean(int n, int n_tiles, const int *blk_off16, const
     DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, wpb * 32, args, smem, st));
     return DDILU_OK;
 }
+#endif  // DDILU_EXPERIMENTS

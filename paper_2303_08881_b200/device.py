@@ -252,7 +252,7 @@ class TriSolveError(ZeroDivisionError):
 # tiled triangular solve (csrc/tiled.cu)
 
 USE_TILED = True
-TILE_KERNEL = "rot"       # "rot": CTA-per-tile kernel with rotating compute warps (production);
+TILE_KERNEL = "rot"       # "rot": CTA-per-tile kernel with rotating compute warps (production; the others need an experiments build);
                           # "warp": warp-per-tile kernels (independent warps; lean records when rows have <= 3
                           # dependencies) -- measured alternative, same throughput per SM
 TILE_MAX_ROWS = 1024
@@ -400,7 +400,7 @@ def build_lattice(t: DeviceCsr, part: TilePartition, upper: bool, unit_diag: boo
     than 3 dependencies, or the tile graph is cyclic -- the caller then uses the general tiled solve."""
     geom = getattr(part, "geom", None)
     n = t.n_rows
-    if not USE_LATTICE or geom is None or n == 0 or part.n != n:
+    if not USE_LATTICE or not _lib.has_experiments() or geom is None or n == 0 or part.n != n:
         return None
     nodes, dims, tdims = geom
     d3 = [int(v) for v in dims] + [1] * (3 - len(dims))
@@ -783,9 +783,10 @@ def sweep_solve(sp: SweepPlan, phases: int, out: torch.Tensor, add: bool = False
 
 def enable_block_local(sched: Schedule, seg_ptr) -> bool:
     """Use the CTA-per-block sweep for this factor if its independent row blocks
-    (seg_ptr, host ints) have narrow levels; returns whether it was enabled."""
+    (seg_ptr, host ints) have narrow levels; returns whether it was enabled.  (Experiments build only:
+    measured slower than the tiled kernel and than the TMA-fed block sweep of csrc/sweep.cu.)"""
     nb = len(seg_ptr) - 1
-    if sched.n == 0 or nb < 1 or sched.n_levels == 0:
+    if sched.n == 0 or nb < 1 or sched.n_levels == 0 or not _lib.has_experiments():
         return False
     if sched.n / (nb * sched.n_levels) > BLOCK_LOCAL_MAX_WIDTH:
         return False

@@ -18,7 +18,7 @@ from . import device as D
 __all__ = [
     "CsrMatrix", "Permutation", "csr_from_arrays", "csr_from_coo", "csr_from_dense", "csr_identity",
     "csr_transpose", "spmv", "tri_solve_lower", "tri_solve_upper", "permute_symmetric", "extract_block",
-    "take_submatrix", "vdot", "vnorm2",
+    "take_submatrix", "vdot", "vnorm2", "sparse_matmul",
 ]
 
 
@@ -285,6 +285,28 @@ def csr_transpose(a: CsrMatrix) -> CsrMatrix:
     out = D.DeviceCsr(a.n_cols, a.n_rows, rp[: a.n_cols + 1], D.gather_i32(rows, perm),
                       d.val[perm.long()], nnz)
     return CsrMatrix.from_device(out)
+
+
+def sparse_matmul(a: CsrMatrix, b: CsrMatrix) -> CsrMatrix:
+    """sparse.py:487-505: a @ b with the exact structural pattern (entries that cancel to zero are kept).
+    Count -> scan -> expand (products of a row in the reference's traversal order, stably sorted by column)
+    -> scan -> sum the runs, on the device; values carry the reference's bits."""
+    if a.n_cols != b.n_rows:
+        raise ValueError("inner dimensions do not match")
+    n = a.n_rows
+    da, db = a.device(), b.device()
+    off = D.zeros_i32(n + 1)
+    D.call("ddilu_spgemm_bound", n, da.rp, da.ci, db.rp, off)
+    D.exclusive_scan_(off, n)
+    total = int(off[-1].item()) if n else 0
+    s_col, s_val = D.empty_i32(max(total, 1)), D.empty_f64(max(total, 1))
+    out_rp = D.zeros_i32(n + 1)
+    D.call("ddilu_spgemm_expand", n, da.rp, da.ci, da.val, db.rp, db.ci, db.val, off, s_col, s_val, out_rp)
+    D.exclusive_scan_(out_rp, n)
+    nnz = int(out_rp[-1].item()) if n else 0
+    out_ci, out_v = D.empty_i32(max(nnz, 1)), D.empty_f64(max(nnz, 1))
+    D.call("ddilu_spgemm_compact", n, off, s_col, s_val, out_rp, out_ci, out_v)
+    return CsrMatrix.from_device(D.DeviceCsr(n, b.n_cols, out_rp, out_ci[:nnz], out_v[:nnz], nnz))
 
 
 _reducer = None

@@ -1,21 +1,83 @@
-"""Small tiled solves for compute-sanitizer (memcheck / racecheck / synccheck)."""
-import os, sys
-import numpy as np, torch
+"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck); logs -> profiles/r2_sanitizer_*.log.
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_case.py [tiled|sweep|mgs|ilut|rcm|pipeline ...]
+
+tiled: sptrsv_tiled on interior + interface factors; sweep: the block sweep (L, U, fused, with product and add);
+mgs: ddilu_mgs_block over ragged lengths and block shapes; ilut: ilut_kernel (27-point, fill);
+rcm: cm_order_kernel on several disconnected blocks; pipeline: one schur + rap-milu FGMRES solve."""
+import os
+import sys
+
+import numpy as np
+import torch
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_08881_b200 as P
 from paper_2303_08881_b200 import device as D
 
-kern = sys.argv[1] if len(sys.argv) > 1 else "rot"
-D.TILE_KERNEL = kern
+which = sys.argv[1:] or ["tiled", "sweep", "mgs", "ilut", "rcm", "pipeline"]
 dims = (20, 18, 17)
 a = P.aniso3d(*dims)
 layout = P.classify_and_order(a, P.partition(a, 4, dims), 4)
-m = P.make_preconditioner("schur", a, layout)
-for f in (m._p.interior, m._p.schur):
-    assert f._tl is not None and f._tu is not None
+
+if "tiled" in which:
+    D.USE_SWEEP = False
+    m = P.make_preconditioner("schur", a, layout)
+    for f in (m._p.interior, m._p.schur):
+        assert f._tl is not None and f._tu is not None
+        r = torch.randn(f.n, dtype=torch.float64, device="cuda")
+        x = torch.empty_like(r)
+        f.lower_solve(r, x)
+        f.upper_solve(r, x)
+        torch.cuda.synchronize()
+        print("tiled", f._tl.kind, f.n, float(x.abs().max()))
+    D.USE_SWEEP = True
+
+if "sweep" in which:
+    from paper_2303_08881_b200.factor import solve_with_product
+    m = P.make_preconditioner("schur", a, layout)
+    f, s = m._p.schur, m.system
+    assert f._sw is not None
     r = torch.randn(f.n, dtype=torch.float64, device="cuda")
     x = torch.empty_like(r)
     f.lower_solve(r, x)
     f.upper_solve(r, x)
+    f.solve(r, x)
+    y = torch.randn(s.n_ext + s.n_halo, dtype=torch.float64, device="cuda")
+    solve_with_product(f, m._coupling, y, None, 0, x, add=y)
     torch.cuda.synchronize()
-    print(kern, f._tl.kind, f.n, float(x.abs().max()))
+    print("sweep", f.n, f._sw.nct, f._sw.sets, float(x.abs().max()))
+
+if "mgs" in which:
+    red = D.Reducer()
+    for n in (1, 33, 1000, 40001):
+        ld = (n + 1) & ~1
+        V = torch.randn((9, ld), dtype=torch.float64, device="cuda")
+        w = torch.randn(ld, dtype=torch.float64, device="cuda")
+        raw = torch.zeros((4, 40), dtype=torch.float64, device="cuda")
+        h = torch.zeros(16, dtype=torch.float64, device="cuda")
+        for kn in (1, 2, 3, 4):
+            red.mgs_block(n, ld, 0, None, None, None, w, kn, V[0], raw[0])
+            red.mgs_block(n, ld, kn, V[0], raw[0], h[:kn], w, min(4, 8 - kn), V[kn], raw[1])
+            red.mgs_block(n, ld, min(4, 8 - kn), V[kn], raw[1], h[kn:kn + min(4, 8 - kn)], w, 0, None, h[9:10])
+    torch.cuda.synchronize()
+    print("mgs ok")
+
+if "ilut" in which:
+    a27 = P.convdiff27(9, 8, 7)
+    f = P.ilut(a27, 1e-3, 10)
+    pf = P.partial_ilu(a27, 300, P.FillRule.parse("ilut:0.001,8"))
+    print("ilut", f.lower.nnz, f.upper.nnz, pf.s_tilde.nnz)
+
+if "rcm" in which:
+    lay8 = P.classify_and_order(a, P.partition(a, 8, dims), 8)
+    m = P.make_preconditioner("bj", a, lay8)
+    print("rcm", [len(d.interior_nodes) for d in m.domains])
+    print("rcm single", int(P.rcm(P.poisson2d(13, 11)).forward.sum()))
+
+if "pipeline" in which:
+    b = P.default_rhs(a)
+    for pc in ("schur", "rap-milu"):
+        m = P.make_preconditioner(pc, a, layout)
+        x, rep = P.fgmres(a, b, m=m.apply)
+        print("pipeline", pc, rep.iterations, rep.converged)

@@ -1,0 +1,42 @@
+"""BASELINE-sized configurations on the GPU against the oracle's cached runs (tests/golden/iterations_large.json,
+written by tests/golden/make_iterations_large.py; the 128^3 counts are also the reference's own, SURVEY.md
+Appendix B: bj p = 1/2/4/8 -> 190/233/244/244, schur 191, rap 182, rap-milu 138): iteration counts within +-1 at
+the same convergence flag (the north star's bar), early residual history to 1e-6."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+with open(os.path.join(HERE, "golden", "iterations_large.json")) as fh:
+    GOLD = json.load(fh)
+
+SMALL = sorted(k for k, v in GOLD.items() if v["dims"][0] <= 128)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2303_08881_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_iterations_match_the_oracle(P, name):
+    g = GOLD[name]
+    dims = tuple(g["dims"])
+    if g["kind"] == "aniso3d":
+        spec = P.ProblemSpec("aniso3d", dims, eps=tuple(g["param"]))
+    else:
+        spec = P.ProblemSpec("convdiff27", dims, velocity=tuple(g["param"]))
+    cfg = P.RunConfig(spec, domains=g["p"], precond=g["precond"], fill=P.FillRule.parse(g["fill"]), history=True)
+    rec, rep = P.run(cfg)
+    assert rec["converged"] == g["converged"]
+    assert abs(rec["its"] - g["its"]) <= 1, (name, rec["its"], g["its"])
+    assert rec["final_relres"] <= 1e-8
+    ref = np.array([float.fromhex(h) for h in g["history_hex"]])
+    k = min(20, len(ref), len(rep.residual_history))
+    assert np.allclose(rep.residual_history[:k], ref[:k], rtol=1e-6, atol=0), name

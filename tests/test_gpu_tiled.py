@@ -20,6 +20,14 @@ def orc():
     return ddilu_oracle
 
 
+@pytest.fixture
+def experiments():
+    """Tests of the measured-slower alternative kernels run against a DDILU_EXPERIMENTS=1 build only."""
+    from paper_2303_08881_b200 import _lib
+    if not _lib.has_experiments():
+        pytest.skip("alternative kernel: needs a DDILU_EXPERIMENTS=1 build")
+
+
 def _factor_pairs(m):
     """(name, DevFactors) of every factor pair a preconditioner solves with."""
     out = []
@@ -37,6 +45,9 @@ def tile_kernel(request):
     """Run with the production kernels (lattice solve where the tiles qualify, CTA-per-tile kernel elsewhere),
     with the CTA-per-tile kernel alone and with the warp-per-tile alternatives."""
     from paper_2303_08881_b200 import device as D
+    from paper_2303_08881_b200 import _lib
+    if request.param != "rot" and not _lib.has_experiments():
+        pytest.skip("alternative kernel: needs a DDILU_EXPERIMENTS=1 build")
     old, old_lat, old_sw = D.TILE_KERNEL, D.USE_LATTICE, D.USE_SWEEP
     D.TILE_KERNEL = "rot" if request.param == "lattice" else request.param
     D.USE_LATTICE = request.param == "lattice"
@@ -190,7 +201,7 @@ def _strict_lower(a):
 
 
 @pytest.mark.parametrize("dims,p", [((20, 20, 20), 8), ((24, 16, 12), 4), ((40, 40), 4)])
-def test_block_window_sweep_bit_exact(P, orc, dims, p):
+def test_block_window_sweep_bit_exact(P, orc, dims, p, experiments):
     """Interface factors solved by the CTA-per-block sweep with x in a shared-memory window
     (`ddilu_sptrsv_blockwin_sell`): same bits as the oracle's serial solves, L and U."""
     import torch
@@ -216,7 +227,7 @@ def test_block_window_sweep_bit_exact(P, orc, dims, p):
         assert np.array_equal(out.cpu().numpy(), ref), ("U" if upper else "L")
 
 
-def test_block_window_refuses_far_dependencies(P):
+def test_block_window_refuses_far_dependencies(P, experiments):
     """A factor whose rows reach further back than the largest window must not get a plan."""
     from paper_2303_08881_b200 import device as D
     n = 3 * D.BLOCK_WINDOW_MAX
@@ -235,7 +246,7 @@ def test_block_window_refuses_far_dependencies(P):
 
 @pytest.mark.parametrize("dims,p,tile", [((40, 37, 29), 8, (8, 8, 8)), ((33, 33, 33), 1, (16, 8, 8)),
                                          ((21, 20, 19), 2, (8, 8, 4)), ((36, 36, 36), 8, (4, 4, 4))])
-def test_lattice_solves_bit_exact(P, orc, dims, p, tile):
+def test_lattice_solves_bit_exact(P, orc, dims, p, tile, experiments):
     """csrc/lattice.cu on ragged boxes, partial tiles and several tile shapes: bit-exact against the oracle's
     serial solves (sparse.py:228-272), L and U (the U solve runs every axis in the opposite direction)."""
     import torch

@@ -12,10 +12,13 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _header_symbols():
-    text = open(os.path.join(ROOT, "include", "ddilu_b200.h")).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(ddilu_[a-z0-9_]+)\s*\(", text)))
+def _header_text(name="ddilu_b200.h"):
+    text = open(os.path.join(ROOT, "include", name)).read()
+    return re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+
+
+def _header_symbols(name="ddilu_b200.h"):
+    return sorted(set(re.findall(r"\b(ddilu_[a-z0-9_]+)\s*\(", _header_text(name))))
 
 
 def test_library_exports_every_declared_symbol():
@@ -28,13 +31,24 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_lib.SIGNATURES) == names, "ctypes table and header disagree"
 
 
+def test_experiment_entries_are_not_part_of_the_product_abi():
+    """Alternative kernels, tuning knobs and diagnostics live in ddilu_b200_experiments.h; a product build
+    exports none of them, an experiments build (DDILU_EXPERIMENTS=1) exports all of them."""
+    from paper_2303_08881_b200 import _lib
+    lib = _lib.load()
+    names = _header_symbols("ddilu_b200_experiments.h")
+    assert sorted(_lib.EXPERIMENT_SIGNATURES) == names, "ctypes table and experiments header disagree"
+    assert not set(names) & set(_header_symbols())
+    present = [hasattr(lib, n) for n in names]
+    assert all(present) if _lib.has_experiments() else not any(present)
+
+
 def test_header_argument_counts_match_ctypes_table():
     from paper_2303_08881_b200 import _lib
-    text = open(os.path.join(ROOT, "include", "ddilu_b200.h")).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    for name, args in re.findall(r"\b(ddilu_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
-        nargs = 0 if args.strip() in ("", "void") else len(args.split(","))
-        assert nargs == len(_lib.SIGNATURES[name][1]), name
+    for header, table in (("ddilu_b200.h", _lib.SIGNATURES), ("ddilu_b200_experiments.h", _lib.EXPERIMENT_SIGNATURES)):
+        for name, args in re.findall(r"\b(ddilu_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", _header_text(header)):
+            nargs = 0 if args.strip() in ("", "void") else len(args.split(","))
+            assert nargs == len(table[name][1]), name
 
 
 def test_no_cpu_fallback_without_cuda():
