@@ -144,7 +144,7 @@ int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned 
  * adds to its results, in U schedule order.
  * ddilu_sweep_solve: phases 1 = L, 2 = U, 3 = L then U; blocks = 8 ints per block {rows, first page, L levels,
  * U levels, offset into levtab, 0, 0, 0}; stages = ring depth (power of two), sets x nct compute threads that own
- * rows_per_thread (1, 2, 4) rows of a level each; out[row] = x (+ add[U position of the row]: `y + S^-1 E y`,
+ * rows_per_thread (1, 2) rows of a level each; out[row] = x (+ add[U position of the row]: `y + S^-1 E y`,
  * precond.py:249). */
 int ddilu_sweep_page_rows(void);
 int ddilu_sweep_helper_threads(void);   /* threads of a CTA that do not compute (TMA issuer, gate, writers) */
@@ -215,6 +215,14 @@ int ddilu_mgs_block(long long n, long long ld, int kp, const double *vprev, cons
 /* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
 int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
                 double *y, void *stream);
+/* krylov.py:233-268: the host arithmetic of `fixed_gmres` (Givens rotations, back substitution) for an m-step
+ * inner solve (m <= ddilu_gmres_small_max()) on the device: H row j = [h_0j .. h_jj, |w_j|^2] with stride ldh,
+ * *bb = <b, b>; coef[0..m) = coefficients of the basis combination.  *flag is set to 1 when the reference
+ * would have left its loop early (zero right-hand side, happy breakdown) or a number is not finite: the caller
+ * then redoes the application on the host-read path. */
+int ddilu_gmres_small_max(void);
+int ddilu_gmres_small_solve(int m, const double *H, int ldh, const double *bb, double happy_tol, double *coef,
+                            int *flag, void *stream);
 /* x (+)= sum_i coef[i] * basis[i*ld + :] in increasing i */
 /* L2 residency hint for the Arnoldi work vector (stream access-policy window, persisting L2); bytes = 0 clears */
 int ddilu_l2_persist_window(const void *ptr, long long bytes, void *stream);

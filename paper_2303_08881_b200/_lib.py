@@ -76,6 +76,8 @@ SIGNATURES = {
     "ddilu_scale": (_I, [_L, _P, _P, _D, _I, _I, _P, _P]),
     "ddilu_l2_persist_window": (_I, [_P, _L, _P]),
     "ddilu_multi_axpy": (_I, [_L, _I, _P, _L, _P, _P, _I, _P]),
+    "ddilu_gmres_small_max": (_I, []),
+    "ddilu_gmres_small_solve": (_I, [_I, _P, _I, _P, _D, _P, _P, _P]),
     "ddilu_ewise": (_I, [_L, _P, _P, _I, _P, _P]),
     "ddilu_gather": (_I, [_L, _P, _P, _P, _P]),
     "ddilu_scatter": (_I, [_L, _P, _P, _P, _P]),

@@ -91,6 +91,16 @@ __device__ __forceinline__ int sw_ld_progress(const int *p) {
 __device__ __forceinline__ void sw_st_progress(int *p, int v) {
     asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(sw_smem_u32(p)), "r"(v) : "memory");
 }
+// pages-landed counter: release / acquire, so that ptxas cannot move a thread's operand loads in front of the
+// load that tells it the page is there (it did, with plain volatile accesses)
+__device__ __forceinline__ int sw_ld_landed(const int *p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(sw_smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sw_st_landed(int *p, int v) {
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(sw_smem_u32(p)), "r"(v) : "memory");
+}
 
 struct SweepArgs {
     const int *blocks;              // SW_BLOCK_INTS per block
@@ -116,7 +126,7 @@ struct SweepArgs {
 __host__ __device__ inline size_t sw_ctl_bytes() { return (2 * SW_MAX_STAGES + 2) * 8; }   // + progress, landed (2 ints)
 __host__ __device__ inline size_t sw_smem_bytes(int K, int stages, int window, int max_lev) {
     size_t b = sw_ctl_bytes();
-    b += ((size_t)max_lev * 4 + 15) & ~(size_t)15;
+    b += ((size_t)max_lev * 8 + 15) & ~(size_t)15;      // (start, end) pair per level
     b += ((size_t)(window + 1) * 8 + 15) & ~(size_t)15;
     b = (b + 127) & ~(size_t)127;
     return b + (size_t)stages * sw_stage_bytes(K);
@@ -164,15 +174,37 @@ __device__ __forceinline__ void sw_mbar_wait_u32(uint32_t bar, uint32_t parity) 
     } while (!done);
 }
 
+__device__ __forceinline__ int sw_gt(int a, int b) {     // a > b, evaluated where it is written
+    int v;
+    asm volatile("{\n .reg .pred q;\n setp.gt.s32 q, %1, %2;\n selp.s32 %0, 1, 0, q;\n}" : "=r"(v) : "r"(a), "r"(b));
+    return v;
+}
+template <int ID>
+__device__ __forceinline__ void sw_bar_sync_c(int threads) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(threads) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void sw_bar_arrive_c(int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(threads) : "memory");
+}
+__device__ __forceinline__ int2 sw_lds_v2(uint32_t a) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+
 // The compute threads form NS (2 or 3) sets that take the levels in turn: while one set runs the chain of level
 // l (K window loads, multiply/subtract chain [, division], two stores per row), the next set has the operands
 // of level l + 1 in registers already and waits on the named barrier the first set arrives at -- operand fetch
-// and address arithmetic (a few hundred cycles of dependent instructions for a lone thread) are off the
-// dependency chain.  A thread owns R rows of its level (row s + t + j * nct): few warps per set keep the named
-// barrier cheap (its cost grows with the number of warps), R independent chains per thread fill the latencies.
+// and address arithmetic are off the dependency chain.  A thread owns R rows of its level (row s + t + j nct).
 // Barrier 1 + (l % NS) = 1 + set: arrived at by the set of level l, synced on by the set of level l + 1.
-template <int K, int R, bool UPPER>
-__device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, const int *lev, int nlev, int gq0,
+// The kernel is bound by instruction issue (ncu: 1.8 warp instructions per cycle and SM, ~500 per level before
+// this loop was trimmed): every instruction a warp executes per level counts, also in warps that own no row of
+// the level, so the loop carries nothing but the (start, end) pair of the level, the barrier pair and, for the
+// rows that exist, operand fetch and chain.  DBG (experiments build) adds cycle counters and the strip flags
+// of scripts/probe_sweep.py.
+template <int K, int R, bool UPPER, bool DBG, int BAR_IN, int BAR_OUT>
+__device__ __forceinline__ void sweep_levels(int set, int NS, int t, int nct, uint32_t lev_u32, int nlev, int gq0,
                                               int smask, const int *landed, uint32_t stage0_u32, uint32_t xs_u32,
                                               int wmask, int *progress, int done_base, long long *dbg, int xflags) {
     constexpr int P = SW_PAGE;
@@ -181,87 +213,101 @@ __device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, c
     constexpr int OFF_RHS = sw_page_bytes(K, true);
     constexpr int STAGE = sw_stage_bytes(K);
     const int pair = 2 * nct;                 // threads of a producer set + a consumer set
-    // l = set + i NS: the set always arrives at barrier 1 + set and syncs on its predecessor's (no modulo per level)
-    const int bar_out = 1 + set, bar_in = 1 + (set == 0 ? NS - 1 : set - 1);
     int have = 0;                             // ring ordinals below `have` are known to have landed
     long long wait_cycles = 0, t_begin = 0, t_ops = 0, t_fin = 0;
-    if (dbg) t_begin = clock64();
+    if (DBG && dbg) t_begin = clock64();
     double c[R][K], rhs[R], d[R], r[R];
     uint32_t sa[R][K], wa[R], slot[R];
-    auto operands = [&](int j, int p) {
-        if (xflags & 128) return;
-        const int g = gq0 + (p >> 8);
-        if (g >= have) {
-            long long c0 = 0;
-            if (dbg) c0 = clock64();
-            while ((have = sw_ld_progress(landed)) <= g) {}
-            if (dbg) wait_cycles += clock64() - c0;
-        }
-        if (xflags & 64) return;
-        const uint32_t sb = stage0_u32 + (uint32_t)(g & smask) * STAGE;
-        const uint32_t off = (uint32_t)(p & (P - 1));
-        const uint32_t a8 = sb + off * 8u, a2 = sb + OFF_CODE + off * 2u;
-        uint32_t code[K];
-        if (K >= 1) { c[j][0] = sw_lds_at<0>(a8); code[0] = sw_lds_u16_at<0>(a2); }
-        if (K >= 2) { c[j][1 % K] = sw_lds_at<8 * P>(a8); code[1 % K] = sw_lds_u16_at<2 * P>(a2); }
-        if (K >= 3) { c[j][2 % K] = sw_lds_at<16 * P>(a8); code[2 % K] = sw_lds_u16_at<4 * P>(a2); }
-        if (K >= 4) { c[j][3 % K] = sw_lds_at<24 * P>(a8); code[3 % K] = sw_lds_u16_at<6 * P>(a2); }
-        if (K >= 8) {
-            c[j][4 % K] = sw_lds_at<32 * P>(a8); code[4 % K] = sw_lds_u16_at<8 * P>(a2);
-            c[j][5 % K] = sw_lds_at<40 * P>(a8); code[5 % K] = sw_lds_u16_at<10 * P>(a2);
-            c[j][6 % K] = sw_lds_at<48 * P>(a8); code[6 % K] = sw_lds_u16_at<12 * P>(a2);
-            c[j][7 % K] = sw_lds_at<56 * P>(a8); code[7 % K] = sw_lds_u16_at<14 * P>(a2);
-        }
-        rhs[j] = sw_lds_at<OFF_RHS>(a8);
-        if (UPPER) {
-            d[j] = sw_lds_at<OFF_PIV>(a8);
-            r[j] = sw_lds_at<OFF_PIV + 8 * P>(a8);
-        }
-        slot[j] = a8 + OFF_RHS;
-        wa[j] = xs_u32 + 8u * (uint32_t)(p & wmask);
-#pragma unroll
-        for (int k = 0; k < K; ++k) sa[j][k] = xs_u32 + 8u * code[k];
-    };
-    auto finish = [&](int j) {
-        double v[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = (xflags & 4) ? 1.0 : sw_lds(sa[j][k]);
-        double sum = rhs[j];
-        if (!(xflags & 8)) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) sum -= c[j][k] * v[k];   // -fmad=false: the product is rounded first
-            if (UPPER) sum = exact_div(sum, d[j], r[j]);
-        }
-        if (!(xflags & 32)) sw_sts(wa[j], sum);
-        if (!(xflags & 16)) sw_sts(slot[j], sum);   // the writer warps take it from the page (the window slot is reused W rows later)
-    };
-    const uint32_t lev_u32 = sw_smem_u32(lev);
-    for (int l = set; l < nlev; l += NS) {
-        const int s = l ? sw_lds_s32(lev_u32 + 4u * (uint32_t)(l - 1)) : 0, e = sw_lds_s32(lev_u32 + 4u * (uint32_t)l);
+#define SW_OPERANDS(j, p)                                                                              \
+    do {                                                                                               \
+        if (DBG && (xflags & 128)) break;                                                              \
+        const int g_ = gq0 + ((p) >> 8);                                                               \
+        if (g_ >= have) {                                                                              \
+            long long w0_ = 0;                                                                         \
+            if (DBG && dbg) w0_ = clock64();                                                           \
+            while ((have = sw_ld_landed(landed)) <= g_) {}                                           \
+            if (DBG && dbg) wait_cycles += clock64() - w0_;                                            \
+        }                                                                                              \
+        if (DBG && (xflags & 64)) break;                                                               \
+        const uint32_t off_ = (uint32_t)((p) & (P - 1));                                               \
+        const uint32_t a8_ = stage0_u32 + (uint32_t)(g_ & smask) * STAGE + off_ * 8u;                  \
+        const uint32_t a2_ = a8_ - off_ * 6u + OFF_CODE;                                               \
+        uint32_t code_[K];                                                                             \
+        if (K >= 1) { c[j][0] = sw_lds_at<0>(a8_); code_[0] = sw_lds_u16_at<0>(a2_); }                 \
+        if (K >= 2) { c[j][1 % K] = sw_lds_at<8 * P>(a8_); code_[1 % K] = sw_lds_u16_at<2 * P>(a2_); } \
+        if (K >= 3) { c[j][2 % K] = sw_lds_at<16 * P>(a8_); code_[2 % K] = sw_lds_u16_at<4 * P>(a2_); } \
+        if (K >= 4) { c[j][3 % K] = sw_lds_at<24 * P>(a8_); code_[3 % K] = sw_lds_u16_at<6 * P>(a2_); } \
+        if (K >= 8) {                                                                                  \
+            c[j][4 % K] = sw_lds_at<32 * P>(a8_); code_[4 % K] = sw_lds_u16_at<8 * P>(a2_);            \
+            c[j][5 % K] = sw_lds_at<40 * P>(a8_); code_[5 % K] = sw_lds_u16_at<10 * P>(a2_);           \
+            c[j][6 % K] = sw_lds_at<48 * P>(a8_); code_[6 % K] = sw_lds_u16_at<12 * P>(a2_);           \
+            c[j][7 % K] = sw_lds_at<56 * P>(a8_); code_[7 % K] = sw_lds_u16_at<14 * P>(a2_);           \
+        }                                                                                              \
+        rhs[j] = sw_lds_at<OFF_RHS>(a8_);                                                              \
+        if (UPPER) {                                                                                   \
+            d[j] = sw_lds_at<OFF_PIV>(a8_);                                                            \
+            r[j] = sw_lds_at<OFF_PIV + 8 * P>(a8_);                                                    \
+        }                                                                                              \
+        slot[j] = a8_ + OFF_RHS;                                                                       \
+        wa[j] = xs_u32 + 8u * (uint32_t)((p) & wmask);                                                 \
+        _Pragma("unroll") for (int k_ = 0; k_ < K; ++k_) sa[j][k_] = xs_u32 + 8u * code_[k_];          \
+    } while (0)
+#define SW_FINISH(j)                                                                                   \
+    do {                                                                                               \
+        double v_[K];                                                                                  \
+        _Pragma("unroll") for (int k_ = 0; k_ < K; ++k_)                                               \
+            v_[k_] = (DBG && (xflags & 4)) ? 1.0 : sw_lds(sa[j][k_]);                                  \
+        double sum_ = rhs[j];                                                                          \
+        if (!(DBG && (xflags & 8))) {                                                                  \
+            /* -fmad=false: every product is rounded before it is subtracted */                       \
+            _Pragma("unroll") for (int k_ = 0; k_ < K; ++k_) sum_ -= c[j][k_] * v_[k_];                \
+            if (UPPER) sum_ = exact_div(sum_, d[j], r[j]);                                             \
+        }                                                                                              \
+        if (!(DBG && (xflags & 32))) sw_sts(wa[j], sum_);                                              \
+        /* the writer warps take the result from the page (the window slot is reused W rows later) */  \
+        if (!(DBG && (xflags & 16))) sw_sts(slot[j], sum_);                                            \
+    } while (0)
+    uint32_t lp = lev_u32 + 8u * (uint32_t)set;
+    const int cover = R * nct;                      // rows of a level the prefetched slots cover
+    for (int l = set; l < nlev; l += NS, lp += 8u * (uint32_t)NS) {
+        const int2 se = sw_lds_v2(lp);              // positions [start, end) of the level
+        const int p0 = se.x + t, e = se.y;
+        // everything the chain does not need is decided BEFORE the barrier: what sits between the barrier and the
+        // arrive is the dependency chain of the whole solve
+        // (inline asm keeps the compiler from sinking the comparisons behind the chain)
+        const int wide = sw_gt(e - se.x, cover), more = sw_gt(nlev, l + 1);
+        const bool first = l == 0;
         long long c0 = 0, c1 = 0;
-        if (dbg) c0 = clock64();
+        if (DBG && dbg) c0 = clock64();
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (s + t + j * nct < e) operands(j, s + t + j * nct);
-        if (dbg) c1 = clock64();
-        if (l > 0) sw_bar_sync_id(bar_in, pair);               // results of the previous level are in the window
-        if (t == 0) sw_st_progress(progress, done_base + s);
+            if (p0 + j * nct < e) SW_OPERANDS(j, p0 + j * nct);
+        if (DBG && dbg) c1 = clock64();
+        if (!first) sw_bar_sync_c<BAR_IN>(pair);    // results of the previous level are in the window
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (s + t + j * nct < e) finish(j);
-        for (int p = s + t + R * nct; p < e; p += nct) {         // levels wider than R rows per thread
-            operands(0, p);
-            finish(0);
+            if (p0 + j * nct < e) SW_FINISH(j);
+        if (wide) {                                 // levels wider than R rows per thread (rare)
+            for (int p = p0 + cover; p < e; p += nct) {
+                SW_OPERANDS(0, p);
+                SW_FINISH(0);
+            }
         }
-        if (l + 1 < nlev) sw_bar_arrive_id(bar_out, pair);
-        if (dbg) {
+        if (more) sw_bar_arrive_c<BAR_OUT>(pair);
+        if (t == 0) sw_st_progress(progress, done_base + se.x);   // rows below the level's start are complete
+        if (DBG && dbg) {
             t_ops += c1 - c0;
             t_fin += clock64() - c1;
         }
     }
-    sw_bar_sync_id(4, NS * nct);                               // end of the phase: every row is stored
-    if (set == 0 && t == 0) sw_st_progress(progress, done_base + (nlev ? lev[nlev - 1] : 0));
-    if (dbg && t == 0) {
+#undef SW_OPERANDS
+#undef SW_FINISH
+    sw_bar_sync_id(4, NS * nct);                    // end of the phase: every row is stored
+    if (set == 0 && t == 0) {
+        const int last = nlev ? sw_lds_v2(lev_u32 + 8u * (uint32_t)(nlev - 1)).y : 0;
+        sw_st_progress(progress, done_base + last);
+    }
+    if (DBG && dbg && t == 0) {
         long long *o = dbg + 16 * set;
         o[UPPER ? 1 : 0] = clock64() - t_begin;
         o[2] += wait_cycles;
@@ -270,8 +316,27 @@ __device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, c
     }
 }
 
-template <int K, int R>
-__global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
+// barrier ids as immediates (a register id makes the compiler pack id and count around every barrier instruction)
+template <int K, int R, bool UPPER, bool DBG>
+__device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, uint32_t lev_u32, int nlev, int gq0,
+                                              int smask, const int *landed, uint32_t stage0_u32, uint32_t xs_u32,
+                                              int wmask, int *progress, int done_base, long long *dbg, int xflags) {
+#define SW_CALL(IN, OUT)                                                                                        \
+    sweep_levels<K, R, UPPER, DBG, IN, OUT>(set, NS, t, nct, lev_u32, nlev, gq0, smask, landed, stage0_u32, xs_u32, \
+                                            wmask, progress, done_base, dbg, xflags)
+    if (set == 0) {
+        if (NS == 2) SW_CALL(2, 1);
+        else SW_CALL(3, 1);
+    } else if (set == 1) {
+        SW_CALL(1, 2);
+    } else {
+        SW_CALL(2, 3);
+    }
+#undef SW_CALL
+}
+
+template <int K, int R, int MAXT, bool DBG>
+__global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepArgs a) {
     constexpr int P = SW_PAGE;
     constexpr int STAGE = sw_stage_bytes(K);
     constexpr int OFF_RHS = sw_page_bytes(K, true);
@@ -286,7 +351,7 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
     int *progress = (int *)(lflush + 1);
     int *landed = progress + 1;
     int *levs = (int *)(sw_smem + sw_ctl_bytes());
-    double *xs = (double *)((unsigned char *)levs + (((size_t)a.max_lev * 4 + 15) & ~(size_t)15));
+    double *xs = (double *)((unsigned char *)levs + (((size_t)a.max_lev * 8 + 15) & ~(size_t)15));
     size_t off = (size_t)((unsigned char *)xs - sw_smem) + ((((size_t)a.wmask + 2) * 8 + 15) & ~(size_t)15);
     off = (off + 127) & ~(size_t)127;
     unsigned char *stage0 = sw_smem + off;
@@ -302,7 +367,13 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
         xs[a.wmask + 1] = 0.0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < nlev_l + nlev_u; i += blockDim.x) levs[i] = a.levtab[lev_off + i];
+    // level table as (start, end) position pairs: one shared-memory load per level in the compute loop
+    for (int i = tid; i < nlev_l + nlev_u; i += blockDim.x) {
+        const int e = a.levtab[lev_off + i];
+        const int st = (i == 0 || i == nlev_l) ? 0 : a.levtab[lev_off + i - 1];
+        levs[2 * i] = st;
+        levs[2 * i + 1] = e;
+    }
     __syncthreads();
     const int n_pages = (n_rows + P - 1) / P;
     const bool do_l = a.phases & 1, do_u = a.phases & 2;
@@ -313,16 +384,16 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
     if (tid < ncomp) {
         // ------------------------------------------------------------ compute warps (NS sets)
         const int set = tid / nct, t = tid - set * nct;
-        long long *dbg = a.dbg ? a.dbg + 64 * blockIdx.x : nullptr;
-        if (dbg && t == 0) dbg[16 * set + 2] = 0;
-        const uint32_t stage0_u32 = sw_smem_u32(stage0), xs_u32 = sw_smem_u32(xs);
+        long long *dbg = (DBG && a.dbg) ? a.dbg + 64 * blockIdx.x : nullptr;
+        if (DBG && dbg && t == 0) dbg[16 * set + 2] = 0;
+        const uint32_t stage0_u32 = sw_smem_u32(stage0), xs_u32 = sw_smem_u32(xs), lev_u32 = sw_smem_u32(levs);
         if (do_l)
-            sweep_compute<K, R, false>(set, NS, t, nct, levs, nlev_l, 0, smask, landed, stage0_u32, xs_u32, a.wmask,
-                                       progress, 0, dbg, a.flags);
+            sweep_compute<K, R, false, DBG>(set, NS, t, nct, lev_u32, nlev_l, 0, smask, landed, stage0_u32, xs_u32,
+                                            a.wmask, progress, 0, dbg, a.flags);
         if (do_u)
-            sweep_compute<K, R, true>(set, NS, t, nct, levs + nlev_l, nlev_u, gq_u, smask, landed, stage0_u32, xs_u32,
-                                      a.wmask, progress, done_u, dbg, a.flags);
-    } else if (a.flags & 256) {
+            sweep_compute<K, R, true, DBG>(set, NS, t, nct, lev_u32 + 8u * (uint32_t)nlev_l, nlev_u, gq_u, smask,
+                                           landed, stage0_u32, xs_u32, a.wmask, progress, done_u, dbg, a.flags);
+    } else if (DBG && (a.flags & 256)) {
         // diagnostics: no helper warps at all (with flags 252: the bare level hand-over of the compute sets)
     } else if (tid == ncomp) {
         // ------------------------------------------------------------ issuer: one TMA group per page
@@ -343,7 +414,7 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
             if (with_add) sw_bulk_g2s(st + OFF_RHS + P * 8, a.add + (size_t)(page0 + q) * P, P * 8, &full[s]);
             // pull the operands of a page further ahead than the ring into L2 (HBM latency > ring depth)
             const int j = i + 2 * S;
-            if (j < total && !(a.flags & 2)) {
+            if (j < total && !(DBG && (a.flags & 2))) {
                 const bool up2 = !(do_l && j < n_pages);
                 const int q2 = up2 ? j - gq_u : j;
                 const uint32_t pb2 = up2 ? sw_page_bytes(K, true) : sw_page_bytes(K, false);
@@ -355,7 +426,7 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
         // compute threads read with a plain load (a try_wait per thread and page cost ~400 cycles per level)
         for (int i = 0; i < total; ++i) {
             sw_mbar_wait(&full[i & smask], (uint32_t)((i / S) & 1));
-            sw_st_progress(landed, i + 1);
+            sw_st_landed(landed, i + 1);
         }
     } else if (tid >= ncomp + 64) {
         // ------------------------------------------------------------ writers: warp w takes pages w, w + 3, ...
@@ -387,7 +458,7 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(const SweepArgs a) {
                 double *dst = to_tmp ? a.tmp : a.out;     // tmp: U schedule position of the row; out: the row
 #pragma unroll
                 for (int u = 0; u < P / 32; ++u)
-                    if (u * 32 + lane < rows && !(a.flags & 1)) dst[id[u]] = x[u];
+                    if (u * 32 + lane < rows && !(DBG && (a.flags & 1))) dst[id[u]] = x[u];
                 __syncwarp();
                 if (lane == 0) sw_mbar_arrive(&empty[s]);
             }
@@ -522,24 +593,33 @@ extern "C" int ddilu_sweep_rhs(int npad, const int *rowof, const int *row_ptr, c
 
 namespace {
 long long *g_sweep_dbg = nullptr;
-int g_sweep_wsleep = 20, g_sweep_flags = 0;
-template <int K, int R>
-int launch_sweep_kr(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
+int g_sweep_wsleep = 100, g_sweep_flags = 0;
+template <int K, int R, int MAXT, bool DBG>
+int launch_sweep_one(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
     static size_t attr = 0;     // monotone: the largest dynamic shared-memory size requested so far
     if (attr < smem) {
-        DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R, MAXT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
         attr = smem;
     }
-    sweep_kernel<K, R><<<n_blocks, a.sets * a.nct + SW_HELPERS, smem, st>>>(a);
+    sweep_kernel<K, R, MAXT, DBG><<<n_blocks, a.sets * a.nct + SW_HELPERS, smem, st>>>(a);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
+}
+template <int K, int R>
+int launch_sweep_kr(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
+    const int threads = a.sets * a.nct + SW_HELPERS;      // register budget follows the CTA size
+#ifdef DDILU_EXPERIMENTS
+    if (a.dbg || a.flags) return launch_sweep_one<K, R, 1024, true>(n_blocks, a, smem, st);
+#endif
+    if (threads <= 768) return launch_sweep_one<K, R, 768, false>(n_blocks, a, smem, st);
+    return launch_sweep_one<K, R, 1024, false>(n_blocks, a, smem, st);
 }
 template <int K>
 int launch_sweep(int rows_per_thread, int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
     switch (rows_per_thread) {
         case 1: return launch_sweep_kr<K, 1>(n_blocks, a, smem, st);
         case 2: return launch_sweep_kr<K, 2>(n_blocks, a, smem, st);
-        case 4: return launch_sweep_kr<K, 4>(n_blocks, a, smem, st);
         default: return DDILU_ERR_ARG;
     }
 }

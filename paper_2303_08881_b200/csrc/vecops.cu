@@ -333,6 +333,70 @@ __global__ void __launch_bounds__(VEC_THREADS) scatter_kernel(long long n, const
         dst[idx[i]] = src[i];
 }
 
+// The host arithmetic of `fixed_gmres` (krylov.py:233-268) for the few-step inner solve, on the device so that a
+// preconditioner application needs no host read: Givens rotations on the Hessenberg columns, back substitution,
+// coefficients of the basis combination.  H row j = [h_0j .. h_jj, |w_j|^2] (stride ldh), *bbp = <b, b>.
+// Same operations in the same order as the host code (products rounded: -fmad=false; IEEE sqrt and division;
+// hypot may differ from CPython's by an ulp).  Any early exit of the reference (zero right-hand side, happy
+// breakdown before the last step) and any non-finite number raises *flag: the caller redoes the application step
+// by step on the host path.
+constexpr int SMALL_GMRES_MAX = 8;
+__global__ void gmres_small_solve_kernel(int m, const double *__restrict__ H, int ldh, const double *__restrict__ bbp,
+                                         double happy_tol, double *__restrict__ coef, int *flag) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double h[SMALL_GMRES_MAX + 1][SMALL_GMRES_MAX], cs[SMALL_GMRES_MAX], sn[SMALL_GMRES_MAX], g[SMALL_GMRES_MAX + 1],
+        y[SMALL_GMRES_MAX];
+    for (int i = 0; i <= m; ++i) {
+        g[i] = 0.0;
+        for (int j = 0; j < m; ++j) h[i][j] = 0.0;
+    }
+    for (int j = 0; j < m; ++j) coef[j] = 0.0;
+    const double bb = *bbp;
+    const double beta = sqrt(bb);
+    bool bad = !(beta > 0.0) || !isfinite(beta);
+    g[0] = beta;
+    int k = 0;
+    for (int j = 0; j < m && !bad; ++j) {
+        const double *col = H + (long long)j * ldh;
+        for (int i = 0; i <= j; ++i) h[i][j] = col[i];
+        const double w2 = col[j + 1];
+        const double hnext = w2 > 0.0 ? sqrt(w2) : 0.0;
+        h[j + 1][j] = hnext;
+        for (int i = 0; i < j; ++i) {                       // krylov.py:137-140
+            const double t = cs[i] * h[i][j] + sn[i] * h[i + 1][j];
+            h[i + 1][j] = -sn[i] * h[i][j] + cs[i] * h[i + 1][j];
+            h[i][j] = t;
+        }
+        const double denom = hypot(h[j][j], hnext);         // krylov.py:141
+        if (denom == 0.0) {
+            cs[j] = 1.0;
+            sn[j] = 0.0;
+        } else {
+            cs[j] = h[j][j] / denom;
+            sn[j] = hnext / denom;
+        }
+        h[j][j] = cs[j] * h[j][j] + sn[j] * hnext;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        k = j + 1;
+        if (!isfinite(w2) || !isfinite(h[j][j])) bad = true;
+        if (hnext < happy_tol) {
+            if (j + 1 < m) bad = true;                      // the queued steps behind a breakdown divided by ~0
+            break;
+        }
+    }
+    if (bad) {
+        atomicExch(flag, 1);
+        return;
+    }
+    for (int i = k - 1; i >= 0; --i) {                      // krylov.py:86-93
+        double s = g[i];
+        for (int j = i + 1; j < k; ++j) s -= h[i][j] * y[j];
+        y[i] = h[i][i] != 0.0 ? s / h[i][i] : 0.0;
+    }
+    for (int i = 0; i < k; ++i) coef[i] = y[i];
+}
+
 static int red_grid(long long n) {
     int g = stream_grid(n, VEC_THREADS, 4, 4);
     return g > RED_MAX_BLOCKS ? RED_MAX_BLOCKS : g;
@@ -428,6 +492,16 @@ extern "C" int ddilu_multi_axpy(long long n, int k, const double *basis, long lo
     if (n <= 0 || k < 0) return DDILU_OK;
     multi_axpy_kernel<<<stream_grid(n, VEC_THREADS, 2), VEC_THREADS, sizeof(double) * (k > 0 ? k : 1),
                         (cudaStream_t)stream>>>(n, k, basis, ld, coef, x, overwrite);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+extern "C" int ddilu_gmres_small_max(void) { return SMALL_GMRES_MAX; }
+
+extern "C" int ddilu_gmres_small_solve(int m, const double *H, int ldh, const double *bb, double happy_tol,
+                                       double *coef, int *flag, void *stream) {
+    if (m < 1 || m > SMALL_GMRES_MAX || ldh < m + 2) return DDILU_ERR_ARG;
+    gmres_small_solve_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(m, H, ldh, bb, happy_tol, coef, flag);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -628,7 +628,7 @@ SWEEP_MAX_AVG_WIDTH = 512      # average rows per level of a block up to which o
 SWEEP_SMEM_BUDGET = 200 * 1024
 SWEEP_MAX_LEVELS = 6144        # level table of a block in shared memory (L + U)
 SWEEP_MAX_THREADS = 416        # compute threads per set (wider levels loop)
-SWEEP_ROWS_PER_THREAD = 1      # rows of a level per thread (1, 2, 4); measured at 256^3 / 128^3: 1 row, 3 sets is the fastest shape
+SWEEP_ROWS_PER_THREAD = 1      # rows of a level per thread (1, 2); measured at 256^3 / 128^3: 1 row, 3 sets is the fastest shape
 SWEEP_SETS = 3                 # compute sets taking the levels in turn (2, 3)
 
 

@@ -178,16 +178,20 @@ class Arnoldi:
 
 DevOp = Callable[[torch.Tensor, torch.Tensor], None]  # op(x, out): out[:n] = Op x[:n]
 
+DEVICE_COEF = os.environ.get("DDILU_DEVICE_COEF", "1") == "1"   # inner GMRES: rotations / back substitution on the device (no host read per application)
 L2_PERSIST_W = False  # pin the Arnoldi work vector in the persisting part of L2 during a solve (measured: slower)
 MGS_BLOCK = int(os.environ.get("DDILU_MGS_BLOCK", "4"))  # basis vectors per pass of the blocked Gram-Schmidt (1: the vector-by-vector launches)
 ALTERNATE_MGS = True  # consecutive MGS steps traverse the vectors in alternating directions (L2 reuse)
 
 
 def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Tensor, x0: torch.Tensor | None,
-                     cfg: KrylovConfig, flexible: bool, comm: Comm, pad: int = 0):
+                     cfg: KrylovConfig, flexible: bool, comm: Comm, pad: int = 0, guard=None):
     """krylov.py:96-179 on device vectors of local length n.  Vectors handed to
     `apply_a` have `pad` extra trailing entries (halo landing zone).  Returns
-    (x[:n] device tensor, SolveReport)."""
+    (x[:n] device tensor, SolveReport).  guard: the preconditioner object when its applications run without
+    host reads (device-side inner-solve arithmetic, CUDA-graph replay); guard.cycle_failed() is asked once per
+    restart cycle whether an application hit one of the reference's early exits, and the cycle is then redone
+    on the host-read path (guard.set_safe)."""
     m = cfg.restart
     ws = Arnoldi(n, m, comm, flexible, pad)
     V, Z, w = ws.V, ws.Z, ws.w
@@ -240,6 +244,13 @@ def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Ten
             ws.normalise_into(j)
             if est <= cfg.rtol or its >= cfg.max_iters:
                 break
+        if guard is not None and guard.cycle_failed():
+            # an inner solve of this cycle left the reference's loop early (zero right-hand side, happy
+            # breakdown): x and r are untouched so far -- redo the cycle with a host read per application
+            guard.set_safe(True)
+            its -= k
+            del history[len(history) - k:]
+            continue
         y = _back_substitute(h, g, k)
         if flexible:
             ws.combine(Z, y, x, overwrite=False)
@@ -247,6 +258,9 @@ def restarted_device(n: int, apply_a: DevOp, apply_m: DevOp | None, b: torch.Ten
             ws.combine(V, y, w, overwrite=True)
             if apply_m is not None:
                 apply_m(w, u)
+                if guard is not None and guard.cycle_failed():
+                    guard.set_safe(True)
+                    apply_m(w, u)
                 D.axpy(n, 1.0, u, x)
             else:
                 D.axpy(n, 1.0, w, x)
@@ -279,6 +293,8 @@ class InnerGmres:
         self.z = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
         self.u = torch.empty(self.ws.ld, dtype=D.F64, device=D.dev())
         self.hcols = None   # device Hessenberg columns of one solve: row j = [h_0j .. h_jj, |w|^2], last row = <b, b>
+        self.flag = D.zeros_i32(1)   # sticky: a device-side solve met an early exit of the reference
+        self.safe = False            # True: host read per solve (the reference's control flow, step by step if needed)
 
     def solve(self, apply_a: DevOp, b: torch.Tensor, out: torch.Tensor, apply_m: DevOp | None = None,
               n_global: int | None = None):
@@ -310,6 +326,16 @@ class InnerGmres:
                 apply_a(V[j], w)
             ws.mgs(j, H[j])
             ws.normalise_into(j, H[j])
+        if DEVICE_COEF and not self.safe and m <= D.query("ddilu_gmres_small_max"):
+            # rotations + back substitution on the device: nothing is read back; an early exit of the
+            # reference raises self.flag and the caller redoes the application with safe = True
+            D.call("ddilu_gmres_small_solve", m, H, H.stride(0), bb, float(self.happy_tol), ws.coef, self.flag)
+            if apply_m is not None:
+                D.multi_axpy(n, m, V, ws.ld, ws.coef, self.u, True)
+                apply_m(self.u, out)
+            else:
+                D.multi_axpy(n, m, V, ws.ld, ws.coef, out, True)
+            return out
         host = H.cpu().numpy()                   # the one synchronisation of the inner solve
         beta = math.sqrt(float(host[self.m, 0]))
         if beta == 0.0:

@@ -17,6 +17,7 @@ from those combined factors on demand.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -308,6 +309,7 @@ class _DDPrecond:
         self.system = LocalSystem(a, layout, use_rcm)
         self._a = a
         self._domains = None
+        self._graph = None
         s = self.system
         self._r = D.empty_f64(max(1, s.n_loc))
         self._z = D.empty_f64(max(1, s.n_loc + s.n_halo))
@@ -323,6 +325,31 @@ class _DDPrecond:
     def apply_local(self, r: torch.Tensor, z: torch.Tensor):
         raise NotImplementedError
 
+    # applications without host reads ------------------------------------
+    def _inner_solvers(self):
+        inner = getattr(self, "_inner", None)
+        return [inner] if inner is not None else []
+
+    def cycle_failed(self) -> bool:
+        """Did a device-side inner solve since the last call meet an early exit of the reference (one host read)?"""
+        failed = False
+        for inner in self._inner_solvers():
+            if not inner.safe and int(inner.flag.item()):
+                inner.flag.zero_()
+                failed = True
+        return failed
+
+    def set_safe(self, on: bool):
+        for inner in self._inner_solvers():
+            inner.safe = on            # (the graphed application checks it and runs the plain method while set)
+
+    def graphed_apply(self):
+        """apply_local replayed from a CUDA graph when the problem is small enough to be launch-bound (one
+        rank, no profiling hooks); the plain method otherwise."""
+        if self._graph is None:
+            self._graph = _GraphedApply(self)
+        return self._graph
+
     def apply(self, r):
         """z = M^-1 r in the ORIGINAL ordering (precond.py:187, 251, 368).  numpy in ->
         numpy out; a CUDA tensor in -> a CUDA tensor out."""
@@ -331,6 +358,10 @@ class _DDPrecond:
         rd = r if on_device else D.to_device_f64(np.asarray(r, dtype=np.float64))
         D.gather(s.n_loc, s.nodes, rd, self._r)
         self.apply_local(self._r, self._z)
+        if self.cycle_failed():                    # early exit of an inner solve: the reference's own control flow
+            self.set_safe(True)
+            self.apply_local(self._r, self._z)
+            self.set_safe(False)
         z = torch.zeros(self.layout.n, dtype=D.F64, device=D.dev()) if s.comm.active \
             else torch.empty(self.layout.n, dtype=D.F64, device=D.dev())
         D.scatter(s.n_loc, s.nodes, self._z, z)
@@ -363,12 +394,77 @@ class _DDPrecond:
             x0_loc = D.empty_f64(max(1, s.n_loc))
             x0d = x0 if isinstance(x0, torch.Tensor) else D.to_device_f64(np.asarray(x0, dtype=np.float64))
             D.gather(s.n_loc, s.nodes, x0d, x0_loc)
-        x_loc, report = restarted_device(s.n_loc, s.spmv, self.apply_local, b_loc, x0_loc, cfg, flexible, s.comm,
-                                         pad=s.n_halo)
+        guard = self if self._inner_solvers() else None
+        try:
+            x_loc, report = restarted_device(s.n_loc, s.spmv, self.graphed_apply(), b_loc, x0_loc, cfg, flexible,
+                                             s.comm, pad=s.n_halo, guard=guard)
+        finally:
+            if guard is not None:
+                self.set_safe(False)
         x = torch.zeros(n, dtype=D.F64, device=D.dev()) if s.comm.active else D.empty_f64(n)
         D.scatter(s.n_loc, s.nodes, x_loc, x)
         s.comm.allreduce_sum_(x)
         return (x if on_device else x.cpu().numpy()), report
+
+
+# Off by default: measured on B200, the stream already runs ahead of the GPU down to 128^3 (the solve is bound by
+# kernel latencies, not by launches: 0.174 s either way), and a fresh capture per preconditioner costs 20-50 ms;
+# it pays for many solves with ONE preconditioner on small problems (64^3: 0.060 -> 0.052 s per solve).
+GRAPH_APPLY = os.environ.get("DDILU_GRAPHS", "0") == "1"
+GRAPH_MAX_ROWS = 6_000_000      # above this a step is GPU-bound (98 % busy at 16.8 M rows): replaying buys nothing
+GRAPH_WARMUP = 2                # eager applications before the capture (lazy workspaces, kernel attributes)
+
+
+class _GraphedApply:
+    """`apply_local(r, z)` captured once into a CUDA graph on fixed buffers and replayed: an application of a
+    two-level preconditioner is 30-60 small launches, which at <= 128^3 rows per GPU cost more host time than
+    GPU time.  Needs an application without host reads (device-side inner-solve arithmetic, krylov.DEVICE_COEF)
+    and a single rank; anything else, and any capture failure, falls back to the plain method."""
+
+    def __init__(self, owner):
+        s = owner.system
+        self.owner = owner
+        self.n = s.n_loc
+        self.enabled = (GRAPH_APPLY and not s.comm.active and 0 < s.n_loc <= GRAPH_MAX_ROWS
+                        and all(not i.safe for i in owner._inner_solvers()))
+        self.calls = 0
+        self.graph = None
+        self.r = self.z = None
+
+    def __call__(self, r, z):
+        from . import _lib
+        from . import krylov
+        owner = self.owner
+        if (not self.enabled or _lib.profile is not None or not krylov.DEVICE_COEF
+                or any(i.safe for i in owner._inner_solvers())):
+            return owner.apply_local(r, z)
+        n = self.n
+        if self.graph is None:
+            self.calls += 1
+            if self.calls <= GRAPH_WARMUP:
+                return owner.apply_local(r, z)
+            s = owner.system
+            self.r = D.empty_f64(n)
+            self.z = D.empty_f64(n + s.n_halo)
+            self.r.copy_(r[:n])
+            try:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    owner.apply_local(self.r, self.z)
+                self.graph = g
+            except Exception:
+                self.enabled = False
+                try:
+                    torch.cuda.synchronize()
+                except Exception:
+                    pass
+                return owner.apply_local(r, z)
+        else:
+            self.r.copy_(r[:n])
+        self.graph.replay()
+        z[:n].copy_(self.z[:n])
+        return z
 
 
 class BjIluPrecond(_DDPrecond):

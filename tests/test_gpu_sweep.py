@@ -34,7 +34,7 @@ CASES = [((20, 20, 20), 8, "schur"), ((24, 17, 9), 4, "schur"), ((40, 40), 4, "s
 
 
 @pytest.mark.parametrize("dims,p,pc", CASES)
-@pytest.mark.parametrize("max_threads,rpt,sets", [(416, 1, 3), (32, 1, 2), (256, 4, 3), (64, 2, 2)])
+@pytest.mark.parametrize("max_threads,rpt,sets", [(416, 1, 3), (32, 1, 2), (256, 2, 3), (64, 2, 2)])
 def test_sweep_solves_bit_exact(P, orc, dims, p, pc, max_threads, rpt, sets):
     """L, U and the fused U^-1 L^-1 against the oracle, for the thread shapes of the kernel (rows per thread,
     two or three sets); max_threads = 32 / 64 forces the loop behind the prefetched rows on the wide levels."""
