@@ -90,6 +90,26 @@ int ddilu_lattice_set_debug(long long *buf);
 int ddilu_sptrsv_lattice(int n_tiles, const void *tab, const unsigned char *blob, int *flags, int n_slots,
                          int has_diag, int blkmax, int tmax, int xemax, const double *b, double *x, void *stream);
 
+/* ---- tile sweep (csrc/experiments/tsweep.cu; measured, not adopted: DESIGN.md 5.7): sparse.py:228-272 for the INTERIOR factors of a structured problem, with
+ * right-hand side and solution kept in TILE ORDER (tiles one after the other, padded to whole 256-row pages with
+ * zeros, rows of a tile in level-major order of the L factor; the U factor walks the reverse order).  Pages of
+ * operands and vector slices arrive by TMA, results leave by bulk stores, boundary values of neighbour tiles are
+ * gathered one tile ahead; persistent CTAs of a cooperative launch take the tiles in a topological order.
+ * ddilu_tsweep_fill: operands into pages (gpos / lpos = padded global / tile-local position of every row in the
+ * factor's own position space, ecode[k] = boundary slot of entry k or -1).  ddilu_tsweep_permute: a vector
+ * between row order and tile order.  ddilu_tsweep_solve: tiles = 16 ints per tile in schedule order {rows, first
+ * page, levels, offset into levtab, boundary values, offset into extpos, producer tiles, offset into prods, pad
+ * rows in front (U), 0 ...}; flags = one int per tile (scratch). */
+long long ddilu_tsweep_page_bytes(int k, int upper);
+long long ddilu_tsweep_smem_bytes(int k, int upper, int stages, int window, int xe_cap, int max_lev);
+int ddilu_tsweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
+                      const int *gpos, const int *lpos, const int *ecode, int window, unsigned char *pages,
+                      int *bad_row, void *stream);
+int ddilu_tsweep_permute(int n, const int *pos, const double *in, double *out, int to_tile, void *stream);
+int ddilu_tsweep_solve(int n_tiles, const int *tiles, const int *levtab, const int *extpos, const int *prods,
+                       const unsigned char *pages, int *flags, int k, int upper, int window, int xe_cap, int max_lev,
+                       int stages, int sets, int nct, const double *b, double *x, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

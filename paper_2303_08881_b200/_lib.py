@@ -113,6 +113,11 @@ SIGNATURES = {
 # entries that exist only in a -DDDILU_EXPERIMENTS build (include/ddilu_b200_experiments.h): measured-slower
 # alternative kernels, tuning knobs, diagnostics.  Bound when the library has them.
 EXPERIMENT_SIGNATURES = {
+    "ddilu_tsweep_page_bytes": (_L, [_I, _I]),
+    "ddilu_tsweep_smem_bytes": (_L, [_I, _I, _I, _I, _I, _I]),
+    "ddilu_tsweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
+    "ddilu_tsweep_permute": (_I, [_I, _P, _P, _P, _I, _P]),
+    "ddilu_tsweep_solve": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_set_tuning": (_I, [_S, _I]),
     "ddilu_blocklocal_table": (_I, [_I, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_blocklocal": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),

@@ -320,8 +320,8 @@ def slab_tile_keys(nodes: torch.Tensor | None, n: int, dims, tdims2, lev: torch.
     return keys[:n], int(nk.value)
 
 
-def tile_partition(keys: torch.Tensor, key_range: int) -> TilePartition | None:
-    """Compact the keys into tile ids; None if a tile would exceed TILE_MAX_ROWS."""
+def tile_partition(keys: torch.Tensor, key_range: int, max_tile_rows: int | None = None) -> TilePartition | None:
+    """Compact the keys into tile ids; None if a tile would exceed max_tile_rows (default TILE_MAX_ROWS)."""
     n = keys.numel()
     if n == 0:
         return None
@@ -335,7 +335,7 @@ def tile_partition(keys: torch.Tensor, key_range: int) -> TilePartition | None:
     tile_of, tpos, tile_ptr = empty_i32(n), empty_i32(n), empty_i32(n_tiles + 1)
     call("ddilu_tile_assign", n, keys, flags, rows, tile_of, tpos, tile_ptr)
     max_rows = int((tile_ptr[1:] - tile_ptr[:-1]).max().item())
-    if max_rows > TILE_MAX_ROWS:
+    if max_rows > (TILE_MAX_ROWS if max_tile_rows is None else max_tile_rows):
         return None
     return TilePartition(n, n_tiles, tile_of, tpos, tile_ptr, rows, max_rows)
 
@@ -779,6 +779,202 @@ def sweep_solve(sp: SweepPlan, phases: int, out: torch.Tensor, add: bool = False
     call("ddilu_sweep_solve", sp.n_blocks, sp.blocks, sp.levtab, sp.pages_l, sp.pages_u, sp.k, sp.window, sp.stages,
          sp.sets, sp.nct, sp.rpt, sp.max_lev, phases, sp.rhs, sp.tmp, out, sp.addbuf if add else None)
     return out
+
+
+# ---------------------------------------------------------------------------
+# tile sweep (csrc/experiments/tsweep.cu): interior factors with vectors in tile order.  EXPERIMENT (needs a
+# DDILU_EXPERIMENTS=1 build; scripts/probe_tsweep.py): bit-exact, 0.62-0.66 of the HBM roofline when the tiles
+# are made independent, but 0.30 / 0.42 (L / U) with the real tile dependencies -- 16^3 tiles leave ~190 tiles
+# per tile level for ~300 resident CTAs and every tile level costs a whole tile time; not integrated.
+
+USE_TSWEEP = os.environ.get("DDILU_TSWEEP", "1") == "1"
+TSWEEP_TILE_3D = (16, 16, 16)
+TSWEEP_SETS = 3
+TSWEEP_MAX_THREADS = 192       # compute threads per set
+TSWEEP_STAGES = 4
+TSWEEP_SMEM_BUDGET = 110 * 1024     # two CTAs per SM
+
+
+@dataclass
+class TileSweepHalf:
+    """One factor (L or U) of a tile-sweep plan."""
+
+    n_tiles: int
+    tiles: torch.Tensor        # int32[n_tiles * 16], schedule order
+    levtab: torch.Tensor
+    extpos: torch.Tensor
+    prods: torch.Tensor
+    pages: torch.Tensor
+    flags: torch.Tensor
+    k: int
+    window: int
+    xe_cap: int
+    max_lev: int
+    stages: int
+    nct: int
+    n_tile_levels: int
+
+
+@dataclass
+class TileSweepPlan:
+    """Tile-order layout of an interior factor pair: vpos[row] = position of a row in the tile-ordered vectors
+    (tiles padded to whole pages), npad = length of those vectors."""
+
+    n: int
+    npad: int
+    vpos: torch.Tensor         # int32[n]
+    lower: TileSweepHalf
+    upper: TileSweepHalf
+    bad_row: int
+    sets: int
+
+
+def build_tsweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l: int, lev_u: torch.Tensor,
+                 nlev_u: int, part: TilePartition) -> "TileSweepPlan | None":
+    """Tile-sweep plan of the factor pair on the tile partition `part` (large box tiles); None when the pair does
+    not qualify: cyclic tile graph, U not walking the reverse of L's order inside a tile, more than 8
+    dependencies per row, window / boundary buffers too large."""
+    n = lower.n_rows
+    if not USE_TSWEEP or not _lib.has_experiments() or part is None or n == 0 or part.n != n:
+        return None
+    P = 256
+    d = dev()
+    i64 = torch.int64
+    nt = part.n_tiles
+    tile = part.tile_of.to(i64)
+    rows = torch.arange(n, dtype=i64, device=d)
+    tptr = part.tile_ptr.to(i64)
+    sizes = tptr[1:] - tptr[:-1]
+    n_pages_t = (sizes + P - 1) // P
+    page0_t = torch.cumsum(n_pages_t, 0) - n_pages_t
+    tpad = n_pages_t * P
+    n_pages = int(n_pages_t.sum().item())
+    ll, lu = lev_l[:n].to(i64), lev_u[:n].to(i64)
+    order = torch.argsort(tile * nlev_l + ll, stable=True)
+    lpos = torch.empty(n, dtype=i64, device=d)
+    lpos[order] = rows - tptr[tile[order]]
+    # U must walk the reverse order: along L's order the U level never increases inside a tile
+    to, uo = tile[order], lu[order]
+    same = to[1:] == to[:-1]
+    if bool(((uo[1:] > uo[:-1]) & same).any().item()):
+        return None
+    upos = tpad[tile] - 1 - lpos
+    vpos = page0_t[tile] * P + lpos
+    kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
+    ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
+    kmax = max(kl, ku, 1)
+    k = next((c for c in (2, 3, 4, 8) if kmax <= c), None)
+    if k is None:
+        return None
+    bad = torch.full((1,), INT_MAX, dtype=I32, device=d)
+    halves = []
+    for fac, lev, nlev, up, pos in ((lower, ll, nlev_l, False, lpos), (upper, lu, nlev_u, True, upos)):
+        sched = tile_schedule(fac, part, up)
+        if sched is None:
+            return None
+        tsched, n_tile_levels = sched
+        tsched = tsched.to(i64)
+        ord_of_tile = torch.empty(nt, dtype=i64, device=d)
+        ord_of_tile[tsched] = torch.arange(nt, dtype=i64, device=d)
+        front = (tpad - sizes) if up else torch.zeros_like(sizes)
+        key = tile * nlev + lev
+        cnt = torch.bincount(key, minlength=nt * nlev).view(nt, nlev)
+        nz = cnt > 0
+        nlev_t = nz.sum(1)
+        lev_end = torch.cumsum(cnt, 1) + front[:, None]        # end position of (tile, level) in the own space
+        max_lev = int(nlev_t.max().item())
+        width_max = int(cnt.max().item())
+        # entries
+        nnz = fac.nnz
+        rlen = (fac.rp[1:] - fac.rp[:-1]).to(i64)
+        erow = torch.repeat_interleave(rows, rlen)
+        ecol = fac.ci[:nnz].to(i64)
+        dep = ecol != erow
+        cross = dep & (tile[ecol] != tile[erow])
+        inner = dep & ~cross
+        row_end = lev_end.reshape(-1)[key]
+        need = torch.where(inner, row_end[erow] - pos[ecol], torch.zeros_like(ecol))
+        max_need = int(need.max().item()) if nnz else 1
+        window = 32
+        while window < max_need:
+            window <<= 1
+        # boundary dependencies: one slot per cross-tile entry, numbered inside the reader's tile
+        cidx = torch.nonzero(cross).flatten()
+        ct = tile[erow[cidx]]
+        o2 = torch.argsort(ct, stable=True)
+        cidx, ct = cidx[o2], ct[o2]
+        n_ext_t = torch.bincount(ct, minlength=nt)
+        ext_first = torch.cumsum(n_ext_t, 0) - n_ext_t
+        eidx = torch.arange(cidx.numel(), dtype=i64, device=d) - ext_first[ct]
+        xe_cap = int(n_ext_t.max().item()) if cidx.numel() else 0
+        xe_cap = (xe_cap + 1) & ~1
+        if window > 8192 or window + 2 + xe_cap > 65535:
+            return None
+        ecode = torch.full((max(nnz, 1),), -1, dtype=I32, device=d)
+        ecode[cidx] = (window + 1 + eidx).to(I32)
+        # the boundary lists are stored tile by tile in SCHEDULE order
+        sizes_s = n_ext_t[tsched]
+        ext_off_s = torch.cumsum(sizes_s, 0) - sizes_s
+        ext_off_t = torch.empty(nt, dtype=i64, device=d)
+        ext_off_t[tsched] = ext_off_s
+        extpos = torch.empty(max(cidx.numel(), 1), dtype=I32, device=d)
+        extpos[(ext_off_t[ct] + eidx)] = vpos[ecol[cidx]].to(I32)
+        # producer tiles
+        pk = torch.unique(ct * nt + tile[ecol[cidx]])
+        pt, pj = pk // nt, pk % nt
+        n_prod_t = torch.bincount(pt, minlength=nt)
+        prod_first = torch.cumsum(n_prod_t, 0) - n_prod_t
+        pidx = torch.arange(pk.numel(), dtype=i64, device=d) - prod_first[pt]
+        psz_s = n_prod_t[tsched]
+        prod_off_s = torch.cumsum(psz_s, 0) - psz_s
+        prod_off_t = torch.empty(nt, dtype=i64, device=d)
+        prod_off_t[tsched] = prod_off_s
+        prods = torch.empty(max(pk.numel(), 1), dtype=I32, device=d)
+        prods[(prod_off_t[pt] + pidx)] = ord_of_tile[pj].to(I32)
+        # level tables tile by tile in schedule order
+        lsz_s = nlev_t[tsched]
+        lev_off_s = torch.cumsum(lsz_s, 0) - lsz_s
+        lev_off_t = torch.empty(nt, dtype=i64, device=d)
+        lev_off_t[tsched] = lev_off_s
+        tl = torch.repeat_interleave(torch.arange(nt, dtype=i64, device=d), nlev_t)      # tile of each table entry
+        within = torch.arange(tl.numel(), dtype=i64, device=d) - (torch.cumsum(nlev_t, 0) - nlev_t)[tl]
+        levtab = torch.empty(max(tl.numel(), 1), dtype=I32, device=d)
+        levtab[lev_off_t[tl] + within] = lev_end[nz].to(I32)
+        hdr = torch.zeros((nt, 16), dtype=i64, device=d)
+        for col, v in enumerate((sizes, page0_t, nlev_t, lev_off_t, n_ext_t, ext_off_t, n_prod_t, prod_off_t, front)):
+            hdr[:, col] = v
+        if os.environ.get("DDILU_TSWEEP_NODEPS") == "1":    # timing experiment only (wrong results): no producer waits
+            hdr[:, 6] = 0
+        hdr = hdr[tsched].to(I32).contiguous().view(-1)
+        nct = min(TSWEEP_MAX_THREADS, max(32, (width_max + 31) & ~31))
+        stages = TSWEEP_STAGES
+        if query("ddilu_tsweep_smem_bytes", k, int(up), stages, window, xe_cap, max_lev) > TSWEEP_SMEM_BUDGET:
+            stages = 2
+            if query("ddilu_tsweep_smem_bytes", k, int(up), stages, window, xe_cap, max_lev) > 220 * 1024:
+                return None
+        pages = torch.zeros(n_pages * query("ddilu_tsweep_page_bytes", k, int(up)), dtype=torch.uint8, device=d)
+        gpos = (page0_t[tile] * P + pos).to(I32).contiguous()
+        call("ddilu_tsweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos, pos.to(I32).contiguous(), ecode,
+             window, pages, bad)
+        halves.append(TileSweepHalf(nt, hdr, levtab, extpos, prods, pages, zeros_i32(nt), k, window, xe_cap, max_lev,
+                                    stages, nct, n_tile_levels))
+    return TileSweepPlan(n, n_pages * P, vpos.to(I32).contiguous(), halves[0], halves[1], int(bad.item()), TSWEEP_SETS)
+
+
+def tsweep_solve(tp: TileSweepPlan, upper: bool, b_tile: torch.Tensor, x_tile: torch.Tensor, check: bool = False):
+    """x = L^-1 b (or U^-1 b) with both vectors in tile order (tp.npad entries, pads 0)."""
+    if check and upper and tp.bad_row != INT_MAX:
+        raise TriSolveError(f"zero or missing diagonal at row {tp.bad_row}")
+    h = tp.upper if upper else tp.lower
+    call("ddilu_tsweep_solve", h.n_tiles, h.tiles, h.levtab, h.extpos, h.prods, h.pages, h.flags, h.k, int(upper),
+         h.window, h.xe_cap, h.max_lev, h.stages, tp.sets, h.nct, b_tile, x_tile)
+    return x_tile
+
+
+def tsweep_permute(tp: TileSweepPlan, src: torch.Tensor, dst: torch.Tensor, to_tile: bool):
+    """Row order -> tile order (dst must be zero at the pads) or back."""
+    call("ddilu_tsweep_permute", tp.n, tp.vpos, src, dst, int(to_tile))
+    return dst
 
 
 def enable_block_local(sched: Schedule, seg_ptr) -> bool:

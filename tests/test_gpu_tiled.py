@@ -289,3 +289,38 @@ def test_lattice_refuses_wide_rows(P):
     b = P.default_rhs(a)
     x, rep = P.fgmres(a, b, m=m.apply)
     assert rep.converged
+
+
+@pytest.mark.parametrize("dims,p,tile", [((40, 37, 29), 8, (16, 16, 16)), ((33, 33, 33), 1, (16, 16, 16)),
+                                         ((36, 36, 36), 8, (8, 8, 8))])
+def test_tile_sweep_bit_exact(P, orc, dims, p, tile, experiments):
+    """csrc/experiments/tsweep.cu (vectors in tile order, U walking L's order backwards, boundary values gathered a
+    tile ahead): bit-exact against the oracle's serial solves through explicit permutations; pads stay zero."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    a = P.aniso3d(*dims)
+    layout = P.classify_and_order(a, P.partition(a, p, dims), p)
+    m = P.make_preconditioner("schur", a, layout)
+    s, f = m.system, m._p.interior
+    keys, nk = s._tile_keys(0, s.n_int, list(tile))
+    part = D.tile_partition(keys, nk * max(1, layout.p), max_tile_rows=tile[0] * tile[1] * tile[2])
+    tp = D.build_tsweep(f.lower, f.upper, *f._lev(False), *f._lev(True), part)
+    assert tp is not None
+    lo, up = P.CsrMatrix.from_device(f.lower), P.CsrMatrix.from_device(f.upper)
+    rng = np.random.default_rng(5)
+    for rep in range(2):
+        b = rng.standard_normal(f.n)
+        bd = D.to_device_f64(b)
+        bt, xt = D.zeros_f64(tp.npad), D.zeros_f64(tp.npad)
+        D.tsweep_permute(tp, bd, bt, True)
+        for upper, ref in ((False, orc.tri_solve_lower(orc.Csr(lo.n_rows, lo.n_cols, lo.row_ptr, lo.col_idx, lo.values), b, True)),
+                           (True, orc.tri_solve_upper(orc.Csr(up.n_rows, up.n_cols, up.row_ptr, up.col_idx, up.values), b))):
+            xt.zero_()
+            D.tsweep_solve(tp, upper, bt, xt)
+            got = D.empty_f64(f.n)
+            D.tsweep_permute(tp, xt, got, False)
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy(), ref), ("U" if upper else "L", rep)
+            pads = torch.ones(tp.npad, dtype=torch.bool, device="cuda")
+            pads[tp.vpos.long()] = False
+            assert float(xt[pads].abs().sum().item()) == 0.0
