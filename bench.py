@@ -468,7 +468,9 @@ def relaunch_under_torchrun(args):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+    # (torchrun's own parser would take a bare "--n" for an abbreviation of --nnodes / --nproc-per-node)
+    cmd += ["--grid" if a == "--n" else a for a in sys.argv[1:]]
     raise SystemExit(subprocess.call(cmd))
 
 
@@ -478,7 +480,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--n", type=int, default=256, help="grid points per axis")
+    ap.add_argument("--n", "--grid", dest="n", type=int, default=256, help="grid points per axis")
     ap.add_argument("--precond", default="schur", choices=("bj", "schur", "rap", "rap-milu"))
     ap.add_argument("--fill", default="ilu0")
     ap.add_argument("--domains", type=int, default=P_DOMAINS)
