@@ -728,7 +728,9 @@ def build_sweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l:
         if query("ddilu_sweep_smem_bytes", k, st, window, max_lev) <= SWEEP_SMEM_BUDGET:
             stages = st
             break
-    if stages < 4 or width_max > (stages - 2) * P:
+    # ring residency: the sets work on up to `sets` consecutive levels at once and a page is freed only when the
+    # progress counter (start of the level being executed) has passed it -- all pages of those levels must fit
+    if stages < 4 or sets * width_max > (stages - 2) * P:
         return None
     # level tables: per block its L levels then its U levels
     lev_off = torch.cumsum(nlev_b, 0) - nlev_b
