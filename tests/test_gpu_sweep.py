@@ -145,3 +145,32 @@ def test_sweep_refuses_unsuitable_factors(P):
     a27 = P.convdiff27(10, 10, 10)
     f27 = P.ilu0(a27).device()
     assert D.build_sweep(f27.lower, f27.upper, *f27._lev(False), *f27._lev(True), [0, f27.n]) is None
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("budget_kb,sets", [(80, 3), (80, 2), (200, 3)])
+def test_sweep_small_ring_does_not_stall(P, orc, budget_kb, sets):
+    """A 4-stage ring (small shared-memory budget) with levels that straddle pages: the residency rule of
+    `build_sweep` (all pages of the levels the sets work on at once must fit) either admits the factor and the
+    solve finishes bit-exactly, or refuses it."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    old = D.SWEEP_SMEM_BUDGET, D.SWEEP_SETS
+    D.SWEEP_SMEM_BUDGET, D.SWEEP_SETS = budget_kb * 1024, sets
+    try:
+        dims = (48, 48, 48)
+        a = P.aniso3d(*dims)
+        layout = P.classify_and_order(a, P.partition(a, 8, dims), 8)
+        m = P.make_preconditioner("schur", a, layout)
+    finally:
+        D.SWEEP_SMEM_BUDGET, D.SWEEP_SETS = old
+    f = m._p.schur
+    if f._sw is None:
+        pytest.skip("refused by the residency rule")
+    assert f._sw.stages == (4 if budget_kb == 80 else 8)
+    b = np.random.default_rng(2).standard_normal(f.n)
+    x = D.empty_f64(f.n)
+    for _ in range(3):
+        f.solve(D.to_device_f64(b), x)
+    torch.cuda.synchronize()
+    assert np.array_equal(x.cpu().numpy(), _oracle_solves(P, orc, f, b)[2])
