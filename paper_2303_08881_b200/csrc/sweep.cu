@@ -32,6 +32,8 @@
 // operands + 8 right-hand side + 8 result.
 #include <stdint.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "ddilu_b200.h"
 
@@ -597,10 +599,14 @@ int g_sweep_wsleep = 100, g_sweep_flags = 0;
 template <int K, int R, int MAXT, bool DBG>
 int launch_sweep_one(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
     static size_t attr = 0;     // monotone: the largest dynamic shared-memory size requested so far
-    if (attr < smem) {
-        DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R, MAXT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        attr = smem;
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (attr < smem) {
+            DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R, MAXT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+            attr = smem;
+        }
     }
     sweep_kernel<K, R, MAXT, DBG><<<n_blocks, a.sets * a.nct + SW_HELPERS, smem, st>>>(a);
     DDILU_LAUNCH_CHECK();

@@ -243,3 +243,50 @@ def test_graph_replay_is_used_and_survives_a_failed_cycle(P):
     finally:
         PC._GraphedApply.__call__ = orig
         PC.GRAPH_APPLY = old_flag
+
+
+def test_device_inner_solve_arithmetic_matches_the_host_code(P):
+    """ddilu_gmres_small_solve against the host functions it replaces (krylov.py:137-149 rotations, :86-93 back
+    substitution) on random Hessenberg columns: coefficients to a few ulp (hypot may differ by one), the
+    reference's early exits (zero right-hand side, happy breakdown before the last step) raise the flag."""
+    import math
+    import torch
+    from paper_2303_08881_b200 import device as D
+    from paper_2303_08881_b200 import krylov as K
+    rng = np.random.default_rng(9)
+    for m in (1, 2, 3, 5, 8):
+        for trial in range(5):
+            H = np.zeros((m + 1, m + 2))
+            for j in range(m):
+                H[j, : j + 1] = rng.standard_normal(j + 1)
+                H[j, j + 1] = rng.uniform(0.1, 2.0) ** 2          # |w_j|^2
+            H[m, 0] = rng.uniform(0.5, 3.0) ** 2                  # <b, b>
+            h = np.zeros((m + 1, m))
+            cs, sn, g = np.empty(m), np.empty(m), np.zeros(m + 1)
+            g[0] = math.sqrt(H[m, 0])
+            for j in range(m):
+                h[: j + 1, j] = H[j, : j + 1]
+                hn = math.sqrt(H[j, j + 1])
+                h[j + 1, j] = hn
+                K._givens(h, cs, sn, g, j, hn)
+            y = K._back_substitute(h, g, m)
+            Hd = torch.from_numpy(H).cuda()
+            coef = torch.zeros(m, dtype=torch.float64, device="cuda")
+            flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+            D.call("ddilu_gmres_small_solve", m, Hd, Hd.stride(0), Hd[m, 0:1], 1e-14, coef, flag)
+            assert int(flag.item()) == 0
+            assert np.allclose(coef.cpu().numpy(), y, rtol=1e-13, atol=0), (m, trial)
+    # early exits
+    m = 3
+    H = np.zeros((m + 1, m + 2))
+    H[m, 0] = 0.0
+    Hd = torch.from_numpy(H).cuda()
+    coef, flag = torch.zeros(m, dtype=torch.float64, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda")
+    D.call("ddilu_gmres_small_solve", m, Hd, Hd.stride(0), Hd[m, 0:1], 1e-14, coef, flag)
+    assert int(flag.item()) == 1                                   # beta == 0
+    H[m, 0] = 1.0
+    H[0, 0], H[0, 1] = 0.5, 0.0                                    # happy breakdown at step 0 of 3
+    Hd = torch.from_numpy(H).cuda()
+    flag.zero_()
+    D.call("ddilu_gmres_small_solve", m, Hd, Hd.stride(0), Hd[m, 0:1], 1e-14, coef, flag)
+    assert int(flag.item()) == 1
