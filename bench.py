@@ -12,11 +12,13 @@ strong scaling).  One step = one complete setup + solve.
 
 JSON line: metric / value = seconds per step (setup + solve, inputs already in
 HBM); e2e = the same through the host API with host buffers (H2D of the CSR
-arrays and b, D2H of x inside the timed region); roofline = the dominant kernel
-(sync-free SpTRSV of the interior factor) from CUDA events inside the timed
-region; cpu_baseline = the CPU oracle (port of the reference, 1 core) on a
+arrays and b, D2H of x into pinned memory inside the timed region); roofline =
+the dominant kernel (tiled SpTRSV of the interior factors L_B / U_B) from CUDA
+events inside the timed region, interface_solves = the fused block-sweep
+launches; cpu_baseline = the CPU oracle (port of the reference, 1 core) on a
 bounded sample of the same workload, scaled to the full job with the measured
-iteration count, next to the oracle's cached full-size run (its_oracle).
+iteration count, next to the oracle's cached full-size run (its_oracle; the
+bench fails when the GPU count is more than one iteration away).
 
 --impl reference runs the oracle port on the SAME configuration (256^3, not a
 sample): one measured step (about 2-4 minutes with the host threads; further
