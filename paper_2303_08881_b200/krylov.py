@@ -469,6 +469,14 @@ def fixed_gmres(apply_a, b, iters: int, apply_m=None, happy_tol: float = 1e-14) 
         return np.zeros(n)
     inner = InnerGmres(n, iters, Comm(), happy_tol=happy_tol)
     out = D.empty_f64(n)
-    inner.solve(_device_operator(apply_a, n), D.to_device_f64(b), out,
-                _device_operator(apply_m, n) if apply_m is not None else None)
+    op_a = _device_operator(apply_a, n)
+    op_m = _device_operator(apply_m, n) if apply_m is not None else None
+    bd = D.to_device_f64(b)
+    inner.solve(op_a, bd, out, op_m)
+    if not inner.safe and int(inner.flag.item()):
+        # the device-side arithmetic met one of the reference's early exits (zero right-hand side, happy
+        # breakdown): redo the solve with the reference's own control flow
+        inner.flag.zero_()
+        inner.safe = True
+        inner.solve(op_a, bd, out, op_m)
     return out.cpu().numpy()
