@@ -174,3 +174,33 @@ def test_sweep_small_ring_does_not_stall(P, orc, budget_kb, sets):
         f.solve(D.to_device_f64(b), x)
     torch.cuda.synchronize()
     assert np.array_equal(x.cpu().numpy(), _oracle_solves(P, orc, f, b)[2])
+
+
+@pytest.mark.parametrize("fill", ["iluk:1", "iluk:2", "ilut:0.001,6"])
+def test_sweep_with_longer_rows(P, orc, fill):
+    """Interface factors of fill-in rules (4 to 8 operand slots per row: the K = 4 / 8 instances of the kernel):
+    bit-exact against the oracle's serial solves, or refused when a row has more than 8 dependencies."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    dims = (28, 26, 24)
+    a = P.aniso3d(*dims)
+    layout = P.classify_and_order(a, P.partition(a, 8, dims), 8)
+    m = P.schur_setup(a, layout, rule=P.FillRule.parse(fill))
+    f = m._p.schur
+    kmax = max(int((f.lower.rp[1:] - f.lower.rp[:-1]).max().item()), int((f.upper.rp[1:] - f.upper.rp[:-1]).max().item()) - 1)
+    if kmax > 8:
+        assert f._sw is None
+        pytest.skip(f"{kmax} dependencies per row: tiled / sync-free kernels")
+    assert f._sw is not None and f._sw.k >= kmax and f._sw.k in (2, 3, 4, 8)
+    b = np.random.default_rng(23).standard_normal(f.n)
+    ref_l, ref_u, ref_lu = _oracle_solves(P, orc, f, b)
+    bd = D.to_device_f64(b)
+    xl, xu, xlu = D.empty_f64(f.n), D.empty_f64(f.n), D.empty_f64(f.n)
+    f.lower_solve(bd, xl)
+    f.upper_solve(bd, xu)
+    f.solve(bd, xlu)
+    torch.cuda.synchronize()
+    assert np.array_equal(xl.cpu().numpy(), ref_l) and np.array_equal(xu.cpu().numpy(), ref_u)
+    assert np.array_equal(xlu.cpu().numpy(), ref_lu)
+    x, rep = P.fgmres(a, P.default_rhs(a), m=m.apply)
+    assert rep.converged
