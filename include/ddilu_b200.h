@@ -135,7 +135,7 @@ int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned 
  * `reduced_matvec`, precond.py:361-366 `_coarse_precond`; arithmetic of sparse.py:228-272, bit-exact).  One CTA
  * per block, the block's x in a shared-memory window, the rows' operands streamed as 256-row pages in schedule
  * order through a TMA ring, L and U back to back in one launch.
- * ddilu_sweep_fill: operands of a factor into its pages (k = operand slots per row, gpos / lpos = global padded /
+ * ddilu_sweep_fill: operands of a factor into its pages (k = operand slots per row: 2, 3, 4, 8, or 16 / 24 for long rows, gpos / lpos = global padded /
  * block-local schedule position of every row, gpos_u = position of the row in the U schedule (lower factor only),
  * window = shared-memory window in doubles, a power of two).
  * ddilu_sweep_rhs: right-hand side in schedule order, out[i] = base[row] (row_ptr NULL), (A y)[row] (mode 0),
@@ -146,7 +146,7 @@ int ddilu_sptrsv_tiled(int n, int n_tiles, const int *blk_off16, const unsigned 
  * U levels, offset into levtab, 0, 0, 0}; stages = ring depth (power of two), sets x nct compute threads that own
  * rows_per_thread (1, 2) rows of a level each; out[row] = x (+ add[U position of the row]: `y + S^-1 E y`,
  * precond.py:249). */
-int ddilu_sweep_page_rows(void);
+int ddilu_sweep_page_rows(int k);         /* rows per operand page: 256, or 64 for long rows (k > 8) */
 int ddilu_sweep_helper_threads(void);   /* threads of a CTA that do not compute (TMA issuer, gate, writers) */
 long long ddilu_sweep_page_bytes(int k, int upper);
 long long ddilu_sweep_smem_bytes(int k, int stages, int window, int max_lev);

@@ -49,7 +49,7 @@ SIGNATURES = {
     "ddilu_tiled_smem_bytes": (_L, [_I, _I, _I]),
     "ddilu_fastdiv_selftest": (_I, [_L, ctypes.c_ulonglong, _P, _P]),
     "ddilu_sptrsv_tiled": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
-    "ddilu_sweep_page_rows": (_I, []),
+    "ddilu_sweep_page_rows": (_I, [_I]),
     "ddilu_sweep_helper_threads": (_I, []),
     "ddilu_sweep_page_bytes": (_L, [_I, _I]),
     "ddilu_sweep_smem_bytes": (_L, [_I, _I, _I, _I]),

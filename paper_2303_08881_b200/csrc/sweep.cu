@@ -39,18 +39,19 @@
 
 namespace ddilu {
 
-constexpr int SW_PAGE = 256;            // rows per page
+constexpr int SW_PAGE = 256;            // rows per page (short rows); long rows (K > 8) use 64-row pages
 constexpr int SW_WRITER_WARPS = 3;      // each takes every 3rd page: the flush latencies of consecutive pages overlap
 constexpr int SW_WRITERS = 32 * SW_WRITER_WARPS;
 constexpr int SW_HELPERS = 64 + SW_WRITERS;   // warp 0: TMA issuer (one lane), warp 1: gate (one lane), then the writer warps
 constexpr int SW_MAX_STAGES = 24;
 constexpr int SW_BLOCK_INTS = 8;        // per block: n_rows, page0, nlev_l, nlev_u, lev_off, 0, 0, 0
 
-__host__ __device__ constexpr int sw_page_bytes(int K, bool upper) {
-    return SW_PAGE * (upper ? 10 * K + 20 : 10 * K + 8);
+__host__ __device__ constexpr int sw_page_bytes(int K, bool upper, int P = SW_PAGE) {
+    return P * (upper ? 10 * K + 20 : 10 * K + 8);
 }
 // stage = operands page | right-hand side slice | slice of the vector added to the result (U phase)
-__host__ __device__ constexpr int sw_stage_bytes(int K) { return sw_page_bytes(K, true) + SW_PAGE * 16; }
+__host__ __device__ constexpr int sw_stage_bytes(int K, int P = SW_PAGE) { return sw_page_bytes(K, true, P) + P * 16; }
+__host__ __device__ constexpr int sw_shift(int P) { return P == 256 ? 8 : (P == 128 ? 7 : (P == 64 ? 6 : 5)); }
 
 __device__ __forceinline__ uint32_t sw_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void sw_mbar_init(uint64_t *bar, int count) {
@@ -126,12 +127,12 @@ struct SweepArgs {
 
 // shared memory: [full[S] | empty[S] | lflush | progress] [levels] [window] [stages]
 __host__ __device__ inline size_t sw_ctl_bytes() { return (2 * SW_MAX_STAGES + 2) * 8; }   // + progress, landed (2 ints)
-__host__ __device__ inline size_t sw_smem_bytes(int K, int stages, int window, int max_lev) {
+__host__ __device__ inline size_t sw_smem_bytes(int K, int stages, int window, int max_lev, int P = SW_PAGE) {
     size_t b = sw_ctl_bytes();
     b += ((size_t)max_lev * 8 + 15) & ~(size_t)15;      // (start, end) pair per level
     b += ((size_t)(window + 1) * 8 + 15) & ~(size_t)15;
     b = (b + 127) & ~(size_t)127;
-    return b + (size_t)stages * sw_stage_bytes(K);
+    return b + (size_t)stages * sw_stage_bytes(K, P);
 }
 
 __device__ __forceinline__ double sw_lds(uint32_t a) {
@@ -154,6 +155,11 @@ __device__ __forceinline__ uint32_t sw_lds_u16_at(uint32_t a) {
 __device__ __forceinline__ int sw_lds_s32(uint32_t a) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t sw_lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ void sw_sts(uint32_t a, double v) {
@@ -205,45 +211,54 @@ __device__ __forceinline__ int2 sw_lds_v2(uint32_t a) {
 // the level, so the loop carries nothing but the (start, end) pair of the level, the barrier pair and, for the
 // rows that exist, operand fetch and chain.  DBG (experiments build) adds cycle counters and the strip flags
 // of scripts/probe_sweep.py.
-template <int K, int R, bool UPPER, bool DBG, int BAR_IN, int BAR_OUT>
+template <int K, int R, bool UPPER, bool DBG, int BAR_IN, int BAR_OUT, int P>
 __device__ __forceinline__ void sweep_levels(int set, int NS, int t, int nct, uint32_t lev_u32, int nlev, int gq0,
                                               int smask, const int *landed, uint32_t stage0_u32, uint32_t xs_u32,
                                               int wmask, int *progress, int done_base, long long *dbg, int xflags) {
-    constexpr int P = SW_PAGE;
+    constexpr int PSH = sw_shift(P);
+    // long-row instances (64-row pages): non-blocking operand prefetch, see SW_OPERANDS; the short-row instances
+    // keep the blocking prefetch (their plans satisfy the stricter residency rule of device.build_sweep) and
+    // with it a chain without the pending-row checks
+    constexpr bool NB = P < SW_PAGE;
     constexpr int OFF_PIV = 8 * K * P;                                   // U: d[P], r[P]
     constexpr int OFF_CODE = UPPER ? 8 * K * P + 20 * P : 8 * K * P + 8 * P;
-    constexpr int OFF_RHS = sw_page_bytes(K, true);
-    constexpr int STAGE = sw_stage_bytes(K);
+    constexpr int OFF_RHS = sw_page_bytes(K, true, P);
+    constexpr int STAGE = sw_stage_bytes(K, P);
     const int pair = 2 * nct;                 // threads of a producer set + a consumer set
     int have = 0;                             // ring ordinals below `have` are known to have landed
     long long wait_cycles = 0, t_begin = 0, t_ops = 0, t_fin = 0;
     if (DBG && dbg) t_begin = clock64();
     double c[R][K], rhs[R], d[R], r[R];
     uint32_t sa[R][K], wa[R], slot[R];
-#define SW_OPERANDS(j, p)                                                                              \
+    /* BLOCK = false: prefetch before the level barrier -- if the row's page has not landed yet the row is marked   \
+     * pending and fetched behind the barrier (BLOCK = true).  A prefetch that waited for its page could wait for   \
+     * ever: the page may need a ring stage that is freed only when the progress counter moves, and the progress   \
+     * counter is moved by this very set behind its barrier. */                                                  \
+#define SW_OPERANDS(j, p, BLOCK)                                                                       \
     do {                                                                                               \
         if (DBG && (xflags & 128)) break;                                                              \
-        const int g_ = gq0 + ((p) >> 8);                                                               \
+        const int g_ = gq0 + ((p) >> PSH);                                                             \
         if (g_ >= have) {                                                                              \
-            long long w0_ = 0;                                                                         \
-            if (DBG && dbg) w0_ = clock64();                                                           \
-            while ((have = sw_ld_landed(landed)) <= g_) {}                                           \
-            if (DBG && dbg) wait_cycles += clock64() - w0_;                                            \
+            have = sw_ld_landed(landed);                                                               \
+            if (have <= g_) {                                                                          \
+                if (NB && !(BLOCK)) {                                                                  \
+                    pend |= 1 << (j);                                                                  \
+                    break;                                                                             \
+                }                                                                                      \
+                long long w0_ = 0;                                                                     \
+                if (DBG && dbg) w0_ = clock64();                                                       \
+                while ((have = sw_ld_landed(landed)) <= g_) {}                                         \
+                if (DBG && dbg) wait_cycles += clock64() - w0_;                                        \
+            }                                                                                          \
         }                                                                                              \
         if (DBG && (xflags & 64)) break;                                                               \
         const uint32_t off_ = (uint32_t)((p) & (P - 1));                                               \
         const uint32_t a8_ = stage0_u32 + (uint32_t)(g_ & smask) * STAGE + off_ * 8u;                  \
         const uint32_t a2_ = a8_ - off_ * 6u + OFF_CODE;                                               \
         uint32_t code_[K];                                                                             \
-        if (K >= 1) { c[j][0] = sw_lds_at<0>(a8_); code_[0] = sw_lds_u16_at<0>(a2_); }                 \
-        if (K >= 2) { c[j][1 % K] = sw_lds_at<8 * P>(a8_); code_[1 % K] = sw_lds_u16_at<2 * P>(a2_); } \
-        if (K >= 3) { c[j][2 % K] = sw_lds_at<16 * P>(a8_); code_[2 % K] = sw_lds_u16_at<4 * P>(a2_); } \
-        if (K >= 4) { c[j][3 % K] = sw_lds_at<24 * P>(a8_); code_[3 % K] = sw_lds_u16_at<6 * P>(a2_); } \
-        if (K >= 8) {                                                                                  \
-            c[j][4 % K] = sw_lds_at<32 * P>(a8_); code_[4 % K] = sw_lds_u16_at<8 * P>(a2_);            \
-            c[j][5 % K] = sw_lds_at<40 * P>(a8_); code_[5 % K] = sw_lds_u16_at<10 * P>(a2_);           \
-            c[j][6 % K] = sw_lds_at<48 * P>(a8_); code_[6 % K] = sw_lds_u16_at<12 * P>(a2_);           \
-            c[j][7 % K] = sw_lds_at<56 * P>(a8_); code_[7 % K] = sw_lds_u16_at<14 * P>(a2_);           \
+        _Pragma("unroll") for (int k_ = 0; k_ < K; ++k_) {      /* offsets fold into immediates after unrolling */ \
+            c[j][k_] = sw_lds(a8_ + (uint32_t)(k_ * 8 * P));                                           \
+            code_[k_] = sw_lds_u16(a2_ + (uint32_t)(k_ * 2 * P));                                      \
         }                                                                                              \
         rhs[j] = sw_lds_at<OFF_RHS>(a8_);                                                              \
         if (UPPER) {                                                                                   \
@@ -281,22 +296,29 @@ __device__ __forceinline__ void sweep_levels(int set, int NS, int t, int nct, ui
         const bool first = l == 0;
         long long c0 = 0, c1 = 0;
         if (DBG && dbg) c0 = clock64();
+        int pend = 0;                               // rows whose page had not landed at prefetch time
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (p0 + j * nct < e) SW_OPERANDS(j, p0 + j * nct);
+            if (p0 + j * nct < e) SW_OPERANDS(j, p0 + j * nct, false);
         if (DBG && dbg) c1 = clock64();
         if (!first) sw_bar_sync_c<BAR_IN>(pair);    // results of the previous level are in the window
+        // rows below the level's start are complete: the writers may flush their pages, the ring moves on (with the
+        // non-blocking prefetch this must come before any wait for a page of this level)
+        if (NB && t == 0) sw_st_progress(progress, done_base + se.x);
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (p0 + j * nct < e) SW_FINISH(j);
+            if (p0 + j * nct < e) {
+                if (NB && (pend & (1 << j))) SW_OPERANDS(j, p0 + j * nct, true);
+                SW_FINISH(j);
+            }
         if (wide) {                                 // levels wider than R rows per thread (rare)
             for (int p = p0 + cover; p < e; p += nct) {
-                SW_OPERANDS(0, p);
+                SW_OPERANDS(0, p, true);
                 SW_FINISH(0);
             }
         }
         if (more) sw_bar_arrive_c<BAR_OUT>(pair);
-        if (t == 0) sw_st_progress(progress, done_base + se.x);   // rows below the level's start are complete
+        if (!NB && t == 0) sw_st_progress(progress, done_base + se.x);   // rows below the level's start are complete
         if (DBG && dbg) {
             t_ops += c1 - c0;
             t_fin += clock64() - c1;
@@ -319,12 +341,12 @@ __device__ __forceinline__ void sweep_levels(int set, int NS, int t, int nct, ui
 }
 
 // barrier ids as immediates (a register id makes the compiler pack id and count around every barrier instruction)
-template <int K, int R, bool UPPER, bool DBG>
+template <int K, int R, bool UPPER, bool DBG, int P>
 __device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, uint32_t lev_u32, int nlev, int gq0,
                                               int smask, const int *landed, uint32_t stage0_u32, uint32_t xs_u32,
                                               int wmask, int *progress, int done_base, long long *dbg, int xflags) {
 #define SW_CALL(IN, OUT)                                                                                        \
-    sweep_levels<K, R, UPPER, DBG, IN, OUT>(set, NS, t, nct, lev_u32, nlev, gq0, smask, landed, stage0_u32, xs_u32, \
+    sweep_levels<K, R, UPPER, DBG, IN, OUT, P>(set, NS, t, nct, lev_u32, nlev, gq0, smask, landed, stage0_u32, xs_u32, \
                                             wmask, progress, done_base, dbg, xflags)
     if (set == 0) {
         if (NS == 2) SW_CALL(2, 1);
@@ -337,11 +359,10 @@ __device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, u
 #undef SW_CALL
 }
 
-template <int K, int R, int MAXT, bool DBG>
+template <int K, int R, int MAXT, bool DBG, int P>
 __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepArgs a) {
-    constexpr int P = SW_PAGE;
-    constexpr int STAGE = sw_stage_bytes(K);
-    constexpr int OFF_RHS = sw_page_bytes(K, true);
+    constexpr int STAGE = sw_stage_bytes(K, P);
+    constexpr int OFF_RHS = sw_page_bytes(K, true, P);
     extern __shared__ __align__(128) unsigned char sw_smem[];
     const int *blk = a.blocks + SW_BLOCK_INTS * blockIdx.x;
     const int n_rows = blk[0], page0 = blk[1], nlev_l = blk[2], nlev_u = blk[3], lev_off = blk[4];
@@ -390,10 +411,10 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepArgs a) {
         if (DBG && dbg && t == 0) dbg[16 * set + 2] = 0;
         const uint32_t stage0_u32 = sw_smem_u32(stage0), xs_u32 = sw_smem_u32(xs), lev_u32 = sw_smem_u32(levs);
         if (do_l)
-            sweep_compute<K, R, false, DBG>(set, NS, t, nct, lev_u32, nlev_l, 0, smask, landed, stage0_u32, xs_u32,
+            sweep_compute<K, R, false, DBG, P>(set, NS, t, nct, lev_u32, nlev_l, 0, smask, landed, stage0_u32, xs_u32,
                                             a.wmask, progress, 0, dbg, a.flags);
         if (do_u)
-            sweep_compute<K, R, true, DBG>(set, NS, t, nct, lev_u32 + 8u * (uint32_t)nlev_l, nlev_u, gq_u, smask,
+            sweep_compute<K, R, true, DBG, P>(set, NS, t, nct, lev_u32 + 8u * (uint32_t)nlev_l, nlev_u, gq_u, smask,
                                            landed, stage0_u32, xs_u32, a.wmask, progress, done_u, dbg, a.flags);
     } else if (DBG && (a.flags & 256)) {
         // diagnostics: no helper warps at all (with flags 252: the bare level hand-over of the compute sets)
@@ -405,7 +426,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepArgs a) {
             const int s = i & smask;
             if (i >= S) sw_mbar_wait(&empty[s], (uint32_t)(((i / S) - 1) & 1));
             if (upper && do_l && q == 0) sw_mbar_wait(lflush, 0);   // the U right-hand side is complete and visible
-            const uint32_t pb = upper ? sw_page_bytes(K, true) : sw_page_bytes(K, false);
+            const uint32_t pb = upper ? sw_page_bytes(K, true, P) : sw_page_bytes(K, false, P);
             const unsigned char *src = (upper ? a.pages_u : a.pages_l) + (size_t)(page0 + q) * pb;
             const double *rsrc = ((upper && do_l) ? a.tmp : a.rhs) + (size_t)(page0 + q) * P;
             unsigned char *st = stage0 + (size_t)s * STAGE;
@@ -419,7 +440,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepArgs a) {
             if (j < total && !(DBG && (a.flags & 2))) {
                 const bool up2 = !(do_l && j < n_pages);
                 const int q2 = up2 ? j - gq_u : j;
-                const uint32_t pb2 = up2 ? sw_page_bytes(K, true) : sw_page_bytes(K, false);
+                const uint32_t pb2 = up2 ? sw_page_bytes(K, true, P) : sw_page_bytes(K, false, P);
                 sw_prefetch_l2((up2 ? a.pages_u : a.pages_l) + (size_t)(page0 + q2) * pb2, pb2);
             }
         }
@@ -507,11 +528,10 @@ template <bool UPPER>
 __global__ void sweep_fill_kernel(int n, const int *__restrict__ rp, const int *__restrict__ ci,
                                   const double *__restrict__ val, int K, const int *__restrict__ gpos,
                                   const int *__restrict__ lpos, const int *__restrict__ gpos_u, int wmask,
-                                  unsigned char *pages, int *bad_row) {
-    constexpr int P = SW_PAGE;
+                                  int P, unsigned char *pages, int *bad_row) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n) return;
-    const int g = gpos[row], q = g >> 8, off = g & (P - 1);
+    const int g = gpos[row], q = g / P, off = g & (P - 1);
     const size_t pb = (size_t)P * (UPPER ? 10 * K + 20 : 10 * K + 8);
     unsigned char *pg = pages + (size_t)q * pb;
     double *cf = (double *)pg;
@@ -555,28 +575,32 @@ using namespace ddilu;
 
 #define ST(s) ((cudaStream_t)(s))
 
-extern "C" int ddilu_sweep_page_rows(void) { return SW_PAGE; }
+/* rows per operand page for k operand slots per row: 256, or 64 for long rows (k > 8: the pages of the levels the
+ * compute sets work on at once must fit the ring) */
+extern "C" int ddilu_sweep_page_rows(int k) { return k > 8 ? 64 : SW_PAGE; }
 
 extern "C" int ddilu_sweep_helper_threads(void) { return SW_HELPERS; }
 
-extern "C" long long ddilu_sweep_page_bytes(int k, int upper) { return sw_page_bytes(k, upper != 0); }
+extern "C" long long ddilu_sweep_page_bytes(int k, int upper) {
+    return sw_page_bytes(k, upper != 0, ddilu_sweep_page_rows(k));
+}
 
 extern "C" long long ddilu_sweep_smem_bytes(int k, int stages, int window, int max_lev) {
-    return (long long)sw_smem_bytes(k, stages, window, max_lev);
+    return (long long)sw_smem_bytes(k, stages, window, max_lev, ddilu_sweep_page_rows(k));
 }
 
 extern "C" int ddilu_sweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
                                 const int *gpos, const int *lpos, const int *gpos_u, int window,
                                 unsigned char *pages, int *bad_row, void *stream) {
     if (n <= 0) return DDILU_OK;
-    if (k < 1 || k > 8 || window < 32 || (window & (window - 1)) || window > 32768) return DDILU_ERR_ARG;
-    const int threads = 256, grid = div_up(n, threads);
+    if (k < 1 || k > 24 || window < 32 || (window & (window - 1)) || window > 32768) return DDILU_ERR_ARG;
+    const int threads = 256, grid = div_up(n, threads), page_rows = ddilu_sweep_page_rows(k);
     if (upper)
         sweep_fill_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, lpos, gpos_u,
-                                                                  window - 1, pages, bad_row);
+                                                                  window - 1, page_rows, pages, bad_row);
     else
         sweep_fill_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, lpos, gpos_u,
-                                                                   window - 1, pages, bad_row);
+                                                                   window - 1, page_rows, pages, bad_row);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
@@ -596,19 +620,19 @@ extern "C" int ddilu_sweep_rhs(int npad, const int *rowof, const int *row_ptr, c
 namespace {
 long long *g_sweep_dbg = nullptr;
 int g_sweep_wsleep = 100, g_sweep_flags = 0;
-template <int K, int R, int MAXT, bool DBG>
+template <int K, int R, int MAXT, bool DBG, int P>
 int launch_sweep_one(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
     static size_t attr = 0;     // monotone: the largest dynamic shared-memory size requested so far
     static std::mutex mu;
     {
         std::lock_guard<std::mutex> lock(mu);
         if (attr < smem) {
-            DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R, MAXT, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
+            DDILU_CHECK(cudaFuncSetAttribute(sweep_kernel<K, R, MAXT, DBG, P>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = smem;
         }
     }
-    sweep_kernel<K, R, MAXT, DBG><<<n_blocks, a.sets * a.nct + SW_HELPERS, smem, st>>>(a);
+    sweep_kernel<K, R, MAXT, DBG, P><<<n_blocks, a.sets * a.nct + SW_HELPERS, smem, st>>>(a);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
@@ -616,10 +640,10 @@ template <int K, int R>
 int launch_sweep_kr(int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
     const int threads = a.sets * a.nct + SW_HELPERS;      // register budget follows the CTA size
 #ifdef DDILU_EXPERIMENTS
-    if (a.dbg || a.flags) return launch_sweep_one<K, R, 1024, true>(n_blocks, a, smem, st);
+    if (a.dbg || a.flags) return launch_sweep_one<K, R, 1024, true, SW_PAGE>(n_blocks, a, smem, st);
 #endif
-    if (threads <= 768) return launch_sweep_one<K, R, 768, false>(n_blocks, a, smem, st);
-    return launch_sweep_one<K, R, 1024, false>(n_blocks, a, smem, st);
+    if (threads <= 768) return launch_sweep_one<K, R, 768, false, SW_PAGE>(n_blocks, a, smem, st);
+    return launch_sweep_one<K, R, 1024, false, SW_PAGE>(n_blocks, a, smem, st);
 }
 template <int K>
 int launch_sweep(int rows_per_thread, int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
@@ -628,6 +652,14 @@ int launch_sweep(int rows_per_thread, int n_blocks, const SweepArgs &a, size_t s
         case 2: return launch_sweep_kr<K, 2>(n_blocks, a, smem, st);
         default: return DDILU_ERR_ARG;
     }
+}
+// long rows (ILUT / ILU(k) / 27-point interface factors, up to 24 dependencies): the K coefficients and K window
+// addresses of a row take ~100 registers, so the CTA is capped at 512 threads (one row per thread), and the pages
+// hold 64 rows so that the levels in flight fit the ring
+template <int K>
+int launch_sweep_long(int rows_per_thread, int n_blocks, const SweepArgs &a, size_t smem, cudaStream_t st) {
+    if (rows_per_thread != 1 || a.sets * a.nct + SW_HELPERS > 512) return DDILU_ERR_ARG;
+    return launch_sweep_one<K, 1, 512, false, 64>(n_blocks, a, smem, st);
 }
 }  // namespace
 
@@ -658,13 +690,15 @@ extern "C" int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *lev
         return DDILU_ERR_ARG;
     SweepArgs a{blocks, levtab, pages_l, pages_u, rhs, tmp, out, add, phases, window - 1, stages, sets, nct, max_lev,
                 g_sweep_wsleep, g_sweep_flags, g_sweep_dbg};
-    const size_t smem = sw_smem_bytes(k, stages, window, max_lev);
+    const size_t smem = sw_smem_bytes(k, stages, window, max_lev, ddilu_sweep_page_rows(k));
     if (smem > 227 * 1024) return DDILU_ERR_ARG;
     switch (k) {
         case 2: return launch_sweep<2>(rows_per_thread, n_blocks, a, smem, ST(stream));
         case 3: return launch_sweep<3>(rows_per_thread, n_blocks, a, smem, ST(stream));
         case 4: return launch_sweep<4>(rows_per_thread, n_blocks, a, smem, ST(stream));
         case 8: return launch_sweep<8>(rows_per_thread, n_blocks, a, smem, ST(stream));
+        case 16: return launch_sweep_long<16>(rows_per_thread, n_blocks, a, smem, ST(stream));
+        case 24: return launch_sweep_long<24>(rows_per_thread, n_blocks, a, smem, ST(stream));
         default: return DDILU_ERR_ARG;
     }
 }

@@ -626,10 +626,12 @@ def sptrsv_block_window(t: DeviceCsr, sched: Schedule, bw: BlockWindow, b: torch
 USE_SWEEP = os.environ.get("DDILU_SWEEP", "1") == "1"
 SWEEP_MAX_AVG_WIDTH = 512      # average rows per level of a block up to which one CTA per block is the right shape
 SWEEP_SMEM_BUDGET = 200 * 1024
+SWEEP_SMEM_BUDGET_LONG = 224 * 1024     # long rows: large windows (27-point interfaces reach 16 k positions back)
 SWEEP_MAX_LEVELS = 6144        # level table of a block in shared memory (L + U)
 SWEEP_MAX_THREADS = 416        # compute threads per set (wider levels loop)
 SWEEP_ROWS_PER_THREAD = 1      # rows of a level per thread (1, 2); measured at 256^3 / 128^3: 1 row, 3 sets is the fastest shape
 SWEEP_SETS = 3                 # compute sets taking the levels in turn (2, 3)
+SWEEP_SETS_LONG = 2            # the same for long rows (k > 8): two sets leave more threads per set in a 512-thread CTA
 
 
 @dataclass
@@ -669,9 +671,16 @@ def build_sweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l:
     nb = len(seg_ptr) - 1
     if not USE_SWEEP or n == 0 or nb < 1 or nlev_l == 0 or nlev_u == 0:
         return None
-    P = query("ddilu_sweep_page_rows")
     d = dev()
     i64 = torch.int64
+    # dependency counts -> operand slots per row (long rows: 64-row pages, one row per thread, 512-thread CTAs)
+    kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
+    ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
+    kmax = max(kl, ku, 1)
+    k = next((c for c in (2, 3, 4, 8, 16, 24) if kmax <= c), None)
+    if k is None:
+        return None
+    P = query("ddilu_sweep_page_rows", k)
     seg = torch.tensor([int(v) for v in seg_ptr], dtype=i64, device=d)
     if int(seg[-1].item()) != n or int(seg[0].item()) != 0:
         return None
@@ -682,13 +691,6 @@ def build_sweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l:
     page0 = torch.cumsum(n_pages_b, 0) - n_pages_b
     n_pages = int(n_pages_b.sum().item())
     npad = n_pages * P
-    # dependency counts -> operand slots per row
-    kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
-    ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
-    kmax = max(kl, ku, 1)
-    k = next((c for c in (2, 3, 4, 8) if kmax <= c), None)
-    if k is None:
-        return None
     plans = []
     for fac, lev, nlev, up in ((lower, lev_l, nlev_l, False), (upper, lev_u, nlev_u, True)):
         key = blk * nlev + lev[:n].to(i64)
@@ -718,19 +720,29 @@ def build_sweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l:
     nlev_b = plans[0][5] + plans[1][5]
     max_lev = int(nlev_b.max().item())
     avg_width = float(n) / max(1, int(plans[0][5].sum().item()))
+    if os.environ.get("DDILU_DEBUG_SWEEP"):
+        print(f"sweep plan: k {k} (max deps {kmax}), page rows {P}, window {window}, widest level {width_max}, "
+              f"levels per block {max_lev}, average width {avg_width:.1f}", flush=True)
     if window > 16384 or max_lev > SWEEP_MAX_LEVELS or avg_width > SWEEP_MAX_AVG_WIDTH:
         return None
     rpt, sets = SWEEP_ROWS_PER_THREAD, SWEEP_SETS
     helpers = query("ddilu_sweep_helper_threads")
-    nct = min(SWEEP_MAX_THREADS, ((1024 - helpers) // sets) & ~31, max(32, ((width_max + rpt - 1) // rpt + 31) & ~31))
+    cta_max = 1024
+    if k > 8:
+        rpt, sets, cta_max = 1, SWEEP_SETS_LONG, 512
+    nct = min(SWEEP_MAX_THREADS, ((cta_max - helpers) // sets) & ~31, max(32, ((width_max + rpt - 1) // rpt + 31) & ~31))
     stages = 0
+    budget = SWEEP_SMEM_BUDGET_LONG if k > 8 else SWEEP_SMEM_BUDGET
     for st in (16, 8, 4):
-        if query("ddilu_sweep_smem_bytes", k, st, window, max_lev) <= SWEEP_SMEM_BUDGET:
+        if query("ddilu_sweep_smem_bytes", k, st, window, max_lev) <= budget:
             stages = st
             break
-    # ring residency: the sets work on up to `sets` consecutive levels at once and a page is freed only when the
-    # progress counter (start of the level being executed) has passed it -- all pages of those levels must fit
-    if stages < 4 or sets * width_max > (stages - 2) * P:
+    # ring residency.  Short rows (blocking operand prefetch): the sets work on up to `sets` consecutive levels at
+    # once and a page is freed only when the progress counter (start of the level being executed) has passed it, so
+    # all pages of those levels must fit.  Long rows (64-row pages): the prefetch never waits for a page -- rows
+    # whose page has not landed are fetched behind the level barrier -- so only the pages of ONE level, plus the
+    # page it shares with its predecessor, must fit.
+    if stages < 4 or (width_max > (stages - 1) * P if k > 8 else sets * width_max > (stages - 2) * P):
         return None
     # level tables: per block its L levels then its U levels
     lev_off = torch.cumsum(nlev_b, 0) - nlev_b

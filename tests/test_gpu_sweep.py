@@ -130,7 +130,7 @@ def test_pipeline_same_with_and_without_sweep(P):
 
 
 def test_sweep_refuses_unsuitable_factors(P):
-    """Wide levels (a block-Jacobi factor of a whole 3D subdomain) and rows with more than 8 dependencies get no
+    """Wide levels (a block-Jacobi factor of a whole 3D subdomain) and rows with more than 24 dependencies get no
     plan; the caller falls back to the tiled / sync-free kernels."""
     from paper_2303_08881_b200 import device as D
     dims = (24, 24, 24)
@@ -142,9 +142,44 @@ def test_sweep_refuses_unsuitable_factors(P):
         assert D.build_sweep(f.lower, f.upper, *f._lev(False), *f._lev(True), [0, f.n]) is None
     finally:
         D.SWEEP_MAX_AVG_WIDTH = old
+    # rows with more than 24 dependencies (27-point ILU(1): up to ~40) get no plan either
     a27 = P.convdiff27(10, 10, 10)
-    f27 = P.ilu0(a27).device()
+    f27 = P.iluk(a27, 1).device()
+    assert int((f27.upper.rp[1:] - f27.upper.rp[:-1]).max().item()) - 1 > 24
     assert D.build_sweep(f27.lower, f27.upper, *f27._lev(False), *f27._lev(True), [0, f27.n]) is None
+
+
+@pytest.mark.parametrize("dims,p,fill", [((24, 24, 24), 8, "ilut:0.001,20"), ((20, 18, 16), 4, "ilu0"),
+                                         ((28, 28, 28), 8, "ilut:0.001,20")])
+def test_sweep_long_rows_27_point(P, orc, dims, p, fill):
+    """Interface factors of the 27-point problem (BASELINE config 5: ILUT(1e-3, 20), up to 20 dependencies per
+    row): the long-row instances of the kernel (16 / 24 operand slots, 64-row pages, 512-thread CTAs) bit-exact
+    against the oracle's serial solves, and the solve converging with the oracle's iteration count."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    a = P.convdiff27(*dims)
+    layout = P.classify_and_order(a, P.partition(a, p, dims), p)
+    m = P.schur_setup(a, layout, rule=P.FillRule.parse(fill))
+    f = m._p.schur
+    sp = f._sw
+    assert sp is not None, "27-point interface factors did not get a plan"
+    if fill.startswith("ilut"):
+        assert sp.k in (16, 24) and sp.rpt == 1, "ILUT interface factors should take the long-row instances"
+    rng = np.random.default_rng(29)
+    for rep in range(2):
+        b = rng.standard_normal(f.n)
+        ref_l, ref_u, ref_lu = _oracle_solves(P, orc, f, b)
+        bd = D.to_device_f64(b)
+        xl, xu, xlu = D.empty_f64(f.n), D.empty_f64(f.n), D.empty_f64(f.n)
+        f.lower_solve(bd, xl)
+        f.upper_solve(bd, xu)
+        f.solve(bd, xlu)
+        torch.cuda.synchronize()
+        assert np.array_equal(xl.cpu().numpy(), ref_l), ("L", rep)
+        assert np.array_equal(xu.cpu().numpy(), ref_u), ("U", rep)
+        assert np.array_equal(xlu.cpu().numpy(), ref_lu), ("LU", rep)
+    x, rep_ = P.fgmres(a, P.default_rhs(a), m=m.apply)
+    assert rep_.converged
 
 
 @pytest.mark.timeout(300)
@@ -188,10 +223,10 @@ def test_sweep_with_longer_rows(P, orc, fill):
     m = P.schur_setup(a, layout, rule=P.FillRule.parse(fill))
     f = m._p.schur
     kmax = max(int((f.lower.rp[1:] - f.lower.rp[:-1]).max().item()), int((f.upper.rp[1:] - f.upper.rp[:-1]).max().item()) - 1)
-    if kmax > 8:
+    if kmax > 24:
         assert f._sw is None
         pytest.skip(f"{kmax} dependencies per row: tiled / sync-free kernels")
-    assert f._sw is not None and f._sw.k >= kmax and f._sw.k in (2, 3, 4, 8)
+    assert f._sw is not None and f._sw.k >= kmax and f._sw.k in (2, 3, 4, 8, 16, 24)
     b = np.random.default_rng(23).standard_normal(f.n)
     ref_l, ref_u, ref_lu = _oracle_solves(P, orc, f, b)
     bd = D.to_device_f64(b)
