@@ -336,6 +336,8 @@ def run_ours(args):
                                     "avg_launch_us": d_s * 1e6, "per_solve_us": d_s * 1e6 / 2,
                                     "launches_in_timed_region": len(sw),
                                     "achieved_gbs": sb / d_s / 1e9, "frac": sb / d_s / 1e9 / peak,
+                                    "algorithmic_bytes_per_launch": sb,
+                                    "traffic": _traffic(f"sweep_solve_{args.n}_{args.precond}"),
                                     "threads": sf._sw.nct, "stages": sf._sw.stages, "window": sf._sw.window,
                                     "note": "latency-bound: dependent levels of ~190 rows; measured inside the timed region"}
     tr = sorted(e0.elapsed_time(e1) * 1e-3 for e0, e1, _ in prof_all.get(trsv_name, []))
