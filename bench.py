@@ -477,7 +477,9 @@ def relaunch_under_torchrun(args):
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
     # (torchrun's own parser would take a bare "--n" for an abbreviation of --nnodes / --nproc-per-node)
     cmd += ["--grid" if a == "--n" else a for a in sys.argv[1:]]
-    raise SystemExit(subprocess.call(cmd))
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")      # the communicator log (ranks, NVLS / P2P transport) goes to stderr
+    raise SystemExit(subprocess.call(cmd, env=env))
 
 
 def main():
