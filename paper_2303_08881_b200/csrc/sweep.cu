@@ -326,11 +326,6 @@ __device__ __forceinline__ void sweep_levels(int set, int NS, int t, int nct, ui
     }
 #undef SW_OPERANDS
 #undef SW_FINISH
-    sw_bar_sync_id(4, NS * nct);                    // end of the phase: every row is stored
-    if (set == 0 && t == 0) {
-        const int last = nlev ? sw_lds_v2(lev_u32 + 8u * (uint32_t)(nlev - 1)).y : 0;
-        sw_st_progress(progress, done_base + last);
-    }
     if (DBG && dbg && t == 0) {
         long long *o = dbg + 16 * set;
         o[UPPER ? 1 : 0] = clock64() - t_begin;
@@ -357,6 +352,13 @@ __device__ __forceinline__ void sweep_compute(int set, int NS, int t, int nct, u
         SW_CALL(2, 3);
     }
 #undef SW_CALL
+    // end of the phase: every row is stored.  ONE barrier instruction for all sets (the level loops above are
+    // separate instances per set; a barrier inside them would be reached at different program counters)
+    sw_bar_sync_id(4, NS * nct);
+    if (set == 0 && t == 0) {
+        const int last = nlev ? sw_lds_v2(lev_u32 + 8u * (uint32_t)(nlev - 1)).y : 0;
+        sw_st_progress(progress, done_base + last);
+    }
 }
 
 template <int K, int R, int MAXT, bool DBG, int P>

@@ -3,6 +3,8 @@
     compute-sanitizer --tool memcheck python scripts/sanitize_case.py [tiled|sweep|mgs|ilut|rcm|pipeline ...]
 
 tiled: sptrsv_tiled on interior + interface factors; sweep: the block sweep (L, U, fused, with product and add);
+sweep_long: its long-row instances on 27-point ILUT interface factors (+ a whole solve: device-side inner-solve
+arithmetic); spgemm: sparse_matmul;
 mgs: ddilu_mgs_block over ragged lengths and block shapes; ilut: ilut_kernel (27-point, fill);
 rcm: cm_order_kernel on several disconnected blocks; pipeline: one schur + rap-milu FGMRES solve."""
 import os
@@ -15,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_08881_b200 as P
 from paper_2303_08881_b200 import device as D
 
-which = sys.argv[1:] or ["tiled", "sweep", "mgs", "ilut", "rcm", "pipeline"]
+which = sys.argv[1:] or ["tiled", "sweep", "sweep_long", "mgs", "ilut", "rcm", "spgemm", "pipeline"]
 dims = (20, 18, 17)
 a = P.aniso3d(*dims)
 layout = P.classify_and_order(a, P.partition(a, 4, dims), 4)
@@ -47,6 +49,27 @@ if "sweep" in which:
     solve_with_product(f, m._coupling, y, None, 0, x, add=y)
     torch.cuda.synchronize()
     print("sweep", f.n, f._sw.nct, f._sw.sets, float(x.abs().max()))
+
+if "sweep_long" in which:
+    d27 = (14, 13, 12)
+    a27 = P.convdiff27(*d27)
+    lay27 = P.classify_and_order(a27, P.partition(a27, 4, d27), 4)
+    m = P.make_preconditioner("schur", a27, lay27, P.FillRule.parse("ilut:0.001,20"))
+    f = m._p.schur
+    assert f._sw is not None and f._sw.k > 8
+    r = torch.randn(f.n, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(r)
+    f.lower_solve(r, x)
+    f.upper_solve(r, x)
+    f.solve(r, x)
+    x2, rep = P.fgmres(a27, P.default_rhs(a27), m=m.apply)
+    torch.cuda.synchronize()
+    print("sweep_long", f.n, f._sw.k, f._sw.nct, f._sw.sets, f._sw.stages, rep.iterations, rep.converged)
+
+if "spgemm" in which:
+    g = P.poisson3d(7, 6, 5)
+    c = P.sparse_matmul(g, g)
+    print("spgemm", c.nnz)
 
 if "mgs" in which:
     red = D.Reducer()
