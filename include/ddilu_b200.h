@@ -58,6 +58,11 @@ int ddilu_schedule_build(int n, const int *lev, int n_levels, int upper, int *ke
  * smallest failing row (the reference raises ZeroDivisionError for that row). */
 int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row_ptr, const int *col_idx, const double *values,
                  const double *b, double *x, int upper, int unit_diag, int *err, void *stream);
+/* the same solve with a WARP per row: long rows (ILUT / ILU(k) / 27-point factors, 10-20 dependencies) -- one
+ * coalesced load of the row, all dependencies polled at once, products added in storage order by one lane */
+int ddilu_sptrsv_warprow(int n, int n_slots, const int *order, const int *row_ptr, const int *col_idx,
+                         const double *values, const double *b, double *x, int upper, int unit_diag, int *err,
+                         void *stream);
 
 /* Schedule-ordered sliced-ELL form of a factor (group = 32 schedule slots = one
  * warp): gw32[g] = 32 * (longest dependency list in group g) -> scan -> goff;

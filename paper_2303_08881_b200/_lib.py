@@ -31,6 +31,7 @@ SIGNATURES = {
     "ddilu_levels": (_I, [_I, _P, _P, _I, _P, _P, _P]),
     "ddilu_schedule_build": (_I, [_I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "ddilu_sptrsv_warprow": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ddilu_sell_width": (_I, [_I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "ddilu_sell_fill": (_I, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
     "ddilu_compose_wait": (_I, [_I, _P, _P, _P, _P, _P]),

@@ -104,6 +104,93 @@ __global__ void __launch_bounds__(TRSV_THREADS) sptrsv_syncfree(int n_slots, con
     }
 }
 
+// Warp-per-row variant for LONG rows (ILUT / ILU(k) / 27-point factors: 10-20 dependencies per row, factors that
+// neither tile nor fit a block sweep).  The thread-per-row kernels above poll a row's dependencies in rounds of
+// 4-16 and add the products one after the other in ONE thread: 3.5 us per level on the 27-point interior factors
+// (3 % of the HBM roofline).  Here a warp owns a row: the lanes fetch the row's entries with one coalesced load,
+// poll all dependencies at once (x is its own ready flag, as above), round their products, and lane 0 adds them
+// in storage order (sparse.py:228-272: same operations, same order -> same bits).  Warps take the schedule slots
+// round-robin; the launch is cooperative, so the earliest unfinished row always belongs to a resident warp.
+constexpr int WR_WARPS = 8;
+template <bool UPPER>
+__global__ void __launch_bounds__(32 * WR_WARPS) sptrsv_warprow(int n_slots, const int *__restrict__ order,
+                                                                const int *__restrict__ rp, const int *__restrict__ ci,
+                                                                const double *__restrict__ val,
+                                                                const double *__restrict__ b, double *x, int unit_diag,
+                                                                int *err, unsigned sleep_ns) {
+    __shared__ double prod[WR_WARPS][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long n_warps = (long long)gridDim.x * WR_WARPS;
+    long long slot = (long long)blockIdx.x * WR_WARPS + wib;
+    // software pipeline: row id, row bounds and right-hand side of the NEXT slot are fetched while this one waits
+    int row = slot < n_slots ? order[slot] : -1;
+    int k0 = 0, k1 = 0;
+    double rhs = 0.0;
+    if (row >= 0) {
+        k0 = rp[row];
+        k1 = rp[row + 1];
+        rhs = b[row];
+    }
+    for (; slot < n_slots; slot += n_warps) {
+        const long long nslot = slot + n_warps;
+        const int nrow = nslot < n_slots ? order[nslot] : -1;
+        int nk0 = 0, nk1 = 0;
+        double nrhs = 0.0;
+        if (nrow >= 0) {
+            nk0 = rp[nrow];
+            nk1 = rp[nrow + 1];
+            nrhs = b[nrow];
+        }
+        if (row >= 0) {
+            double s = rhs, diag = 1.0;
+            bool seen = false;
+            for (int base = k0; base < k1; base += 32) {
+                const int k = base + lane;
+                const bool in = k < k1;
+                const int col = in ? ci[k] : row;
+                const double a = in ? val[k] : 0.0;
+                const bool dep = in && (UPPER ? col > row : col < row);
+                const unsigned dmask = __ballot_sync(0xffffffffu, in && col == row);
+                if (dmask) {
+                    diag = __shfl_sync(0xffffffffu, a, __ffs(dmask) - 1);
+                    seen = true;
+                }
+                double v = 0.0;
+                if (dep) {
+                    v = ld_l2(x + col);
+                    while (is_sentinel(v)) {
+                        if (sleep_ns) __nanosleep(sleep_ns);
+                        v = ld_l2(x + col);
+                    }
+                }
+                prod[wib][lane] = dep ? a * v : 0.0;          // every product rounded (-fmad=false)
+                __syncwarp();
+                if (lane == 0) {
+                    const int cnt = min(32, k1 - base);
+                    for (int q = 0; q < cnt; ++q) s -= prod[wib][q];   // storage order; non-dependencies subtract 0.0
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                double res = s;
+                if (!unit_diag) {
+                    if (!seen || fabs(diag) < 1e-300) {
+                        atomicMin(err, row);
+                        res = __longlong_as_double(0x7FF8000000000000LL);
+                    } else {
+                        res = s / diag;
+                    }
+                }
+                st_l2(x + row, scrub_sentinel(res));
+            }
+        }
+        row = nrow;
+        k0 = nk0;
+        k1 = nk1;
+        rhs = nrhs;
+    }
+}
+
 // Topological level of every row (lev[i] = 1 + max lev[j] over dependencies),
 // rows visited in index order (reverse for U).  lev is preset to -1 and is its
 // own ready flag.  Dependencies may sit in the same warp here, so the loop
@@ -877,6 +964,27 @@ extern "C" int ddilu_sptrsv(int n, int n_slots, const int *order, const int *row
         int grid = coop_grid(sptrsv_syncfree<false>, TRSV_THREADS, g_trsv.blocks_per_sm, n_slots);
         DDILU_CHECK(cudaLaunchCooperativeKernel((void *)sptrsv_syncfree<false>, grid, TRSV_THREADS, args, 0, st));
     }
+    return DDILU_OK;
+}
+
+/* the same solve with a warp per row (long rows: ILUT / ILU(k) / 27-point factors) */
+extern "C" int ddilu_sptrsv_warprow(int n, int n_slots, const int *order, const int *row_ptr, const int *col_idx,
+                                    const double *values, const double *b, double *x, int upper, int unit_diag,
+                                    int *err, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return DDILU_OK;
+    if (x == b) return DDILU_ERR_ARG;
+    DDILU_CHECK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n, st));
+    unsigned sleep_ns = g_trsv.sleep_ns;
+    void *args[] = {&n_slots, &order, &row_ptr, &col_idx, &values, &b, &x, &unit_diag, &err, &sleep_ns};
+    void *fn = upper ? (void *)sptrsv_warprow<true> : (void *)sptrsv_warprow<false>;
+    int occ = 0;
+    DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * WR_WARPS, 0));
+    if (occ < 1) occ = 1;
+    long long grid = (long long)occ * device_info().sm_count;
+    const long long need = ((long long)n_slots + WR_WARPS - 1) / WR_WARPS;
+    if (grid > need) grid = need < 1 ? 1 : need;
+    DDILU_CHECK(cudaLaunchCooperativeKernel(fn, (int)grid, 32 * WR_WARPS, args, 0, st));
     return DDILU_OK;
 }
 

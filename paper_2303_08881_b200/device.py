@@ -506,6 +506,8 @@ def sptrsv_tiled(ts, b: torch.Tensor, out: torch.Tensor, check: bool = False):
 
 
 USE_SELL = True   # False: CSR thread-per-row kernel (kept for comparison runs)
+USE_WARPROW = os.environ.get("DDILU_WARPROW", "1") == "1"   # warp-per-row sync-free solve for long rows
+WARPROW_MIN_AVG_ROW = 8.0     # stored entries per row from which a warp per row pays
 UNIFORM_SELL = True
 USE_GWAIT = True
 USE_BLOCK_WINDOW = os.environ.get("DDILU_BLOCK_WINDOW", "0") == "1"   # interface factors: CTA-per-block sweep, x window in shared memory
@@ -1009,6 +1011,11 @@ def enable_block_local(sched: Schedule, seg_ptr) -> bool:
     return True
 
 
+def uses_warprow(t: DeviceCsr) -> bool:
+    """Whether `sptrsv` serves this factor with the warp-per-row kernel (long rows) instead of the SELL layout."""
+    return bool(USE_WARPROW and t.n_rows and t.nnz >= WARPROW_MIN_AVG_ROW * t.n_rows)
+
+
 def get_sell(t: DeviceCsr, sched: Schedule, upper: bool, unit_diag: bool) -> Sell:
     if sched.sell is None:
         sched.sell = {}
@@ -1046,6 +1053,16 @@ def sptrsv(t: DeviceCsr, sched: Schedule, b: torch.Tensor, out: torch.Tensor, up
         bl = sched.blocks
         call("ddilu_sptrsv_blocklocal", bl.n_blocks, sched.n_levels, bl.start, bl.cnt, sched.level_rows, t.rp, t.ci,
              t.val, b, out, int(upper), int(unit_diag), _err())
+        if check:
+            bad = int(_err().item())
+            if bad != INT_MAX:
+                _err().fill_(INT_MAX)
+                raise TriSolveError(f"zero or missing diagonal at row {bad}")
+        return out
+    if uses_warprow(t):
+        # long rows (ILUT / ILU(k) / 27-point factors): a warp per row
+        call("ddilu_sptrsv_warprow", t.n_rows, sched.n_slots, sched.order, t.rp, t.ci, t.val, b, out, int(upper),
+             int(unit_diag), _err())
         if check:
             bad = int(_err().item())
             if bad != INT_MAX:

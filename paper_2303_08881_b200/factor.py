@@ -153,9 +153,9 @@ class DevFactors:
         if seg_ptr is not None and (self._tl is None or self._tu is None):
             D.enable_block_local(self.sched_l, seg_ptr) and D.enable_block_local(self.sched_u, seg_ptr)
         if self._tl is None:
-            D.get_sell(self.lower, self.sched_l, False, True)
+            self.sched_l if D.uses_warprow(self.lower) else D.get_sell(self.lower, self.sched_l, False, True)
         if self._tu is None:
-            D.get_sell(self.upper, self.sched_u, True, False)
+            self.sched_u if D.uses_warprow(self.upper) else D.get_sell(self.upper, self.sched_u, True, False)
         if self._tmp is None:
             self._tmp = D.empty_f64(max(self.n, 1))
         return self

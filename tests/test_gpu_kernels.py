@@ -284,3 +284,40 @@ def test_compact_row_updates_match_the_full_pass(P):
     dense_rp = np.arange(n_rows + 1, dtype=np.int64)
     d = P.CsrMatrix(n_rows, n_cols, dense_rp, np.zeros(n_rows, dtype=np.int64), np.ones(n_rows)).device()
     assert D.compact_rows(d) is None
+
+
+def test_warp_per_row_solve_bit_exact(P, orc):
+    """`ddilu_sptrsv_warprow` (long rows: 27-point ILU(0) / ILUT / ILU(1) factors) against the oracle's serial solves
+    and against the thread-per-row kernels, L and U, plus the zero-pivot report."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    rng = np.random.default_rng(41)
+    for a, f in ((P.convdiff27(11, 10, 9), None), (P.convdiff27(9, 9, 9), "ilut"), (P.poisson3d(12, 11, 10), "iluk")):
+        fac = P.ilu0(a) if f is None else (P.ilut(a, 1e-3, 20) if f == "ilut" else P.iluk(a, 2))
+        dv = fac.device()
+        assert D.uses_warprow(dv.upper)
+        b = rng.standard_normal(a.n_rows)
+        bd = D.to_device_f64(b)
+        lo, up = fac.lower, fac.upper
+        ref_l = orc.tri_solve_lower(orc.Csr(lo.n_rows, lo.n_cols, lo.row_ptr, lo.col_idx, lo.values), b, True)
+        ref_u = orc.tri_solve_upper(orc.Csr(up.n_rows, up.n_cols, up.row_ptr, up.col_idx, up.values), b)
+        for t, sched, upper, unit, ref in ((dv.lower, dv.sched_l, False, True, ref_l), (dv.upper, dv.sched_u, True, False, ref_u)):
+            out = {}
+            for mode in (True, False):
+                old = D.USE_WARPROW
+                D.USE_WARPROW = mode
+                try:
+                    x = D.empty_f64(a.n_rows)
+                    D.sptrsv(t, sched, bd, x, upper, unit)
+                    torch.cuda.synchronize()
+                    out[mode] = x.cpu().numpy()
+                finally:
+                    D.USE_WARPROW = old
+            assert np.array_equal(out[True], ref), (f, upper)
+            assert np.array_equal(out[True], out[False]), (f, upper)
+    # zero pivot: reported as the failing row, like the reference (sparse.py:268-270)
+    d = np.triu(rng.standard_normal((40, 40))) + 5.0 * np.eye(40)
+    d[17, 17] = 0.0
+    u = P.csr_from_dense(d, keep_zeros=True) if "keep_zeros" in P.csr_from_dense.__code__.co_varnames else P.csr_from_dense(d)
+    with pytest.raises(ZeroDivisionError):
+        P.tri_solve_upper(u, np.ones(40))
