@@ -31,6 +31,7 @@ constexpr int TRSV_UNROLL = 4;
 
 struct TrsvTuning {
     int blocks_per_sm = 3;
+    int wr_blocks_per_sm = 0;  // warp-per-row kernel: CTAs per SM (0: as many as fit; measured best, scripts/probe_warprow.py)
     unsigned sleep_ns = 0;
     int pipe = 0;            // 1: software-pipelined SELL kernel, 0: plain SELL kernel
     int pipe_warps_per_sm = 8;
@@ -900,6 +901,7 @@ extern "C" int ddilu_set_tuning(const char *key, int value) {
     if (!key) return DDILU_ERR_ARG;
     if (!strcmp(key, "trsv_blocks_per_sm")) g_trsv.blocks_per_sm = value;
     else if (!strcmp(key, "trsv_sleep_ns")) g_trsv.sleep_ns = (unsigned)value;
+    else if (!strcmp(key, "wr_blocks_per_sm")) g_trsv.wr_blocks_per_sm = value;
     else if (!strcmp(key, "trsv_pipe")) g_trsv.pipe = value;
     else if (!strcmp(key, "trsv_depth")) g_trsv.depth = value;
     else if (!strcmp(key, "trsv_chunk")) g_trsv.chunk = value;
@@ -981,6 +983,7 @@ extern "C" int ddilu_sptrsv_warprow(int n, int n_slots, const int *order, const 
     int occ = 0;
     DDILU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * WR_WARPS, 0));
     if (occ < 1) occ = 1;
+    if (g_trsv.wr_blocks_per_sm > 0 && occ > g_trsv.wr_blocks_per_sm) occ = g_trsv.wr_blocks_per_sm;
     long long grid = (long long)occ * device_info().sm_count;
     const long long need = ((long long)n_slots + WR_WARPS - 1) / WR_WARPS;
     if (grid > need) grid = need < 1 ? 1 : need;
