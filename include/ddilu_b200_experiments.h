@@ -69,6 +69,7 @@ int ddilu_sptrsv_warptile(int n, int n_tiles, const int *blk_off16, const unsign
 
 int ddilu_sweep_set_tuning(int writer_sleep_ns, int flags);   /* diagnostics */
 int ddilu_sweep_set_debug(long long *buf);   /* diagnostics: 64 int64 cycle counters per block, NULL = off */
+int ddilu_csweep_set_debug(long long *buf);  /* cluster sweep: 16 int64 cycle counters per CTA and probe thread (first, last), NULL = off */
 
 /* ---- lattice triangular solve (csrc/experiments/lattice.cu): the fast path of sparse.py:228-272 for factors whose box
  * tiles are lattices with one-way axes and <= 3 dependencies per row (7-point ILU(0) factors).  One warp per

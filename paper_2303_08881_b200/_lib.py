@@ -57,6 +57,14 @@ SIGNATURES = {
     "ddilu_sweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "ddilu_sweep_rhs": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sweep_solve": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "ddilu_csweep_threads": (_I, [_I, _I]),
+    "ddilu_csweep_window": (_I, []),
+    "ddilu_csweep_max_push": (_I, []),
+    "ddilu_csweep_record_bytes": (_I, [_I]),
+    "ddilu_csweep_smem_bytes": (_L, [_I, _I, _I]),
+    "ddilu_csweep_active_clusters": (_I, [_I, _I, _I]),
+    "ddilu_csweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "ddilu_csweep_solve": (_I, [_I, _I, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),
@@ -132,6 +140,7 @@ EXPERIMENT_SIGNATURES = {
     "ddilu_sptrsv_lean": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_sptrsv_warptile": (_I, [_I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_sweep_set_debug": (_I, [_P]),
+    "ddilu_csweep_set_debug": (_I, [_P]),
     "ddilu_sweep_set_tuning": (_I, [_I, _I]),
     "ddilu_lattice_build": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
     "ddilu_lattice_max_ext": (_I, []),

@@ -798,6 +798,223 @@ def sweep_solve(sp: SweepPlan, phases: int, out: torch.Tensor, add: bool = False
 
 
 # ---------------------------------------------------------------------------
+# cluster sweep (csrc/csweep.cu): block-diagonal factors with LARGE deep blocks (the interior factors L_B / U_B) --
+# a thread-block cluster per block, x in a window distributed over the CTAs' shared memory
+
+USE_CSWEEP = os.environ.get("DDILU_CSWEEP", "1") == "1"
+CSWEEP_CLUSTER = int(os.environ.get("DDILU_CSWEEP_CLUSTER", "16"))   # CTAs per block at most (the largest size whose clusters can all be resident is taken)
+CSWEEP_NSET = int(os.environ.get("DDILU_CSWEEP_DEPTH", "3"))         # stages of the operand ring: operands requested depth - 1 steps ahead
+CSWEEP_MIN_CHUNK = int(os.environ.get("DDILU_CSWEEP_MIN_CHUNK", "32"))   # rows of a level a CTA takes at least (narrow levels stay on few CTAs)
+CSWEEP_MIN_AVG_WIDTH = 1024    # average rows per level of a block from which a cluster pays (below: one CTA per block)
+CSWEEP_MIN_SMS = 60            # blocks x cluster size: SMs the launch must fill to have the bandwidth of the GPU
+_csweep_active = {}
+
+
+def csweep_active_clusters(csize: int, depth: int, max_steps: int) -> int:
+    key = (csize, depth, max_steps)
+    if key not in _csweep_active:
+        _csweep_active[key] = query("ddilu_csweep_active_clusters", csize, depth, max_steps)
+    return _csweep_active[key]
+
+
+@dataclass
+class ClusterSweepHalf:
+    """One factor (L or U) in the layout of `ddilu_csweep_solve`."""
+
+    ctas: torch.Tensor         # int32[n_blocks * csize * 4]
+    steps: torch.Tensor        # int32[total steps * 8]
+    recs: torch.Tensor         # uint8: one record per position (coefficients, dependency slots, push targets, pivot pair)
+    rowid: torch.Tensor
+    np: int
+    max_steps: int
+    contiguous: bool           # every level chunk is a range of consecutive rows (no row-id loads)
+
+
+@dataclass
+class ClusterSweepPlan:
+    n: int
+    n_blocks: int
+    csize: int
+    k: int
+    nset: int
+    lower: ClusterSweepHalf
+    upper: ClusterSweepHalf
+    bad_row: int
+
+
+def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l: int, lev_u: torch.Tensor,
+                 nlev_u: int, seg_ptr) -> "ClusterSweepPlan | None":
+    """Plan of the cluster sweep for the factor pair (L strictly lower, U with its diagonal) whose independent
+    diagonal blocks are the row ranges seg_ptr (host ints); None when the pair does not qualify (a dependency
+    leaves its block, more than 4 dependencies per row, blocks too few / too narrow for clusters, a dependency
+    further back than the window, clusters cannot be resident)."""
+    n = lower.n_rows
+    nb = len(seg_ptr) - 1
+    if not USE_CSWEEP or n == 0 or nb < 1 or nlev_l == 0 or nlev_u == 0:
+        return None
+    d = dev()
+    i64 = torch.int64
+    debug = bool(os.environ.get("DDILU_DEBUG_SWEEP"))
+    if n / (nb * max(nlev_l, nlev_u)) < CSWEEP_MIN_AVG_WIDTH:
+        return None
+    kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
+    ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
+    kmax = max(kl, ku, 1)
+    k = next((c for c in (3, 4) if kmax <= c), None)
+    if k is None:
+        return None
+    W = query("ddilu_csweep_window")
+    nset = CSWEEP_NSET
+    lev_cap = 2 * max(nlev_l, nlev_u)           # steps of a CTA: its levels, the wide ones in several pieces
+    if query("ddilu_csweep_smem_bytes", 1, nset, lev_cap) > 227 * 1024:
+        return None
+    csize = next((c for c in range(min(16, CSWEEP_CLUSTER), 0, -1) if csweep_active_clusters(c, nset, lev_cap) >= nb), 0)
+    if debug:
+        print(f"cluster sweep: {nb} blocks -> clusters of {csize}", flush=True)
+    if not csize or nb * csize < CSWEEP_MIN_SMS:
+        return None
+    seg = torch.tensor([int(v) for v in seg_ptr], dtype=i64, device=d)
+    if int(seg[-1].item()) != n or int(seg[0].item()) != 0:
+        return None
+    rows = torch.arange(n, dtype=i64, device=d)
+    blk = torch.bucketize(rows, seg[1:], right=True)
+    halves = []
+    bad = torch.full((1,), INT_MAX, dtype=I32, device=d)
+    for fac, lev, nlev, up in ((lower, lev_l, nlev_l, False), (upper, lev_u, nlev_u, True)):
+        lv = lev[:n].to(i64)
+        key = blk * nlev + lv
+        order = torch.argsort(key, stable=True)
+        cnt = torch.bincount(key, minlength=nb * nlev).view(nb, nlev)
+        lev_start = torch.cumsum(cnt, 1) - cnt
+        pib = torch.empty(n, dtype=i64, device=d)              # position in the block's level-major order
+        pib[order] = rows - seg[blk[order]]
+        ril = pib - lev_start.reshape(-1)[key]                 # rank of the row inside its level (rows of a level by index)
+        cs = torch.clamp((cnt + csize - 1) // csize, min=CSWEEP_MIN_CHUNK)        # chunk rows per (block, level)
+        csr = cs.reshape(-1)[key]
+        rk = ril // csr                                        # CTA of the row
+        ro = ril - rk * csr
+        ranks = torch.arange(csize, dtype=i64, device=d).view(1, csize, 1)
+        ncl = torch.clamp(cnt.view(nb, 1, nlev) - ranks * cs.view(nb, 1, nlev), min=0)
+        ncl = torch.minimum(ncl, cs.view(nb, 1, nlev).expand(nb, csize, nlev))    # rows of CTA (b, r) in level l
+        lend = torch.cumsum(ncl, 2)
+        lstart = lend - ncl
+        ckey = (blk * csize + rk) * nlev + lv
+        lpos = lstart.reshape(-1)[ckey] + ro
+        rows_cta = lend[:, :, -1].reshape(-1)
+        padded = (rows_cta + 31) // 32 * 32
+        base = torch.cumsum(padded, 0) - padded
+        npos = int(padded.sum().item())
+        gpos = base[blk * csize + rk] + lpos
+        cta = blk * csize + rk                                 # CTA of every row
+        nnz = fac.nnz
+        rlen = (fac.rp[1:] - fac.rp[:-1]).to(i64)
+        erow = torch.repeat_interleave(rows, rlen)
+        ecol = fac.ci[:nnz].to(i64)
+        if bool((blk[ecol] != blk[erow]).any().item()):
+            return None
+        dep = ecol != erow
+        # halo: (consumer CTA, producer row) pairs whose CTAs differ; a CTA numbers the values it holds level by
+        # level -- own rows of the level, then the level's halo values (in row order)
+        remote = dep & (cta[erow] != cta[ecol])
+        hkey_e = cta[erow] * n + ecol
+        hu = torch.unique(hkey_e[remote])                      # sorted by (consumer CTA, producer row)
+        h_cta, h_row = hu // n, hu % n
+        h_lev = lv[h_row]
+        gkey = h_cta * nlev + h_lev
+        n_in = torch.bincount(gkey, minlength=nb * csize * nlev).view(nb, csize, nlev)
+        gorder = torch.argsort(gkey, stable=True)
+        gstart = (torch.cumsum(n_in.reshape(-1), 0) - n_in.reshape(-1))
+        h_idx = torch.empty_like(gkey)
+        h_idx[gorder] = torch.arange(gkey.numel(), dtype=i64, device=d) - gstart[gkey[gorder]]
+        n_ext = ncl + n_in
+        wend = torch.cumsum(n_ext, 2)                          # window positions: end of every level per CTA
+        wstart = wend - n_ext
+        wpos = wstart.reshape(-1)[ckey] + ro                   # own rows
+        h_wpos = wstart.reshape(-1)[gkey] + ncl.reshape(-1)[gkey] + h_idx
+        # window slot of every dependency in the READER's CTA, and how far back it lies
+        e_wpos = wpos[ecol]
+        if hu.numel():
+            hit = torch.searchsorted(hu, hkey_e[remote])
+            e_wpos = e_wpos.clone()
+            e_wpos[remote] = h_wpos[hit]
+        need = torch.where(dep, wend.reshape(-1)[cta[erow] * nlev + lv[erow]] - e_wpos, torch.zeros_like(ecol))
+        max_need = int(need.max().item()) if nnz else 1
+        # push targets of every row: the other CTAs that hold its value, (slot << 4 | rank)
+        NP = query("ddilu_csweep_max_push")
+        porder = torch.argsort(h_row, stable=True)
+        prow = h_row[porder]
+        pidx = torch.arange(prow.numel(), dtype=i64, device=d) - torch.searchsorted(prow, prow)
+        max_push = int(pidx.max().item()) + 1 if prow.numel() else 0
+        nz = cnt > 0
+        nlev_b = torch.where(nz.any(1), nlev - torch.flip(nz, [1]).to(i64).argmax(1), torch.zeros(nb, dtype=i64, device=d))
+        max_lev = int(nlev_b.max().item())
+        width_cta = int(ncl.max().item())
+        # chunks that are ranges of consecutive rows need no row ids
+        row_lo = torch.full((nb * csize * nlev,), n, dtype=i64, device=d).scatter_reduce_(0, ckey, rows, "amin")
+        row_hi = torch.full((nb * csize * nlev,), -1, dtype=i64, device=d).scatter_reduce_(0, ckey, rows, "amax")
+        nclf = ncl.reshape(-1)
+        consecutive = (nclf == 0) | (row_hi - row_lo + 1 == nclf)
+        contiguous = bool(consecutive.all().item())
+        row0 = torch.where((nclf > 0) & consecutive, row_lo, torch.full_like(row_lo, -1))
+        NT = query("ddilu_csweep_threads", int(up), nset)
+        # steps: a CTA's chunk of a level, cut into pieces of at most one row per thread; the first piece waits for
+        # the previous level, the last one signals
+        nsub = torch.clamp((nclf + NT - 1) // NT, min=1)
+        # levels behind the block's last one do not exist for the kernel
+        live = (torch.arange(nlev, dtype=i64, device=d).view(1, 1, nlev) < nlev_b.view(nb, 1, 1)).expand(nb, csize, nlev).reshape(-1)
+        nsub = torch.where(live, nsub, torch.zeros_like(nsub))
+        steps_cta = nsub.view(nb * csize, nlev).sum(1)
+        max_steps = int(steps_cta.max().item())
+        if debug:
+            print(f"cluster sweep plan ({'U' if up else 'L'}): k {k}, cluster {csize}, furthest dependency {max_need} "
+                  f"(window {W}), widest level per CTA {width_cta} ({NT} threads, <= {max_steps} steps), levels per block {max_lev}, "
+                  f"positions {npos} for {n} rows, halo values {hu.numel()}, push targets per row <= {max_push}, "
+                  f"consecutive chunks: {contiguous}", flush=True)
+        if max_need > W or max_push > NP or query("ddilu_csweep_smem_bytes", int(up), nset, max_steps) > 227 * 1024:
+            return None
+        tot = int(nsub.sum().item())
+        src = torch.repeat_interleave(torch.arange(nsub.numel(), dtype=i64, device=d), nsub)    # (CTA, level) of a step
+        first = torch.cumsum(nsub, 0) - nsub
+        e = torch.arange(tot, dtype=i64, device=d) - first[src]                                  # piece index
+        s_start = lstart.reshape(-1)[src] + e * NT
+        s_end = torch.minimum(lend.reshape(-1)[src], s_start + NT)
+        s_slot = (wstart.reshape(-1)[src] + e * NT) % W
+        s_row0 = torch.where(row0[src] >= 0, row0[src] + e * NT, row0[src])
+        is_first, is_last = e == 0, e == nsub[src] - 1
+        s_tx = torch.where(is_first, 8 * n_in.reshape(-1)[src], torch.zeros_like(e))
+        s_flags = is_first.to(i64) + 2 * is_last.to(i64)
+        zero = torch.zeros_like(e)
+        steps = torch.stack([s_start, s_end, s_slot, s_row0, s_tx, s_flags, zero, zero], 1)
+        ctas = torch.zeros((nb * csize, 4), dtype=i64, device=d)
+        ctas[:, 0], ctas[:, 1] = base, rows_cta
+        ctas[:, 2] = torch.cumsum(steps_cta, 0) - steps_cta
+        ctas[:, 3] = steps_cta
+        RB = query("ddilu_csweep_record_bytes", int(up))
+        recs = torch.zeros(npos * RB, dtype=torch.uint8, device=d)
+        halves16 = recs.view(torch.int16).view(npos, RB // 2)                     # a record's halves start at byte 32
+        halves16[:, 16 + k:16 + k + NP] = -1                                      # 0xffff: no push target
+        if prow.numel():
+            pcode = ((h_wpos[porder] % W) << 4) | (h_cta[porder] % csize)
+            halves16.view(-1)[gpos[prow] * (RB // 2) + 16 + k + pidx] = pcode.to(torch.int32).to(torch.int16)
+        rowid = torch.zeros(npos, dtype=I32, device=d)
+        call("ddilu_csweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos.to(I32).contiguous(),
+             (e_wpos % W).to(I32).contiguous(), recs, rowid, bad)
+        halves.append(ClusterSweepHalf(ctas.to(I32).contiguous().view(-1), steps.to(I32).contiguous().view(-1),
+                                       recs, rowid, npos, max_steps, contiguous))
+    return ClusterSweepPlan(n, nb, csize, k, nset, halves[0], halves[1], int(bad.item()))
+
+
+def csweep_solve(cp: ClusterSweepPlan, upper: bool, b: torch.Tensor, out: torch.Tensor, check: bool = False):
+    """out = L^-1 b (upper False) or U^-1 b (upper True) on the cluster-sweep layout (vectors by row)."""
+    if check and upper and cp.bad_row != INT_MAX:
+        raise TriSolveError(f"zero or missing diagonal at row {cp.bad_row}")
+    h = cp.upper if upper else cp.lower
+    call("ddilu_csweep_solve", cp.n_blocks, cp.csize, h.ctas, h.steps, h.recs, h.rowid, h.np, cp.k, int(upper),
+         h.max_steps, cp.nset, b, out)
+    return out
+
+
+# ---------------------------------------------------------------------------
 # tile sweep (csrc/experiments/tsweep.cu): interior factors with vectors in tile order.  EXPERIMENT (needs a
 # DDILU_EXPERIMENTS=1 build; scripts/probe_tsweep.py): bit-exact, 0.62-0.66 of the HBM roofline when the tiles
 # are made independent, but 0.30 / 0.42 (L / U) with the real tile dependencies -- 16^3 tiles leave ~190 tiles

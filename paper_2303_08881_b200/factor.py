@@ -86,6 +86,7 @@ class DevFactors:
         self._tl = self._tu = None  # tiled layouts (D.TileSched) when the factor tiles
         self._bw = None             # (L, U) shared-memory-window plans of the block-local sweep
         self._sw = None             # D.SweepPlan: one CTA per diagonal block (interface factors)
+        self._cs = None             # D.ClusterSweepPlan: one thread-block cluster per diagonal block (interior factors)
         self._tmp = None
 
     @property
@@ -109,11 +110,19 @@ class DevFactors:
             self._su = D.build_schedule(self.upper, True, *self._lev(True))
         return self._su
 
-    def prepare(self, seg_ptr=None, part: "D.TilePartition | None" = None):
+    def prepare(self, seg_ptr=None, part: "D.TilePartition | None" = None, cluster_seg=None):
         """Build the solve layouts now (inside setup).  part: tile partition of the
         rows (structured problems) -> tiled solve, with the sync-free SELL solve as the
         fallback when the tile graph is not one-way.  seg_ptr: row ranges of independent
-        diagonal blocks (one per subdomain), if known."""
+        diagonal blocks (one per subdomain), if known.  cluster_seg: the same for LARGE blocks
+        (interior factors) -> cluster sweep when the pair qualifies; part may then be a callable
+        () -> partition so that the tiles are only built when they are needed."""
+        if cluster_seg is not None and D.USE_CSWEEP and self.n:
+            self._cs = D.build_csweep(self.lower, self.upper, *self._lev(False), *self._lev(True), cluster_seg)
+            if self._cs is not None:
+                return self
+        if getattr(part, "lazy", False):
+            part = part()
         if seg_ptr is not None and D.USE_SWEEP and self.n:
             # small, deep, block-diagonal (the interface factors): one CTA per block walks the levels in shared
             # memory, L and U in one launch (csrc/sweep.cu); the other layouts are then built only on demand
@@ -161,6 +170,8 @@ class DevFactors:
         return self
 
     def lower_solve(self, b, out):
+        if self._cs is not None:
+            return D.csweep_solve(self._cs, False, b, out)
         if self._sw is not None:
             D.sweep_rhs(self._sw, False, b)
             return D.sweep_solve(self._sw, 1, out)
@@ -171,6 +182,8 @@ class DevFactors:
         return D.sptrsv(self.lower, self.sched_l, b, out, False, True)
 
     def upper_solve(self, b, out):
+        if self._cs is not None:
+            return D.csweep_solve(self._cs, True, b, out)
         if self._sw is not None:
             D.sweep_rhs(self._sw, True, b)
             return D.sweep_solve(self._sw, 2, out)

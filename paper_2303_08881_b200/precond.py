@@ -133,6 +133,13 @@ class LocalSystem:
         slab.fallback = box
         return slab
 
+    def lazy_tile_part_interior(self):
+        """tile_part_interior, built on first use (the cluster sweep does not need tiles)."""
+        def make():
+            return self.tile_part_interior()
+        make.lazy = True
+        return make
+
     def _ext_partition(self, max_rows: int, int_keys, int_range: int):
         """Box tiles of the interface rows with at most max_rows rows each (edge 32, 16, ... until it
         fits); with int_keys the interior rows (keys below int_range) are partitioned along."""
@@ -515,7 +522,7 @@ class SchurIluPrecond(_DDPrecond):
         s = self.system
         self.rule, self.inner_iters = rule, inner_iters
         self._p = d_partial_ilu(s.a_dom, s.n_int, rule, schur_drop_tol=schur_drop_tol, factor_schur=True)
-        self._p.interior.prepare(part=s.tile_part_interior())
+        self._p.interior.prepare(part=s.lazy_tile_part_interior(), cluster_seg=s.int_ptr)
         self._p.schur.prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))   # interface factors: one block per subdomain
         self._coupling = s.coupling()
         ne, nh = s.n_ext, s.n_halo
@@ -635,7 +642,7 @@ class RapIluPrecond(_DDPrecond):
         else:
             coarse = plain
         l_b, u_b, w, z, l_s, u_s = d_carve(coarse, s.n_int)
-        self._interior = DevFactors(l_b, u_b).prepare(part=s.tile_part_interior())
+        self._interior = DevFactors(l_b, u_b).prepare(part=s.lazy_tile_part_interior(), cluster_seg=s.int_ptr)
         self._w, self._zt = w, z
         self._ztc = D.compact_rows(z) if COMPACT_Z else None
         self._schur = DevFactors(l_s, u_s).prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))
