@@ -172,27 +172,27 @@ int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const 
  * into chunks, one per CTA; a CTA keeps the values it needs (own results and halo values of other CTAs) in a
  * shared-memory window; a producer pushes a result into the windows of the other CTAs that need it through
  * distributed shared memory (st.async completing bytes on the consumer's mbarrier); one mbarrier wait per level.
- * ddilu_csweep_fill: the rows' records in CTA-local schedule order (k = operand slots per row: 3 or 4; gpos =
- * position of the row in the record array, dep_slot = per stored entry the window slot of that dependency in the
- * READER's CTA).  A record is record_bytes(upper) = 48 / 64 bytes: c[4] | 8 halves: the k dependency slots (filled
- * here), then max_push push targets slot << 4 | rank, 0xffff = none (filled by the caller) | upper: pivot, 1 / pivot.
+ * ddilu_csweep_fill: operands of a factor in CTA-local schedule order (k = operand slots per row: 3 or 4;
+ * gpos = position of the row in the operand arrays, dep_slot = per stored entry the window slot of that dependency
+ * in the READER's CTA; np = length of the position space; coef[k][np]; code[code_words(k)][np]: the 16-bit halves
+ * of a row's words are its k dependency slots (filled here) and then its max_push push targets slot << 4 | rank,
+ * 0xffff = none (filled by the caller); rowid[np]; piv[2][np] = pivot and its reciprocal (upper only)).
  * ddilu_csweep_solve: ctas = 4 ints per CTA {first position, rows, first step, steps}; steps = 8 ints per step
- * {start, end (positions, at most `threads` rows), window slot of the first row, first row when the rows are
- * consecutive else -1 (rowid is read), halo bytes arriving for the level (first step of a level), flags 1 = first |
- * 2 = last step of its level, 0, 0}; depth = stages of the operand ring (2..4): operands are requested depth - 1
- * steps ahead. */
-int ddilu_csweep_threads(int upper, int depth);
+ * {start (a multiple of 4), end (positions, at most `threads` rows), window slot of the first row, first row when
+ * the rows are consecutive else -1 (rowid is read), halo bytes arriving for the level (first step of a level),
+ * flags 1 = first | 2 = last step of its level, 0, 0}; depth = stages of the operand ring (2..4). */
+int ddilu_csweep_threads(void);
 int ddilu_csweep_window(void);
 int ddilu_csweep_max_push(void);
-int ddilu_csweep_record_bytes(int upper);
-long long ddilu_csweep_smem_bytes(int upper, int depth, int max_steps);
-int ddilu_csweep_active_clusters(int cluster_size, int depth, int max_steps);
+int ddilu_csweep_code_words(int k);
+long long ddilu_csweep_smem_bytes(int k, int upper, int depth, int max_steps);
+int ddilu_csweep_active_clusters(int cluster_size, int k, int depth, int max_steps);
 int ddilu_csweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
-                      const int *gpos, const int *dep_slot, unsigned char *recs, int *rowid, int *bad_row,
-                      void *stream);
-int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps, const unsigned char *recs,
-                       const int *rowid, long long np, int k, int upper, int max_steps, int depth, const double *b,
-                       double *out, void *stream);
+                      const int *gpos, const int *dep_slot, long long np, double *coef, unsigned *code, int *rowid,
+                      double *piv, int *bad_row, void *stream);
+int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps, const double *coef,
+                       const unsigned *code, const int *rowid, const double *piv, long long np, int k, int upper,
+                       int max_steps, int depth, const double *b, double *out, void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,

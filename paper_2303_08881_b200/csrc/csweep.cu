@@ -19,8 +19,9 @@
 //     together, no fence, no cluster-scope release (barrier.cluster.arrive.release costs a MEMBAR.ALL.GPU per
 //     level, ~700 cycles: measured);
 //   * ONE mbarrier wait per level: the phase of level l completes when all warps of the own CTA have stored their
-//     level-l rows, all halo bytes of level l have landed (expect_tx) and every warp of every other CTA has
-//     finished level l (a token arrive -- the flow control that makes the window slots safe to overwrite);
+//     level-l rows, all halo bytes of level l have landed (expect_tx) and every warp of every CTA this one exchanges
+//     values with has finished level l (a token arrive -- the flow control that makes the window slots safe to overwrite;
+//     CTAs that exchange nothing are not coupled);
 //   * operands are one 48-byte record per row (4 coefficients, 8 halves: K slots and <= 3 push targets; + the pivot
 //     pair for U; the row id only when a level chunk is not a contiguous row range) in the CTA's schedule order and
 //     travel to thread-private shared-memory slots by cp.async, D - 1 steps ahead (coalesced); a step is at
@@ -41,35 +42,41 @@ namespace ddilu {
 constexpr int CS_WINDOW = 4095;       // doubles per CTA; slot CS_WINDOW holds 0.0
 constexpr int CS_STEP_INTS = 8;       // per CTA and step: first / end operand position, window slot of the first row,
                                       // first row (-1: row ids), halo bytes of the level, flags, 0, 0
-constexpr int CS_CTA_INTS = 4;        // per CTA: first position in the operand arrays, rows, offset into steps, number of steps
+constexpr int CS_CTA_INTS = 4;        // per CTA: first position in the operand arrays, signal mask | arrivals << 16, first step, number of steps
 constexpr int CS_NP = 3;              // push targets per row
 constexpr unsigned CS_NO_PUSH = 0xffffu;
 constexpr int CS_WAIT = 1, CS_ARRIVE = 2;   // step flags: first / last step of its level
-constexpr int CS_REC = 48;            // bytes of a row's record without the pivot pair
+constexpr int CS_NT = 768;            // compute threads of a CTA = rows of a step at most; one more warp feeds the ring
+constexpr int CS_THREADS = CS_NT + 32;
+constexpr int CS_MAX_DEPTH = 4;
+__host__ __device__ constexpr int cs_words(int K) { return (K + CS_NP + 1) / 2; }   // 32-bit words holding a row's K slots and CS_NP push targets
 
 struct CSweepArgs {
     const int *ctas;                  // CS_CTA_INTS per CTA (block-major, rank-minor)
     const int *steps;                 // CS_STEP_INTS per CTA and step
-    const unsigned char *recs;        // [np] records of 48 (lower) / 64 (upper) bytes: c[4] | 8 halves: K window slots of the
-                                      // dependencies, then CS_NP push targets slot << 4 | rank (0xffff = none) | upper: d, 1/d
+    const double *coef;               // [K][np]
+    const unsigned *code;             // [cs_words(K)][np]: 16-bit halves = K window slots of the dependencies, then CS_NP
+                                      // push targets slot << 4 | rank (0xffff = none)
     const int *rowid;                 // [np]
+    const double *piv;                // [2][np]: pivot, reciprocal (upper)
     const double *b;                  // right-hand side by row
     double *out;                      // results by row
     long long np;
     int max_steps;
+    int depth;                        // stages of the operand ring
     long long *dbg;                   // experiments build: 16 cycle counters per CTA and probe thread (first, last)
 };
 
-__host__ __device__ constexpr int cs_threads(bool upper, int depth) {
-    return (upper && depth > 3) ? 640 : 768;
+// a stage of the operand ring (structure of arrays, slot = row of the step):
+// coef[K][NT] | pivot pairs[2][NT] (upper) | rhs[NT + 2] | words[NW][NT] | row ids[NT]
+__host__ __device__ constexpr int cs_stage_bytes(int K, bool upper) {
+    return CS_NT * (8 * K + (upper ? 16 : 0) + 4 * cs_words(K) + 4) + 8 * (CS_NT + 2);
 }
-// a stage of the operand ring: per thread the row's record, right-hand side, pivot pair (upper)
-__host__ __device__ constexpr int cs_stage_bytes(bool upper, int threads) {
-    return threads * (CS_REC + 8 + (upper ? 16 : 0));
-}
-__host__ __device__ inline size_t cs_smem_bytes(bool upper, int depth, int max_steps) {
-    return 16 + (size_t)max_steps * CS_STEP_INTS * 4 + ((size_t)CS_WINDOW + 1) * 8 +
-           (size_t)depth * cs_stage_bytes(upper, cs_threads(upper, depth));
+__host__ __device__ inline size_t cs_ctl_bytes() { return (2 + 2 * CS_MAX_DEPTH) * 8; }   // level pair, full[], empty[]
+__host__ __device__ inline size_t cs_smem_bytes(int K, bool upper, int depth, int max_steps) {
+    size_t b = cs_ctl_bytes() + (size_t)max_steps * CS_STEP_INTS * 4 + ((size_t)CS_WINDOW + 1) * 8;
+    b = (b + 127) & ~(size_t)127;
+    return b + (size_t)depth * cs_stage_bytes(K, upper);
 }
 
 __device__ __forceinline__ uint32_t cs_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -87,17 +94,24 @@ __device__ __forceinline__ double cs_lds(uint32_t a) {
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
     return v;
 }
+template <int OFF>
+__device__ __forceinline__ double cs_lds_at(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ uint32_t cs_lds_u32_at(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+}
 __device__ __forceinline__ void cs_sts(uint32_t a, double v) {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 __device__ __forceinline__ int4 cs_lds_v4(uint32_t a) {
     int4 v;
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ int2 cs_lds_v2(uint32_t a) {
-    int2 v;
-    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
     return v;
 }
 // a result into another CTA's window, completing 8 bytes on that CTA's mbarrier
@@ -111,6 +125,12 @@ __device__ __forceinline__ void cs_mbar_init(uint32_t bar, int count) {
 }
 __device__ __forceinline__ void cs_mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cs_mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cs_mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 // arrive on the mbarrier of a CTA of the cluster (own included); release.cta orders the warp's window stores before
 // the arrive for the readers of the own CTA -- other CTAs get their data through cs_push
@@ -127,285 +147,273 @@ __device__ __forceinline__ void cs_mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
-// operand loads: read once, keep them out of L1
-__device__ __forceinline__ double cs_ldg_f64(const double *p) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
+// global -> shared memory, bytes a multiple of 16, both addresses 16-byte aligned; completes bytes on the mbarrier
+__device__ __forceinline__ void cs_bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
-__device__ __forceinline__ uint32_t cs_ldg_u32(const unsigned *p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
+__device__ __forceinline__ void cs_cp_async8(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ int cs_ldg_s32(const int *p) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ uint32_t cs_lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-// global -> shared memory without a register (and without a scoreboard): completion by cp.async.wait_group
-__device__ __forceinline__ void cs_cp_async8(uint32_t dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cs_cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ double2 cs_lds_f64x2(uint32_t a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint4 cs_lds_u32x4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
-    return v;
-}
 __device__ __forceinline__ uint32_t cs_half(const uint32_t *w, int i) {     // 16-bit half i of the packed words
     return (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu);
 }
 
-// the registers of one step of one thread
-template <int K>
-struct CsRow {
-    double c[K], rhs, d, r;
-    uint32_t ad[K];           // shared-memory addresses of the dependencies
-    uint32_t push[2];         // halves K .. K + 2 of the record's tail: push targets (K = 3: halves 3, 4, 5; K = 4: 4, 5, 6)
-    int id, slot;             // row (CS_NO_ROW: the thread has no row in the step), window slot (before wrap-around)
-};
-constexpr int CS_NO_ROW = (int)0x80000000;
-
 // One CTA of the cluster that owns block blockIdx.x / cluster size.  A CTA walks its STEPS: a step is (a part of)
-// the CTA's chunk of a level, at most one row per thread -- levels wider than the CTA are cut into several steps at
-// setup; only the first step of a level waits, only the last one signals.  Thread t owns row t of every step.
-// Operands travel global -> shared memory by cp.async (16-byte pieces of the row's record into thread-private
-// slots of a D-deep stage ring, D - 1 steps ahead; completion by cp.async.wait_group, i.e. NOT through the six
-// register scoreboards of a warp: operands prefetched into registers made every consumer wait for the youngest
-// load in flight), and shared memory -> registers one step ahead:
-// iteration i   B: operands of step i + 1 from the ring into registers, slots -> shared-memory addresses
-//               A: operands of step i + D requested
-//               C: (first step of a level) mbarrier phase of the previous level: own rows stored, halo landed,
-//                  every warp of the cluster past it
-//               D: the row: K window loads, multiply / subtract chain [, division], window store, pushes
-//               E: (last step of a level) arrive at every CTA's mbarrier of the level; result to global memory
-template <int K, bool UPPER, int D>
-__global__ void __launch_bounds__(cs_threads(UPPER, D), 1) csweep_kernel(const CSweepArgs a) {
-    constexpr int NT = cs_threads(UPPER, D);
-    constexpr int STAGE = cs_stage_bytes(UPPER, NT);
-    // stage layout (slot = thread): records[NT][48] | rhs[NT][8] | pivot pairs[NT][16] (upper)
-    constexpr int OFF_RHS = CS_REC * NT, OFF_PIV = OFF_RHS + 8 * NT;
-    extern __shared__ __align__(16) unsigned char cs_smem[];
+// the CTA's chunk of a level, at most one row per compute thread -- levels wider than the CTA are cut into several
+// steps at setup; only the first step of a level waits, only the last one signals.  Compute thread t owns row t of
+// every step; every warp instruction of its loop counts (24 warps share four schedulers), so the operands do NOT
+// come by per-thread loads: lane 0 of the feeder warp streams every operand array of a step into a stage of a
+// shared-memory ring with one bulk copy each (steps start at multiples of 4 positions, so every run is 16-byte
+// aligned), `depth` steps ahead, and a compute thread takes its operands with plain shared-memory loads.
+// per step      feeder: wait until the stage is free, bulk copies with complete_tx on full[stage]
+//               compute: wait full[stage]; operands -> registers; arrive empty[stage];
+//                        (first step of a level) wait for the mbarrier phase of the previous level: own rows
+//                        stored, halo landed, every warp of the cluster past it;
+//                        K window loads, multiply / subtract chain [, division], window store, pushes;
+//                        (last step of a level) arrive at every CTA's mbarrier of the level; result to global memory
+template <int K, bool UPPER>
+__global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs a) {
+    constexpr int NT = CS_NT;
+    constexpr int NW = cs_words(K);
+    constexpr int STAGE = cs_stage_bytes(K, UPPER);
+    constexpr int OFF_PIV = 8 * K * NT, OFF_RHS = OFF_PIV + (UPPER ? 16 * NT : 0), OFF_W = OFF_RHS + 8 * (NT + 2),
+                  OFF_ID = OFF_W + 4 * NW * NT;
+    extern __shared__ __align__(128) unsigned char cs_smem[];
     const int *cta = a.ctas + CS_CTA_INTS * blockIdx.x;
     uint32_t csize;
     asm volatile("mov.u32 %0, %%cluster_nctaid.x;" : "=r"(csize));
     const long long base = cta[0];
     const int step_off = cta[2], nsteps = cta[3];
+    // the CTAs this one signals at the end of a level (itself and the CTAs it exchanges values with, a symmetric
+    // relation: a producer must know that its consumer is done reading before it overwrites the consumer's window
+    // slots, and a coupled pair stays within one level of each other), and how many CTAs signal this one
+    const uint32_t sigmask = (uint32_t)cta[1] & 0xffffu;
+    const int signallers = cta[1] >> 16;
     const int tid = threadIdx.x, lane = tid & 31;
-    uint64_t *bars = (uint64_t *)cs_smem;                     // [2]: levels of even / odd index
-    int4 *steps = (int4 *)(cs_smem + 16);
-    double *xs = (double *)(cs_smem + 16 + (size_t)a.max_steps * CS_STEP_INTS * 4);
-    unsigned char *ring = (unsigned char *)(xs + CS_WINDOW + 1);
+    const int D = a.depth;
+    uint64_t *bars = (uint64_t *)cs_smem;                     // [2]: levels of even / odd index, then full[], empty[]
+    int4 *steps = (int4 *)(cs_smem + cs_ctl_bytes());
+    double *xs = (double *)((unsigned char *)steps + (size_t)a.max_steps * CS_STEP_INTS * 4);
+    size_t ring_off = cs_ctl_bytes() + (size_t)a.max_steps * CS_STEP_INTS * 4 + ((size_t)CS_WINDOW + 1) * 8;
+    ring_off = (ring_off + 127) & ~(size_t)127;
     {
         const int4 *src = (const int4 *)a.steps + 2 * (size_t)step_off;
-        for (int i = tid; i < 2 * nsteps; i += NT) steps[i] = src[i];
+        for (int i = tid; i < 2 * nsteps; i += CS_THREADS) steps[i] = src[i];
     }
-    const uint32_t bar_u32 = cs_smem_u32(bars);
+    const uint32_t bar_u32 = cs_smem_u32(bars), full_u32 = bar_u32 + 16, empty_u32 = full_u32 + 8 * CS_MAX_DEPTH;
     if (tid == 0) {
         xs[CS_WINDOW] = 0.0;                  // padded operands: coefficient 0 times this slot
-        cs_mbar_init(bar_u32, (NT / 32) * (int)csize);
-        cs_mbar_init(bar_u32 + 8, (NT / 32) * (int)csize);
+        cs_mbar_init(bar_u32, (NT / 32) * signallers);
+        cs_mbar_init(bar_u32 + 8, (NT / 32) * signallers);
+        for (int s = 0; s < D; ++s) {
+            cs_mbar_init(full_u32 + 8 * s, 2);    // the feeder's arrive.expect_tx and its asynchronous cp.async arrive
+            cs_mbar_init(empty_u32 + 8 * s, NT / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     cs_cluster_sync();                        // every CTA of the cluster is running, its mbarriers are initialised
-    const uint32_t st_u32 = cs_smem_u32(steps), xs_u32 = cs_smem_u32(xs);
-    const uint32_t rec_u32 = cs_smem_u32(ring) + (uint32_t)(CS_REC * tid);     // this thread's slots of stage 0
-    const uint32_t rhs_u32 = cs_smem_u32(ring) + OFF_RHS + 8u * (uint32_t)tid;
-    const uint32_t piv_u32 = cs_smem_u32(ring) + OFF_PIV + 16u * (uint32_t)tid;
-    const unsigned char *recs = a.recs + (size_t)base * (UPPER ? CS_REC + 16 : CS_REC);
-    const int *ids = a.rowid + base;
-    // lane r < cluster size signals CTA r: the address of that CTA's mbarrier pair
-    const uint32_t peer_bar = cs_mapa(bar_u32, (uint32_t)lane < csize ? (uint32_t)lane : 0u);
-    const bool signals = (uint32_t)lane < csize;
+    const uint32_t st_u32 = cs_smem_u32(steps), xs_u32 = cs_smem_u32(xs), ring_u32 = cs_smem_u32(cs_smem + ring_off);
+    const long long np = a.np;
 
-    // A: request the operands of step i into a stage (an empty group when the warp has no row there).  The records
-    // of a warp's 32 rows are one contiguous run in global memory AND in the stage: lane j copies the 16-byte
-    // pieces j, j + 32, ... of the run (fully coalesced) -- a thread's record is assembled by its whole warp, so
-    // fetch() synchronises the warp behind its wait
-    constexpr int PIECES = UPPER ? 4 : 3;     // 16-byte pieces of a record in global memory (the 4th: pivot pair)
-    const uint32_t wrec_u32 = cs_smem_u32(ring) + (uint32_t)(CS_REC * (tid - lane));      // stage 0 slots of the warp's lane 0
-    const uint32_t wpiv_u32 = cs_smem_u32(ring) + OFF_PIV + 16u * (uint32_t)(tid - lane);
-    auto issue = [&](int i, uint32_t stage_off) {
-        if (i < nsteps) {
-            const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
-            const int p0 = sv.x + tid - lane;                 // position of the warp's first row
-            const int rows = min(32, sv.y - p0);              // rows of the warp in this step
-            if (rows > 0) {
-                const unsigned char *g = recs + (size_t)p0 * (16 * PIECES);
-#pragma unroll
-                for (int q = 0; q < PIECES; ++q) {
-                    const int m = lane + 32 * q;              // piece of the run
-                    if (m < rows * PIECES) {
-                        const int t = UPPER ? m >> 2 : m / 3, o = UPPER ? m & 3 : m - 3 * t;      // row of the warp, piece of its record
-                        const uint32_t dst = (UPPER && o == 3) ? wpiv_u32 + 16u * (uint32_t)t : wrec_u32 + (uint32_t)(CS_REC * t + 16 * o);
-                        cs_cp_async16(dst + stage_off, g + 16 * m);
+    if (tid >= NT) {
+        // ------------------------------------------------------------ feeder (one lane)
+        if (lane == 0) {
+            const double *cf = a.coef + base;
+            const unsigned *cd = a.code + base;
+            const int *ids = a.rowid + base;
+            const double *pv = a.piv + base;
+            int s = 0;
+            uint32_t round = 0;               // how often the ring has wrapped
+            for (int i = 0; i < nsteps; ++i) {
+                const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
+                const int rows = sv.y - sv.x;
+                const uint32_t st = ring_u32 + (uint32_t)(s * STAGE), full = full_u32 + 8u * (uint32_t)s;
+                if (round) cs_mbar_wait(empty_u32 + 8u * (uint32_t)s, (round - 1) & 1u);
+                if (rows > 0) {
+                    const uint32_t r4 = (uint32_t)(rows + 3) & ~3u;                 // whole 16-byte pieces of every array
+                    uint32_t tx = r4 * (uint32_t)(8 * K + 4 * NW + (UPPER ? 16 : 0));
+                    uint32_t nb_bulk = 0;
+                    const double *bsrc = nullptr;
+                    uint32_t bdst = 0;
+                    if (sv.w >= 0) {
+                        // right-hand side b[row0 .. row0 + rows): element j of the step lands at rhs[j + head] with
+                        // head = row0 & 1 -- the 16-byte aligned run by one bulk copy, an odd head / tail element by
+                        // an 8-byte cp.async of this thread (signalled through the asynchronous arrive below)
+                        const int head = sv.w & 1;
+                        const int body = (rows - head) & ~1;
+                        bsrc = a.b + sv.w + head;
+                        bdst = st + OFF_RHS + 8u * (uint32_t)(2 * head);
+                        nb_bulk = 8u * (uint32_t)body;
+                        tx += nb_bulk;
+                        if (head) cs_cp_async8(st + OFF_RHS + 8u, a.b + sv.w);
+                        if (head + body < rows) cs_cp_async8(st + OFF_RHS + 8u * (uint32_t)(head + rows - 1), a.b + sv.w + rows - 1);
+                    } else {
+                        tx += r4 * 4u;
                     }
-                }
-                if (lane < rows && sv.w >= 0) cs_cp_async8(rhs_u32 + stage_off, a.b + sv.w + tid);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    // B: the operands of step i (requested D - 1 iterations ago) from their stage into registers
-    auto fetch = [&](int i, uint32_t stage_off, CsRow<K> &x) {
-        x.id = CS_NO_ROW;
-        if (i >= nsteps) return;
-        asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
-        __syncwarp();                         // the record was copied by the other lanes of the warp
-        const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
-        const int p = sv.x + tid;
-        if (p < sv.y) {
-            x.slot = sv.z + tid;
-            const double2 c01 = cs_lds_f64x2(rec_u32 + stage_off), c23 = cs_lds_f64x2(rec_u32 + stage_off + 16u);
-            const uint4 h = cs_lds_u32x4(rec_u32 + stage_off + 32u);
-            x.c[0] = c01.x, x.c[1] = c01.y, x.c[2] = c23.x;
-            if (K > 3) x.c[3] = c23.y;
-            if (UPPER) {
-                const double2 dr = cs_lds_f64x2(piv_u32 + stage_off);
-                x.d = dr.x, x.r = dr.y;
-            }
-            if (sv.w >= 0) {
-                x.id = sv.w + tid;
-                x.rhs = cs_lds(rhs_u32 + stage_off);
-            } else {                                    // rows by id: two dependent loads on the spot (rare layouts)
-                x.id = cs_ldg_s32(ids + p);
-                x.rhs = __ldg(a.b + x.id);
-            }
-            // halves: K slots, then the push targets
-            const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+                    // second arrival of the phase: when this thread's cp.async copies (if any) have landed
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+                    cs_mbar_arrive_tx(full, tx);
 #pragma unroll
-            for (int k = 0; k < K; ++k) x.ad[k] = xs_u32 + 8u * cs_half(w, k);
-            if (K == 3) x.push[0] = (h.y >> 16) | (h.z << 16), x.push[1] = h.z >> 16;      // halves 3, 4 | 5
-            else x.push[0] = h.z, x.push[1] = h.w & 0xffffu;                                // halves 4, 5 | 6
+                    for (int k = 0; k < K; ++k) cs_bulk_g2s(st + (uint32_t)(8 * k * NT), cf + (long long)k * np + sv.x, 8u * r4, full);
+#pragma unroll
+                    for (int k = 0; k < NW; ++k) cs_bulk_g2s(st + OFF_W + (uint32_t)(4 * k * NT), cd + (long long)k * np + sv.x, 4u * r4, full);
+                    if (UPPER) {
+                        cs_bulk_g2s(st + OFF_PIV, pv + sv.x, 8u * r4, full);
+                        cs_bulk_g2s(st + OFF_PIV + 8u * NT, pv + np + sv.x, 8u * r4, full);
+                    }
+                    if (sv.w >= 0) {
+                        if (nb_bulk) cs_bulk_g2s(bdst, bsrc, nb_bulk, full);
+                    } else {
+                        cs_bulk_g2s(st + OFF_ID, ids + sv.x, 4u * r4, full);
+                    }
+                } else {
+                    cs_mbar_arrive(full);
+                    cs_mbar_arrive(full);
+                }
+                if (++s == D) {
+                    s = 0;
+                    ++round;
+                }
+            }
         }
-    };
-
+    } else {
+        // ------------------------------------------------------------ compute threads
+        // lane r signals CTA r when the mask says so: the address of that CTA's mbarrier pair
+        const bool signals = (uint32_t)lane < csize && ((sigmask >> lane) & 1u);
+        const uint32_t peer_bar = cs_mapa(bar_u32, signals ? (uint32_t)lane : 0u);
+        const uint32_t my8 = ring_u32 + 8u * (uint32_t)tid, my4 = ring_u32 + 4u * (uint32_t)tid;
 #ifdef DDILU_EXPERIMENTS
-    unsigned tq[6] = {0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
-    const bool probe = a.dbg && (tid == 0 || tid == NT - 1);
+        unsigned tq[6] = {0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+        const bool probe = a.dbg && (tid == 0 || tid == NT - 1);
 #define CS_TICK(i)                  \
     if (probe) {                    \
         t1 = (unsigned)clock();     \
         tq[i] += t1 - t0;           \
         t0 = t1;                    \
     }
+        if (probe) t0 = (unsigned)clock();
 #else
 #define CS_TICK(i)
 #endif
-    int lev = 0;                              // level of the current step
-    uint32_t stage_off = 0;                   // stage of the current step
-    // one step: `cur` holds its operands, `nxt` receives those of the next step
-    auto step = [&](int i, const CsRow<K> &cur, CsRow<K> &nxt) {
-        const uint32_t cur_stage = stage_off;
-        stage_off = stage_off + STAGE == (uint32_t)(D * STAGE) ? 0u : stage_off + STAGE;
-        const int2 tf = cs_lds_v2(st_u32 + 32u * (uint32_t)i + 16u);         // halo bytes of the level, flags
-        const uint32_t mybar = bar_u32 + 8u * (uint32_t)(lev & 1);           // phase of this level: own and (offset) peers'
-        // the halo bytes of the level (before this warp's arrive: the phase cannot complete without them)
-        if (tid == 0 && tf.x) cs_mbar_expect_tx(mybar, (uint32_t)tf.x);
-        CS_TICK(0)
-        fetch(i + 1, stage_off, nxt);
-        CS_TICK(1)
-        issue(i + D, cur_stage);              // the stage of step i is free: its operands are in registers
-        CS_TICK(2)
-        // previous level: own rows stored, halo landed, every warp of the cluster past it
-        if ((tf.y & CS_WAIT) && lev) cs_mbar_wait(bar_u32 + 8u * (uint32_t)((lev - 1) & 1), (uint32_t)(((lev - 1) >> 1) & 1));
-        CS_TICK(3)
-        double res = 0.0;
-        const bool have = cur.id != CS_NO_ROW;
-        if (have) {
-            double v[K];
+        int lev = 0;                          // level of the current step
+        int s = 0;
+        uint32_t round = 0;
+        for (int i = 0; i < nsteps; ++i) {
+            const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
+            const int4 tf = cs_lds_v4(st_u32 + 32u * (uint32_t)i + 16u);     // halo bytes of the level, flags
+            const uint32_t mybar = bar_u32 + 8u * (uint32_t)(lev & 1);       // phase of this level: own and (offset) peers'
+            // the halo bytes of the level (before this warp's arrive: the phase cannot complete without them)
+            if (tid == 0 && tf.x) cs_mbar_expect_tx(mybar, (uint32_t)tf.x);
+            const uint32_t so = (uint32_t)(s * STAGE);
+            const bool have = tid < sv.y - sv.x;
+            CS_TICK(0)
+            cs_mbar_wait(full_u32 + 8u * (uint32_t)s, round & 1u);
+            CS_TICK(1)
+            double c[K], rhs = 0.0, d = 1.0, r = 0.0;
+            uint32_t w[NW], ad[K];
+            int id = 0;
+            if (have) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = cs_lds(cur.ad[k]);
-            double sum = cur.rhs;
-            // -fmad=false: every product is rounded before it is subtracted
+                for (int k = 0; k < K; ++k) c[k] = cs_lds(my8 + so + (uint32_t)(8 * k * NT));
 #pragma unroll
-            for (int k = 0; k < K; ++k) sum -= cur.c[k] * v[k];
-            if (UPPER) sum = exact_div(sum, cur.d, cur.r);
-            int sl = cur.slot;
-            sl -= sl >= CS_WINDOW ? CS_WINDOW : 0;
-            cs_sts(xs_u32 + 8u * (uint32_t)sl, sum);
-            // to the other CTAs that need the value (rare: rows on the border of a chunk)
-            if ((cur.push[0] & cur.push[1]) != 0xffffffffu || false) {
+                for (int k = 0; k < NW; ++k) w[k] = cs_lds_u32_at<OFF_W>(my4 + so + (uint32_t)(4 * k * NT));
+                if (UPPER) {
+                    d = cs_lds_at<OFF_PIV>(my8 + so);
+                    r = cs_lds_at<OFF_PIV + 8 * NT>(my8 + so);
+                }
+                if (sv.w >= 0) {
+                    id = sv.w + tid;
+                    rhs = cs_lds_at<OFF_RHS>(my8 + so + 8u * (uint32_t)(sv.w & 1));
+                } else {                                // rows by id: a dependent load on the spot (rare layouts)
+                    id = (int)cs_lds_u32_at<OFF_ID>(my4 + so);
+                    rhs = __ldg(a.b + id);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) ad[k] = xs_u32 + 8u * cs_half(w, k);
+            }
+            // the stage may be refilled (the loads above have returned: their values were used)
+            __syncwarp();
+            if (lane == 0) cs_mbar_arrive(empty_u32 + 8u * (uint32_t)s);
+            if (++s == D) {
+                s = 0;
+                ++round;
+            }
+            CS_TICK(2)
+            // previous level: own rows stored, halo landed, every warp of the cluster past it
+            if ((tf.y & CS_WAIT) && lev) cs_mbar_wait(bar_u32 + 8u * (uint32_t)((lev - 1) & 1), (uint32_t)(((lev - 1) >> 1) & 1));
+            CS_TICK(3)
+            double res = 0.0;
+            if (have) {
+                double v[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) v[k] = cs_lds(ad[k]);
+                double sum = rhs;
+                // -fmad=false: every product is rounded before it is subtracted
+#pragma unroll
+                for (int k = 0; k < K; ++k) sum -= c[k] * v[k];
+                if (UPPER) sum = exact_div(sum, d, r);
+                int sl = sv.z + tid;
+                sl -= sl >= CS_WINDOW ? CS_WINDOW : 0;
+                cs_sts(xs_u32 + 8u * (uint32_t)sl, sum);
+                // to the other CTAs that need the value (rows on the border of a chunk)
 #pragma unroll
                 for (int k = 0; k < CS_NP; ++k) {
-                    const uint32_t pp = k == 0 ? (cur.push[0] & 0xffffu) : (k == 1 ? cur.push[0] >> 16 : (cur.push[1] & 0xffffu));
+                    const uint32_t pp = cs_half(w, K + k);
                     if (pp != CS_NO_PUSH) cs_push(cs_mapa(xs_u32 + 8u * (pp >> 4), pp & 15u), sum, cs_mapa(mybar, pp & 15u));
                 }
+                res = sum;
             }
-            res = sum;
+            CS_TICK(4)
+            if (tf.y & CS_ARRIVE) {
+                // this warp is through the level: one arrive per CTA of the cluster (lane r -> CTA r)
+                __syncwarp();
+                if (signals) cs_mbar_arrive_cluster(peer_bar + 8u * (uint32_t)(lev & 1));
+                ++lev;
+            }
+            // behind the arrive: the hand-over must not wait for the store
+            if (have) a.out[id] = res;
+            CS_TICK(5)
         }
-        CS_TICK(4)
-        if (tf.y & CS_ARRIVE) {
-            // this warp is through the level: one arrive per CTA of the cluster (lane r -> CTA r)
-            __syncwarp();
-            if (signals) cs_mbar_arrive_cluster(peer_bar + 8u * (uint32_t)(lev & 1));
-            ++lev;
+        // the last phase: nobody pushes into this CTA's window or signals its mbarriers any more
+        if (lev) cs_mbar_wait(bar_u32 + 8u * (uint32_t)((lev - 1) & 1), (uint32_t)(((lev - 1) >> 1) & 1));
+#ifdef DDILU_EXPERIMENTS
+        if (probe) {
+            long long *o = a.dbg + 16 * (2 * blockIdx.x + (tid ? 1 : 0));
+            for (int q = 0; q < 6; ++q) o[q] = tq[q];
         }
-        // behind the arrive: the hand-over must not wait for the store
-        if (have) a.out[cur.id] = res;
-        CS_TICK(5)
-    };
-
-    // prologue: D groups in flight, step 0 in registers
-#pragma unroll
-    for (int s = 0; s < D; ++s) issue(s, (uint32_t)(s * STAGE));
-    CsRow<K> r0, r1;
-    fetch(0, 0, r0);
-#ifdef DDILU_EXPERIMENTS
-    if (probe) t0 = (unsigned)clock();
-#endif
-    for (int i = 0; i < nsteps; i += 2) {     // two register sets take the steps in turn
-        step(i, r0, r1);
-        if (i + 1 < nsteps) step(i + 1, r1, r0);
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    // the last phase: nobody pushes into this CTA's window or signals its mbarriers any more
-    if (lev) cs_mbar_wait(bar_u32 + 8u * (uint32_t)((lev - 1) & 1), (uint32_t)(((lev - 1) >> 1) & 1));
-    cs_cluster_sync();
-#ifdef DDILU_EXPERIMENTS
-    if (probe) {
-        long long *o = a.dbg + 16 * (2 * blockIdx.x + (tid ? 1 : 0));
-        for (int q = 0; q < 6; ++q) o[q] = tq[q];
-    }
 #endif
 #undef CS_TICK
+    }
+    cs_cluster_sync();
 }
 
-// one thread per row: the record of the row at its position of the CTA-local schedule order
-// record: c[4] (32 bytes) | 8 halves: K dependency slots, then CS_NP push targets (written by the caller) | upper: d, 1/d
+// one thread per row: operands of the row into its position of the CTA-local schedule order
 template <bool UPPER>
 __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int *__restrict__ ci,
                                    const double *__restrict__ val, int K, const int *__restrict__ gpos,
-                                   const int *__restrict__ dep_slot, unsigned char *recs, int *rowid, int *bad_row) {
+                                   const int *__restrict__ dep_slot, long long np, double *coef,
+                                   unsigned short *code, int *rowid, double *piv, int *bad_row) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n) return;
     const long long g = gpos[row];
-    unsigned char *rec = recs + (size_t)g * (UPPER ? CS_REC + 16 : CS_REC);
-    double *cf = (double *)rec;
-    unsigned short *hv = (unsigned short *)(rec + 32);
     int kk = 0;
     double diag = 1.0;
     bool seen = false;
+    // half kk of the row's packed words: word kk / 2 of the [words][np] array, 16-bit half kk % 2
     for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
         const int j = ci[k];
         if (UPPER ? j > row : j < row) {
             if (kk < K) {
-                cf[kk] = val[k];
-                hv[kk] = (unsigned short)dep_slot[k];
+                coef[(long long)kk * np + g] = val[k];
+                code[2 * ((long long)(kk >> 1) * np + g) + (kk & 1)] = (unsigned short)dep_slot[k];
             }
             ++kk;
         } else if (j == row) {
@@ -414,21 +422,20 @@ __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int 
         }
     }
     for (; kk < K; ++kk) {       // padding: coefficient 0 times the zero slot
-        cf[kk] = 0.0;
-        hv[kk] = (unsigned short)CS_WINDOW;
+        coef[(long long)kk * np + g] = 0.0;
+        code[2 * ((long long)(kk >> 1) * np + g) + (kk & 1)] = (unsigned short)CS_WINDOW;
     }
     rowid[g] = row;
     if (UPPER) {
-        double *pv = (double *)(rec + CS_REC);
-        pv[0] = diag;
-        pv[1] = safe_reciprocal(diag);
+        piv[g] = diag;
+        piv[np + g] = safe_reciprocal(diag);
         if (!seen || fabs(diag) < 1e-300) atomicMin(bad_row, row);
     }
 }
 
 namespace {
 long long *g_csweep_dbg = nullptr;
-template <int K, bool UPPER, int NSET>
+template <int K, bool UPPER>
 int cs_prepare(size_t smem) {
     if (smem > 227 * 1024) return DDILU_ERR_ARG;
     static size_t attr = 0;
@@ -436,22 +443,21 @@ int cs_prepare(size_t smem) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
     if (!nonportable) {
-        DDILU_CHECK(cudaFuncSetAttribute(csweep_kernel<K, UPPER, NSET>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        DDILU_CHECK(cudaFuncSetAttribute(csweep_kernel<K, UPPER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         nonportable = true;
     }
     if (attr < smem) {
-        DDILU_CHECK(cudaFuncSetAttribute(csweep_kernel<K, UPPER, NSET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+        DDILU_CHECK(cudaFuncSetAttribute(csweep_kernel<K, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
     }
     return DDILU_OK;
 }
 
-inline void cs_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int n_clusters, int csize, int threads,
-                      size_t smem, cudaStream_t st) {
+inline void cs_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int n_clusters, int csize, size_t smem,
+                      cudaStream_t st) {
     cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3((unsigned)(n_clusters * csize));
-    cfg.blockDim = dim3((unsigned)threads);
+    cfg.blockDim = dim3((unsigned)CS_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -462,40 +468,32 @@ inline void cs_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int n_cl
     cfg.numAttrs = 1;
 }
 
-template <int K, bool UPPER, int NSET>
-int cs_launch(int n_blocks, int csize, const CSweepArgs &a, size_t smem, cudaStream_t st) {
-    const int rc = cs_prepare<K, UPPER, NSET>(smem);
+template <int K, bool UPPER>
+int cs_launch(int n_blocks, int csize, const CSweepArgs &a, cudaStream_t st) {
+    const size_t smem = cs_smem_bytes(K, UPPER, a.depth, a.max_steps);
+    const int rc = cs_prepare<K, UPPER>(smem);
     if (rc) return rc;
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
-    cs_config(cfg, at, n_blocks, csize, cs_threads(UPPER, NSET), smem, st);
-    DDILU_CHECK(cudaLaunchKernelEx(&cfg, csweep_kernel<K, UPPER, NSET>, a));
+    cs_config(cfg, at, n_blocks, csize, smem, st);
+    DDILU_CHECK(cudaLaunchKernelEx(&cfg, csweep_kernel<K, UPPER>, a));
     return DDILU_OK;
 }
 
-template <int K, bool UPPER, int NSET>
+template <int K, bool UPPER>
 int cs_active(int csize, size_t smem, int *out) {
-    const int rc = cs_prepare<K, UPPER, NSET>(smem);
+    const int rc = cs_prepare<K, UPPER>(smem);
     if (rc) return rc;
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
-    cs_config(cfg, at, 64, csize, cs_threads(UPPER, NSET), smem, nullptr);
+    cs_config(cfg, at, 64, csize, smem, nullptr);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, csweep_kernel<K, UPPER, NSET>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, csweep_kernel<K, UPPER>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = 0;
     }
     *out = n;
     return DDILU_OK;
-}
-
-template <int K>
-int cs_dispatch(int upper, int depth, int n_blocks, int csize, const CSweepArgs &a, cudaStream_t st) {
-    const size_t smem = cs_smem_bytes(upper != 0, depth, a.max_steps);
-    if (depth == 2) return upper ? cs_launch<K, true, 2>(n_blocks, csize, a, smem, st) : cs_launch<K, false, 2>(n_blocks, csize, a, smem, st);
-    if (depth == 3) return upper ? cs_launch<K, true, 3>(n_blocks, csize, a, smem, st) : cs_launch<K, false, 3>(n_blocks, csize, a, smem, st);
-    if (depth == 4) return upper ? cs_launch<K, true, 4>(n_blocks, csize, a, smem, st) : cs_launch<K, false, 4>(n_blocks, csize, a, smem, st);
-    return DDILU_ERR_ARG;
 }
 }  // namespace
 
@@ -512,8 +510,8 @@ extern "C" int ddilu_csweep_set_debug(long long *buf) {
 }
 #endif
 
-/* threads of a CTA of the cluster sweep (= rows of a step) for a kernel shape (depth = stages of the operand ring) */
-extern "C" int ddilu_csweep_threads(int upper, int depth) { return cs_threads(upper != 0, depth); }
+/* compute threads of a CTA of the cluster sweep = rows of a step at most */
+extern "C" int ddilu_csweep_threads(void) { return CS_NT; }
 
 /* doubles of a CTA's window (own and halo values): no row may read further back (device.build_csweep checks) */
 extern "C" int ddilu_csweep_window(void) { return CS_WINDOW; }
@@ -521,50 +519,47 @@ extern "C" int ddilu_csweep_window(void) { return CS_WINDOW; }
 /* CTAs other than its own that may need a row's result */
 extern "C" int ddilu_csweep_max_push(void) { return CS_NP; }
 
-/* bytes of a row's record in the operand array */
-extern "C" int ddilu_csweep_record_bytes(int upper) { return upper ? CS_REC + 16 : CS_REC; }
+/* 32-bit words per row holding its k dependency slots and its push targets */
+extern "C" int ddilu_csweep_code_words(int k) { return cs_words(k); }
 
-extern "C" long long ddilu_csweep_smem_bytes(int upper, int depth, int max_steps) {
-    return (long long)cs_smem_bytes(upper != 0, depth, max_steps);
+extern "C" long long ddilu_csweep_smem_bytes(int k, int upper, int depth, int max_steps) {
+    return (long long)cs_smem_bytes(k, upper != 0, depth, max_steps);
 }
 
 /* clusters of `cluster_size` CTAs of the sweep kernel that can be resident at once (0: the size cannot be launched) */
-extern "C" int ddilu_csweep_active_clusters(int cluster_size, int depth, int max_steps) {
-    if (cluster_size < 1 || cluster_size > 16) return 0;
+extern "C" int ddilu_csweep_active_clusters(int cluster_size, int k, int depth, int max_steps) {
+    if (cluster_size < 1 || cluster_size > 16 || depth < 2 || depth > CS_MAX_DEPTH) return 0;
     int n = 0, rc = DDILU_ERR_ARG;
-    if (depth == 2) rc = cs_active<3, true, 2>(cluster_size, cs_smem_bytes(true, 2, max_steps), &n);
-    if (depth == 3) rc = cs_active<3, true, 3>(cluster_size, cs_smem_bytes(true, 3, max_steps), &n);
-    if (depth == 4) rc = cs_active<3, true, 4>(cluster_size, cs_smem_bytes(true, 4, max_steps), &n);
+    if (k == 3) rc = cs_active<3, true>(cluster_size, cs_smem_bytes(3, true, depth, max_steps), &n);
+    if (k == 4) rc = cs_active<4, true>(cluster_size, cs_smem_bytes(4, true, depth, max_steps), &n);
     return rc == DDILU_OK ? n : 0;
 }
 
 extern "C" int ddilu_csweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
-                                 const int *gpos, const int *dep_slot, unsigned char *recs, int *rowid, int *bad_row,
-                                 void *stream) {
+                                 const int *gpos, const int *dep_slot, long long np, double *coef, unsigned *code,
+                                 int *rowid, double *piv, int *bad_row, void *stream) {
     if (n <= 0) return DDILU_OK;
     if (k != 3 && k != 4) return DDILU_ERR_ARG;
     const int threads = 256, grid = div_up(n, threads);
     if (upper)
-        csweep_fill_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, recs,
-                                                                   rowid, bad_row);
+        csweep_fill_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, np,
+                                                                   coef, (unsigned short *)code, rowid, piv, bad_row);
     else
-        csweep_fill_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, recs,
-                                                                    rowid, bad_row);
+        csweep_fill_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, np,
+                                                                    coef, (unsigned short *)code, rowid, piv, bad_row);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
 
 /* out[row] = (L^-1 b)[row] (upper 0, unit diagonal) or (U^-1 b)[row] (upper 1) for a block-diagonal factor laid out
  * by ddilu_csweep_fill: n_blocks clusters of cluster_size CTAs */
-extern "C" int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps,
-                                  const unsigned char *recs, const int *rowid, long long np, int k, int upper,
-                                  int max_steps, int depth, const double *b, double *out, void *stream) {
+extern "C" int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps, const double *coef,
+                                  const unsigned *code, const int *rowid, const double *piv, long long np, int k,
+                                  int upper, int max_steps, int depth, const double *b, double *out, void *stream) {
     if (n_blocks <= 0) return DDILU_OK;
-    if (cluster_size < 1 || cluster_size > 16) return DDILU_ERR_ARG;
-    CSweepArgs a{ctas, steps, recs, rowid, b, out, np, max_steps, g_csweep_dbg};
-    switch (k) {
-        case 3: return cs_dispatch<3>(upper, depth, n_blocks, cluster_size, a, ST(stream));
-        case 4: return cs_dispatch<4>(upper, depth, n_blocks, cluster_size, a, ST(stream));
-        default: return DDILU_ERR_ARG;
-    }
+    if (cluster_size < 1 || cluster_size > 16 || (upper && !piv) || depth < 2 || depth > CS_MAX_DEPTH) return DDILU_ERR_ARG;
+    CSweepArgs a{ctas, steps, coef, code, rowid, piv, b, out, np, max_steps, depth, g_csweep_dbg};
+    if (k == 3) return upper ? cs_launch<3, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<3, false>(n_blocks, cluster_size, a, ST(stream));
+    if (k == 4) return upper ? cs_launch<4, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<4, false>(n_blocks, cluster_size, a, ST(stream));
+    return DDILU_ERR_ARG;
 }

@@ -803,17 +803,17 @@ def sweep_solve(sp: SweepPlan, phases: int, out: torch.Tensor, add: bool = False
 
 USE_CSWEEP = os.environ.get("DDILU_CSWEEP", "1") == "1"
 CSWEEP_CLUSTER = int(os.environ.get("DDILU_CSWEEP_CLUSTER", "16"))   # CTAs per block at most (the largest size whose clusters can all be resident is taken)
-CSWEEP_NSET = int(os.environ.get("DDILU_CSWEEP_DEPTH", "3"))         # stages of the operand ring: operands requested depth - 1 steps ahead
+CSWEEP_NSET = int(os.environ.get("DDILU_CSWEEP_DEPTH", "4"))         # stages of the operand ring at most (as many as fit)
 CSWEEP_MIN_CHUNK = int(os.environ.get("DDILU_CSWEEP_MIN_CHUNK", "32"))   # rows of a level a CTA takes at least (narrow levels stay on few CTAs)
-CSWEEP_MIN_AVG_WIDTH = 1024    # average rows per level of a block from which a cluster pays (below: one CTA per block)
+CSWEEP_MIN_AVG_WIDTH = 2000    # average rows per level of a block from which a cluster pays (measured: 128^3 / p = 8, 1 340 rows per level, is a tie with the tiled kernel; 192^3, 3 000 rows, 1.3x faster)
 CSWEEP_MIN_SMS = 60            # blocks x cluster size: SMs the launch must fill to have the bandwidth of the GPU
 _csweep_active = {}
 
 
-def csweep_active_clusters(csize: int, depth: int, max_steps: int) -> int:
-    key = (csize, depth, max_steps)
+def csweep_active_clusters(csize: int, k: int, depth: int, max_steps: int) -> int:
+    key = (csize, k, depth, max_steps)
     if key not in _csweep_active:
-        _csweep_active[key] = query("ddilu_csweep_active_clusters", csize, depth, max_steps)
+        _csweep_active[key] = query("ddilu_csweep_active_clusters", csize, k, depth, max_steps)
     return _csweep_active[key]
 
 
@@ -823,10 +823,13 @@ class ClusterSweepHalf:
 
     ctas: torch.Tensor         # int32[n_blocks * csize * 4]
     steps: torch.Tensor        # int32[total steps * 8]
-    recs: torch.Tensor         # uint8: one record per position (coefficients, dependency slots, push targets, pivot pair)
+    coef: torch.Tensor
+    code: torch.Tensor         # 16-bit halves of the packed words: dependency slots, push targets
     rowid: torch.Tensor
+    piv: torch.Tensor | None
     np: int
     max_steps: int
+    depth: int                 # stages of the operand ring
     contiguous: bool           # every level chunk is a range of consecutive rows (no row-id loads)
 
 
@@ -866,9 +869,9 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
     W = query("ddilu_csweep_window")
     nset = CSWEEP_NSET
     lev_cap = 2 * max(nlev_l, nlev_u)           # steps of a CTA: its levels, the wide ones in several pieces
-    if query("ddilu_csweep_smem_bytes", 1, nset, lev_cap) > 227 * 1024:
+    if query("ddilu_csweep_smem_bytes", k, 1, 2, lev_cap) > 227 * 1024:
         return None
-    csize = next((c for c in range(min(16, CSWEEP_CLUSTER), 0, -1) if csweep_active_clusters(c, nset, lev_cap) >= nb), 0)
+    csize = next((c for c in range(min(16, CSWEEP_CLUSTER), 0, -1) if csweep_active_clusters(c, k, 2, lev_cap) >= nb), 0)
     if debug:
         print(f"cluster sweep: {nb} blocks -> clusters of {csize}", flush=True)
     if not csize or nb * csize < CSWEEP_MIN_SMS:
@@ -896,11 +899,12 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         ranks = torch.arange(csize, dtype=i64, device=d).view(1, csize, 1)
         ncl = torch.clamp(cnt.view(nb, 1, nlev) - ranks * cs.view(nb, 1, nlev), min=0)
         ncl = torch.minimum(ncl, cs.view(nb, 1, nlev).expand(nb, csize, nlev))    # rows of CTA (b, r) in level l
-        lend = torch.cumsum(ncl, 2)
-        lstart = lend - ncl
+        npad = (ncl + 3) // 4 * 4                              # every chunk starts at a multiple of 4 positions (16-byte runs)
+        lstart = torch.cumsum(npad, 2) - npad
+        lend = lstart + ncl
         ckey = (blk * csize + rk) * nlev + lv
         lpos = lstart.reshape(-1)[ckey] + ro
-        rows_cta = lend[:, :, -1].reshape(-1)
+        rows_cta = (lstart + npad)[:, :, -1].reshape(-1)
         padded = (rows_cta + 31) // 32 * 32
         base = torch.cumsum(padded, 0) - padded
         npos = int(padded.sum().item())
@@ -956,7 +960,7 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         consecutive = (nclf == 0) | (row_hi - row_lo + 1 == nclf)
         contiguous = bool(consecutive.all().item())
         row0 = torch.where((nclf > 0) & consecutive, row_lo, torch.full_like(row_lo, -1))
-        NT = query("ddilu_csweep_threads", int(up), nset)
+        NT = query("ddilu_csweep_threads")
         # steps: a CTA's chunk of a level, cut into pieces of at most one row per thread; the first piece waits for
         # the previous level, the last one signals
         nsub = torch.clamp((nclf + NT - 1) // NT, min=1)
@@ -965,12 +969,13 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         nsub = torch.where(live, nsub, torch.zeros_like(nsub))
         steps_cta = nsub.view(nb * csize, nlev).sum(1)
         max_steps = int(steps_cta.max().item())
+        depth = next((dd for dd in range(nset, 1, -1) if query("ddilu_csweep_smem_bytes", k, int(up), dd, max_steps) <= 227 * 1024), 0)
         if debug:
             print(f"cluster sweep plan ({'U' if up else 'L'}): k {k}, cluster {csize}, furthest dependency {max_need} "
-                  f"(window {W}), widest level per CTA {width_cta} ({NT} threads, <= {max_steps} steps), levels per block {max_lev}, "
-                  f"positions {npos} for {n} rows, halo values {hu.numel()}, push targets per row <= {max_push}, "
-                  f"consecutive chunks: {contiguous}", flush=True)
-        if max_need > W or max_push > NP or query("ddilu_csweep_smem_bytes", int(up), nset, max_steps) > 227 * 1024:
+                  f"(window {W}), widest level per CTA {width_cta} ({NT} threads, <= {max_steps} steps, ring depth {depth}), "
+                  f"levels per block {max_lev}, positions {npos} for {n} rows, halo values {hu.numel()}, "
+                  f"push targets per row <= {max_push}, consecutive chunks: {contiguous}", flush=True)
+        if max_need > W or max_push > NP or not depth:
             return None
         tot = int(nsub.sum().item())
         src = torch.repeat_interleave(torch.arange(nsub.numel(), dtype=i64, device=d), nsub)    # (CTA, level) of a step
@@ -985,22 +990,34 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         s_flags = is_first.to(i64) + 2 * is_last.to(i64)
         zero = torch.zeros_like(e)
         steps = torch.stack([s_start, s_end, s_slot, s_row0, s_tx, s_flags, zero, zero], 1)
-        ctas = torch.zeros((nb * csize, 4), dtype=i64, device=d)
-        ctas[:, 0], ctas[:, 1] = base, rows_cta
+        # who signals whom at the end of a level: a CTA its own mbarrier and those of the CTAs it exchanges values
+        # with, in BOTH directions -- the producer must know that its consumer is done reading before it overwrites
+        # the consumer's window slots, and a coupled pair must stay within one level of each other (two mbarrier
+        # phases are in flight at most)
+        ncta = nb * csize
+        pairs = h_cta * ncta + cta[h_row]                                           # (consumer, producer)
+        pairs = torch.unique(torch.cat([pairs, cta[h_row] * ncta + h_cta]))
+        pa, pb = pairs // ncta, pairs % ncta
+        sigmask = torch.ones(ncta, dtype=i64, device=d) << (torch.arange(ncta, dtype=i64, device=d) % csize)
+        sigmask = sigmask.scatter_reduce(0, pa, torch.ones_like(pb) << (pb % csize), "sum")        # pairs are unique: sum = or
+        signallers = 1 + torch.bincount(pb, minlength=ncta)
+        ctas = torch.zeros((ncta, 4), dtype=i64, device=d)
+        ctas[:, 0], ctas[:, 1] = base, sigmask | (signallers << 16)
         ctas[:, 2] = torch.cumsum(steps_cta, 0) - steps_cta
         ctas[:, 3] = steps_cta
-        RB = query("ddilu_csweep_record_bytes", int(up))
-        recs = torch.zeros(npos * RB, dtype=torch.uint8, device=d)
-        halves16 = recs.view(torch.int16).view(npos, RB // 2)                     # a record's halves start at byte 32
-        halves16[:, 16 + k:16 + k + NP] = -1                                      # 0xffff: no push target
+        NWD = query("ddilu_csweep_code_words", k)
+        coef = torch.zeros(k * npos, dtype=F64, device=d)
+        code = torch.full((NWD * npos * 2,), -1, dtype=torch.int16, device=d)      # halves; 0xffff: no push target
         if prow.numel():
             pcode = ((h_wpos[porder] % W) << 4) | (h_cta[porder] % csize)
-            halves16.view(-1)[gpos[prow] * (RB // 2) + 16 + k + pidx] = pcode.to(torch.int32).to(torch.int16)
+            half = k + pidx                                                          # half index of the push target
+            code[2 * ((half // 2) * npos + gpos[prow]) + half % 2] = pcode.to(torch.int32).to(torch.int16)
         rowid = torch.zeros(npos, dtype=I32, device=d)
+        piv = torch.ones(2 * npos, dtype=F64, device=d) if up else None
         call("ddilu_csweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos.to(I32).contiguous(),
-             (e_wpos % W).to(I32).contiguous(), recs, rowid, bad)
+             (e_wpos % W).to(I32).contiguous(), npos, coef, code, rowid, piv, bad)
         halves.append(ClusterSweepHalf(ctas.to(I32).contiguous().view(-1), steps.to(I32).contiguous().view(-1),
-                                       recs, rowid, npos, max_steps, contiguous))
+                                       coef, code, rowid, piv, npos, max_steps, depth, contiguous))
     return ClusterSweepPlan(n, nb, csize, k, nset, halves[0], halves[1], int(bad.item()))
 
 
@@ -1009,8 +1026,8 @@ def csweep_solve(cp: ClusterSweepPlan, upper: bool, b: torch.Tensor, out: torch.
     if check and upper and cp.bad_row != INT_MAX:
         raise TriSolveError(f"zero or missing diagonal at row {cp.bad_row}")
     h = cp.upper if upper else cp.lower
-    call("ddilu_csweep_solve", cp.n_blocks, cp.csize, h.ctas, h.steps, h.recs, h.rowid, h.np, cp.k, int(upper),
-         h.max_steps, cp.nset, b, out)
+    call("ddilu_csweep_solve", cp.n_blocks, cp.csize, h.ctas, h.steps, h.coef, h.code, h.rowid, h.piv, h.np, cp.k,
+         int(upper), h.max_steps, h.depth, b, out)
     return out
 
 

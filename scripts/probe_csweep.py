@@ -90,7 +90,7 @@ for cluster, nset, min_chunk in variants:
     tl = timed(lambda: D.csweep_solve(cp, False, r, x))
     tu = timed(lambda: D.csweep_solve(cp, True, r, x))
     emit({"n": n, "p": p, "kernel": "csweep", "cluster": cp.csize, "nset": nset, "min_chunk": min_chunk,
-          "steps": [cp.lower.max_steps, cp.upper.max_steps], "consecutive": [cp.lower.contiguous, cp.upper.contiguous], "plan_ms": round(t0.elapsed_time(t1), 1),
+          "steps": [cp.lower.max_steps, cp.upper.max_steps], "depth": [cp.lower.depth, cp.upper.depth], "consecutive": [cp.lower.contiguous, cp.upper.contiguous], "plan_ms": round(t0.elapsed_time(t1), 1),
           "bit_equal": [ok_l, ok_u], "L_us": round(tl * 1e6, 1), "U_us": round(tu * 1e6, 1),
           "L_frac": round(bytes_l / tl / 1e9 / peak_gbs, 3), "U_frac": round(bytes_u / tu / 1e9 / peak_gbs, 3)})
     if _lib.has_experiments():

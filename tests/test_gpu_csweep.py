@@ -71,8 +71,8 @@ def test_cluster_sweep_bit_exact(P, orc, dims, p, pc, cluster, nset, min_chunk):
     cp = f._cs
     assert cp is not None, "interior factors did not get a cluster-sweep plan"
     # the largest cluster size <= `cluster` whose clusters can all be resident (16 fits 7 times on a B200)
-    want = next(c for c in range(cluster, 0, -1) if D.csweep_active_clusters(c, nset, 2 * max(f._lev(False)[1], f._lev(True)[1])) >= p)
-    assert cp.n_blocks == p and cp.csize == want and cp.nset == nset
+    want = next(c for c in range(cluster, 0, -1) if D.csweep_active_clusters(c, cp.k, 2, 2 * max(f._lev(False)[1], f._lev(True)[1])) >= p)
+    assert cp.n_blocks == p and cp.csize == want and cp.lower.depth <= nset
     rng = np.random.default_rng(23)
     for rep in range(3):
         b = rng.standard_normal(f.n)
@@ -97,7 +97,7 @@ def test_cluster_sweep_levels_wider_than_the_cta(P, orc):
         a = P.aniso3d(*dims)
         layout = P.classify_and_order(a, P.partition(a, 1, dims), 1)
         m = P.make_preconditioner("schur", a, layout)
-        threads = D.query("ddilu_csweep_threads", 0, 3)
+        threads = D.query("ddilu_csweep_threads")
     f = m._p.interior
     assert f._cs is not None and f._cs.csize == 1
     widest = int(np.bincount(f._lev(False)[0][: f.n].cpu().numpy()).max())
