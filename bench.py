@@ -199,7 +199,7 @@ def run_ours(args):
         step(True)
     # --- timed region 1: inputs resident in HBM; only the dominant kernel (the triangular solve) carries
     # CUDA events inside the timed region -- event pairs around all ~75 launches of an iteration cost ~4 %
-    trsv_watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_sweep_solve")
+    trsv_watch = ("ddilu_csweep_solve", "ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_sweep_solve")
     _lib.profile = {k: [] for k in trsv_watch} if args.kernel_events else None
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     total, recs, launches, m = timed(True, args.steps)
@@ -213,7 +213,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         prof, _lib.profile = _lib.profile, None
     # --- one extra UNTIMED step with events on the other hot kernels (or on every entry: --watch-all)
-    watch = ("ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_sweep_solve", "ddilu_sweep_rhs", "ddilu_spmv_csr_f64_tuned",
+    watch = ("ddilu_csweep_solve", "ddilu_sptrsv_tiled", "ddilu_sptrsv_sell", "ddilu_sweep_solve", "ddilu_sweep_rhs", "ddilu_spmv_csr_f64_tuned",
              "ddilu_axpy_dot_dir", "ddilu_dot_dir", "ddilu_mgs_block")
     if args.watch_all:
         watch = tuple(k for k, (res, a) in _lib.SIGNATURES.items() if res is _lib._I and a and a[-1] is _lib._P)
@@ -242,11 +242,12 @@ def run_ours(args):
     nL, nU, nrows = fac.lower.nnz, fac.upper.nnz, fac.n
     # split the watched sptrsv launches by size: interior-factor solves are the long ones
     tiled = fac._tl is not None
-    trsv_name = "ddilu_sptrsv_tiled" if tiled else "ddilu_sptrsv_sell"
+    clustered = getattr(fac, "_cs", None) is not None          # cluster sweep (csrc/csweep.cu): only the interior factors use it
+    trsv_name = "ddilu_csweep_solve" if clustered else ("ddilu_sptrsv_tiled" if tiled else "ddilu_sptrsv_sell")
     ev = [(e0.elapsed_time(e1) * 1e-3) for e0, e1, _ in prof[trsv_name]]
     # schur: 2 of the 10 solves of an outer iteration are interior-factor solves (L_B, U_B: the long ones), 8 are interface solves
     swept = args.precond == "schur" and getattr(m._p.schur, "_sw", None) is not None
-    share = (1.0 if swept else 0.2) if args.precond == "schur" else 0.5
+    share = 1.0 if clustered else ((1.0 if swept else 0.2) if args.precond == "schur" else 0.5)
     big = sorted(ev)[len(ev) - int(round(len(ev) * share)):] if ev else []
     # bytes per launch: average of the L and U interior solves (they alternate 1:1)
     alg = 0.5 * (algorithmic_bytes_sptrsv(nL, nrows) + algorithmic_bytes_sptrsv(nU, nrows))
@@ -283,10 +284,15 @@ def run_ours(args):
                      "levels": fac._lev(False)[1],
                      "tiles": fac._tl.n_tiles if tiled else None,
                      "tile_levels": fac._tl.n_tile_levels if tiled else None,
+                     "cluster": ({"ctas_per_block": fac._cs.csize, "blocks": fac._cs.n_blocks,
+                                  "sms_used": fac._cs.csize * fac._cs.n_blocks,
+                                  "steps_per_cta": [fac._cs.lower.max_steps, fac._cs.upper.max_steps],
+                                  "ring_depth": [fac._cs.lower.depth, fac._cs.upper.depth]} if clustered else None),
                      "latency_bound_us": fac._lev(False)[1] * 0.38,
                      "note": "latency_bound_us = levels x 0.38 us (measured L2 store->poll hop): what a solve costs "
-                             "when every level crosses L2 (sync-free kernel); the tiled kernel keeps a tile's "
-                             "levels in shared memory"},
+                             "when every level crosses L2 (sync-free kernel); the cluster sweep hands a level over "
+                             "through distributed shared memory (one thread-block cluster per subdomain block), the "
+                             "tiled kernel keeps a tile's levels in shared memory"},
         "kernels_one_untimed_step": kern,
     }
     # secondary rooflines from the untimed instrumented step (north_star asks for SpTRSV AND SpMV GB/s):

@@ -2,7 +2,8 @@
 
     compute-sanitizer --tool memcheck python scripts/sanitize_case.py [tiled|sweep|mgs|ilut|rcm|pipeline ...]
 
-tiled: sptrsv_tiled on interior + interface factors; sweep: the block sweep (L, U, fused, with product and add);
+tiled: sptrsv_tiled on interior + interface factors; csweep: the cluster sweep on interior factors (clusters of 4 and
+of the largest size that fits, a 32^3 block on one CTA: levels in several steps); sweep: the block sweep (L, U, fused, with product and add);
 sweep_long: its long-row instances on 27-point ILUT interface factors (+ a whole solve: device-side inner-solve
 arithmetic); spgemm: sparse_matmul;
 mgs: ddilu_mgs_block over ragged lengths and block shapes; ilut: ilut_kernel (27-point, fill);
@@ -17,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_08881_b200 as P
 from paper_2303_08881_b200 import device as D
 
-which = sys.argv[1:] or ["tiled", "sweep", "sweep_long", "mgs", "ilut", "rcm", "spgemm", "pipeline"]
+which = sys.argv[1:] or ["tiled", "csweep", "sweep", "sweep_long", "mgs", "ilut", "rcm", "spgemm", "pipeline"]
 dims = (20, 18, 17)
 a = P.aniso3d(*dims)
 layout = P.classify_and_order(a, P.partition(a, 4, dims), 4)
@@ -34,6 +35,27 @@ if "tiled" in which:
         torch.cuda.synchronize()
         print("tiled", f._tl.kind, f.n, float(x.abs().max()))
     D.USE_SWEEP = True
+
+if "csweep" in which:
+    old = D.CSWEEP_MIN_AVG_WIDTH, D.CSWEEP_MIN_SMS, D.CSWEEP_CLUSTER
+    D.CSWEEP_MIN_AVG_WIDTH = D.CSWEEP_MIN_SMS = 0
+    for cluster, (aa, lay) in ((4, (a, layout)), (16, (a, layout)), (1, None)):
+        D.CSWEEP_CLUSTER = cluster
+        if lay is None:
+            d1 = (32, 32, 32)
+            aa = P.aniso3d(*d1)
+            lay = P.classify_and_order(aa, P.partition(aa, 1, d1), 1)
+        m = P.make_preconditioner("schur", aa, lay)
+        f = m._p.interior
+        assert f._cs is not None
+        r = torch.randn(f.n, dtype=torch.float64, device="cuda")
+        x = torch.empty_like(r)
+        f.lower_solve(r, x)
+        f.upper_solve(r, x)
+        f.solve(r, x)
+        torch.cuda.synchronize()
+        print("csweep", f.n, f._cs.csize, f._cs.lower.max_steps, f._cs.lower.depth, float(x.abs().max()))
+    D.CSWEEP_MIN_AVG_WIDTH, D.CSWEEP_MIN_SMS, D.CSWEEP_CLUSTER = old
 
 if "sweep" in which:
     from paper_2303_08881_b200.factor import solve_with_product
