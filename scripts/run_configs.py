@@ -79,7 +79,7 @@ def kernel_rates(m):
             continue
         r = torch.randn(n, dtype=torch.float64, device="cuda")
         x = torch.empty_like(r)
-        kind = "sweep" if f._sw is not None else ("tiled" if f._tl is not None else "syncfree")
+        kind = "cluster-sweep" if f._cs is not None else ("sweep" if f._sw is not None else ("tiled" if f._tl is not None else "syncfree"))
         rec = {"rows": n, "kernel": kind}
         if f._sw is not None:
             t = timed(lambda: f.solve(r, x))
