@@ -132,8 +132,13 @@ __device__ __forceinline__ void cs_mbar_arrive_tx(uint32_t bar, uint32_t bytes) 
 __device__ __forceinline__ void cs_mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// arrive on the mbarrier of a CTA of the cluster (own included); release.cta orders the warp's window stores before
-// the arrive for the readers of the own CTA -- other CTAs get their data through cs_push
+// arrive on the own mbarrier: release.cta orders the warp's window stores (made visible to the arriving lane by
+// __syncwarp) before the arrive for the readers of the own CTA
+__device__ __forceinline__ void cs_mbar_arrive_release(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// token arrive on the mbarrier of another CTA of the cluster: it carries no data (that CTA gets its data through
+// cs_push), it only says that this warp's reads of the level are done
 __device__ __forceinline__ void cs_mbar_arrive_cluster(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
@@ -286,8 +291,12 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
         }
     } else {
         // ------------------------------------------------------------ compute threads
-        // lane r signals CTA r when the mask says so: the address of that CTA's mbarrier pair
-        const bool signals = (uint32_t)lane < csize && ((sigmask >> lane) & 1u);
+        // lane r signals CTA r when the mask says so: the address of that CTA's mbarrier pair (the own CTA's through
+        // its shared::cta address)
+        uint32_t my_rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(my_rank));
+        const bool self = (uint32_t)lane == my_rank;
+        const bool signals = (uint32_t)lane < csize && ((sigmask >> lane) & 1u) && !self;
         const uint32_t peer_bar = cs_mapa(bar_u32, signals ? (uint32_t)lane : 0u);
         const uint32_t my8 = ring_u32 + 8u * (uint32_t)tid, my4 = ring_u32 + 4u * (uint32_t)tid;
 #ifdef DDILU_EXPERIMENTS
@@ -306,9 +315,19 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
         int lev = 0;                          // level of the current step
         int s = 0;
         uint32_t round = 0;
+        // the table entry of a step is loaded one step ahead (its two shared-memory loads head the step's chain)
+        int4 sv_n = make_int4(0, 0, 0, 0), tf_n = sv_n;
+        if (nsteps) {
+            sv_n = cs_lds_v4(st_u32);
+            tf_n = cs_lds_v4(st_u32 + 16u);
+        }
         for (int i = 0; i < nsteps; ++i) {
-            const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
-            const int4 tf = cs_lds_v4(st_u32 + 32u * (uint32_t)i + 16u);     // halo bytes of the level, flags
+            const int4 sv = sv_n;
+            const int4 tf = tf_n;                                            // halo bytes of the level, flags
+            if (i + 1 < nsteps) {
+                sv_n = cs_lds_v4(st_u32 + 32u * (uint32_t)(i + 1));
+                tf_n = cs_lds_v4(st_u32 + 32u * (uint32_t)(i + 1) + 16u);
+            }
             const uint32_t mybar = bar_u32 + 8u * (uint32_t)(lev & 1);       // phase of this level: own and (offset) peers'
             // the halo bytes of the level (before this warp's arrive: the phase cannot complete without them)
             if (tid == 0 && tf.x) cs_mbar_expect_tx(mybar, (uint32_t)tf.x);
@@ -363,11 +382,14 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
                 int sl = sv.z + tid;
                 sl -= sl >= CS_WINDOW ? CS_WINDOW : 0;
                 cs_sts(xs_u32 + 8u * (uint32_t)sl, sum);
-                // to the other CTAs that need the value (rows on the border of a chunk)
+                // to the other CTAs that need the value (rows on the border of a chunk; the targets of a row are
+                // stored front to back, so one test tells the common case "none")
+                if (cs_half(w, K) != CS_NO_PUSH) {
 #pragma unroll
-                for (int k = 0; k < CS_NP; ++k) {
-                    const uint32_t pp = cs_half(w, K + k);
-                    if (pp != CS_NO_PUSH) cs_push(cs_mapa(xs_u32 + 8u * (pp >> 4), pp & 15u), sum, cs_mapa(mybar, pp & 15u));
+                    for (int k = 0; k < CS_NP; ++k) {
+                        const uint32_t pp = cs_half(w, K + k);
+                        if (pp != CS_NO_PUSH) cs_push(cs_mapa(xs_u32 + 8u * (pp >> 4), pp & 15u), sum, cs_mapa(mybar, pp & 15u));
+                    }
                 }
                 res = sum;
             }
@@ -375,6 +397,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
             if (tf.y & CS_ARRIVE) {
                 // this warp is through the level: one arrive per CTA of the cluster (lane r -> CTA r)
                 __syncwarp();
+                if (self) cs_mbar_arrive_release(mybar);
                 if (signals) cs_mbar_arrive_cluster(peer_bar + 8u * (uint32_t)(lev & 1));
                 ++lev;
             }

@@ -39,9 +39,10 @@ if "tiled" in which:
 if "csweep" in which:
     old = D.CSWEEP_MIN_AVG_WIDTH, D.CSWEEP_MIN_SMS, D.CSWEEP_CLUSTER
     D.CSWEEP_MIN_AVG_WIDTH = D.CSWEEP_MIN_SMS = 0
-    for cluster, (aa, lay) in ((4, (a, layout)), (16, (a, layout)), (1, None)):
+    for cluster in (4, 16, 1):
         D.CSWEEP_CLUSTER = cluster
-        if lay is None:
+        aa, lay = a, layout
+        if cluster == 1:
             d1 = (32, 32, 32)
             aa = P.aniso3d(*d1)
             lay = P.classify_and_order(aa, P.partition(aa, 1, d1), 1)
