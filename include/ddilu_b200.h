@@ -208,12 +208,14 @@ int ddilu_ilu0_numeric(int n, int n_slots, const int *order, const int *p_rp, co
 /* ---- factor.py:482-656 `_ilut_factor` + :465-479 `_select_largest`.  Rows are
  * written to fixed-capacity slabs: caps_h = {lcap, ucap, scap} from ddilu_ilut_caps;
  * L row i at i*lcap; U row i at i*ucap (i < n_elim, diagonal first) or
- * n_elim*ucap + (i-n_elim)*scap (Schur rows).  *status != 0: row_cap too small. */
+ * n_elim*ucap + (i-n_elim)*scap (Schur rows).  *status != 0: row_cap too small.
+ * order (NULL = index order): processing order of the rows, any permutation in which a row comes after its pivot
+ * rows -- callers interleave independent diagonal blocks so that all of them advance at once. */
 long long ddilu_ilut_smem_bytes(int row_cap);
 int ddilu_ilut_caps(int maxfill, int row_cap, int *caps_h);
 int ddilu_ilut_factor(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, double tau, int maxfill,
                       double tau_s, double delta, int row_cap, int *l_cnt, int *l_ci, double *l_v, int *u_cnt,
-                      int *u_ci, double *u_v, int *done, int *status, void *stream);
+                      int *u_ci, double *u_v, int *done, int *status, const int *order, void *stream);
 /* slab rows (cap_a for rows < n_split, cap_b after) -> CSR with the given row_ptr */
 int ddilu_compact_rows(int n, int n_split, int cap_a, int cap_b, const int *cnt, const int *ci, const double *v,
                        const int *out_rp, int *out_ci, double *out_v, void *stream);

@@ -12,7 +12,35 @@ from ._lib import DdiluError, call, query
 MAX_ROW_CAP = 1900  # 4 warps x (24 B + 1 B) x cap must fit the 200 KB shared-memory budget
 
 
-def d_ilut_factor(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float, safeguard: float):
+def interleaved_order(n: int, sections) -> torch.Tensor | None:
+    """Processing order for a matrix whose rows are [section 0 | section 1 | ...], every section a sequence of
+    independent diagonal blocks given by its pointer array (host ints, local to the section): inside a section the
+    rows of all blocks are dealt round-robin (row j of block 0, row j of block 1, ...), so that the warps of the
+    factorisation kernel work on every block at once instead of on one block after the other.  A row still comes
+    after every row of its own block with a smaller index and after all rows of the earlier sections."""
+    parts, start = [], 0
+    dev = D.dev()
+    for ptr in sections:
+        ptr = [int(v) for v in ptr]
+        m, nb = ptr[-1] - ptr[0], len(ptr) - 1
+        if m <= 0:
+            continue
+        if nb <= 1:
+            parts.append(torch.arange(start, start + m, dtype=torch.int64, device=dev))
+        else:
+            rows = torch.arange(m, dtype=torch.int64, device=dev)
+            p = torch.tensor(ptr, dtype=torch.int64, device=dev) - ptr[0]
+            blk = torch.bucketize(rows, p[1:], right=True)
+            key = (rows - p[blk]) * nb + blk
+            parts.append(start + torch.argsort(key))
+        start += m
+    if start != n or not parts:
+        return None
+    return torch.cat(parts).to(D.I32).contiguous()
+
+
+def d_ilut_factor(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float, safeguard: float,
+                  order: torch.Tensor | None = None):
     from .factor import DevFactors
     n = a.n_rows
     if n == 0:
@@ -34,7 +62,7 @@ def d_ilut_factor(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: 
         l_ci, l_v = D.empty_i32(max(1, l_slots)), D.empty_f64(max(1, l_slots))
         u_ci, u_v = D.empty_i32(max(1, u_slots)), D.empty_f64(max(1, u_slots))
         call("ddilu_ilut_factor", n, a.rp, a.ci, a.val, int(n_elim), float(tau), int(maxfill), float(tau_s),
-             float(safeguard), int(row_cap), l_cnt, l_ci, l_v, u_cnt, u_ci, u_v, done, status)
+             float(safeguard), int(row_cap), l_cnt, l_ci, l_v, u_cnt, u_ci, u_v, done, status, order)
         if int(status.item()) == 0:
             break
         if row_cap >= MAX_ROW_CAP:

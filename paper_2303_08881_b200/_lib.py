@@ -70,7 +70,7 @@ SIGNATURES = {
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),
     "ddilu_ilut_smem_bytes": (_L, [_I]),
     "ddilu_ilut_caps": (_I, [_I, _I, _P]),
-    "ddilu_ilut_factor": (_I, [_I, _P, _P, _P, _I, _D, _I, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_ilut_factor": (_I, [_I, _P, _P, _P, _I, _D, _I, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_compact_rows": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_csr_block_count": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "ddilu_csr_block_fill": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(ILUT_WARPS * 32) ilut_kernel(int n, const int 
                                                                const double *__restrict__ a_v, double tau, int maxfill,
                                                                double tau_s, double delta, int cap, IlutSlabs sl,
                                                                int *l_cnt, int *l_ci, double *l_v, int *u_cnt,
-                                                               int *u_ci, double *u_v, int *done, int *status) {
+                                                               int *u_ci, double *u_v, int *done, int *status,
+                                                               const int *__restrict__ order) {
     extern __shared__ unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     // per-warp carve: valsA, valsB (double[cap]), colsA, colsB (int[cap]), insj (int[32]), sel (uchar[cap])
@@ -78,8 +79,10 @@ __global__ void __launch_bounds__(ILUT_WARPS * 32) ilut_kernel(int n, const int 
     const int n_elim = sl.n_elim;
     const long long W = (long long)gridDim.x * ILUT_WARPS;
 
-    for (long long row = (long long)blockIdx.x * ILUT_WARPS + wib; row < n; row += W) {
-        const int i = (int)row;
+    // rows are taken in PROCESSING order: order[slot] (any order in which a row comes after its pivot rows; the
+    // caller interleaves the independent diagonal blocks so that all of them advance at once), else index order
+    for (long long slot = (long long)blockIdx.x * ILUT_WARPS + wib; slot < n; slot += W) {
+        const int i = order ? order[slot] : (int)slot;
         const int lim = i < n_elim ? i : n_elim;
         const int a0 = a_rp[i], len0 = a_rp[i + 1] - a0;
         bool overflow = false;
@@ -344,7 +347,7 @@ extern "C" int ddilu_ilut_caps(int maxfill, int row_cap, int *caps_h) {
 extern "C" int ddilu_ilut_factor(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, double tau,
                                  int maxfill, double tau_s, double delta, int row_cap, int *l_cnt, int *l_ci,
                                  double *l_v, int *u_cnt, int *u_ci, double *u_v, int *done, int *status,
-                                 void *stream) {
+                                 const int *order, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) return DDILU_OK;
     if (row_cap < 2) return DDILU_ERR_ARG;
@@ -366,7 +369,7 @@ extern "C" int ddilu_ilut_factor(int n, const int *a_rp, const int *a_ci, const 
     if (grid > need) grid = need;
     int g = (int)grid;
     void *args[] = {&n, &a_rp, &a_ci, &a_v, &tau, &maxfill, &tau_s, &delta, &row_cap, &sl,
-                    &l_cnt, &l_ci, &l_v, &u_cnt, &u_ci, &u_v, &done, &status};
+                    &l_cnt, &l_ci, &l_v, &u_cnt, &u_ci, &u_v, &done, &status, &order};
     DDILU_CHECK(cudaLaunchCooperativeKernel((void *)ilut_kernel, g, ILUT_WARPS * 32, args, smem, st));
     return DDILU_OK;
 }

@@ -249,15 +249,19 @@ def d_factor_level0(a: D.DeviceCsr, n_elim: int, milu: bool = False, target: tor
 
 
 def d_ilut(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float,
-           safeguard: float = DIAG_SAFEGUARD) -> DevFactors:
-    from ._ilut import d_ilut_factor
-    return d_ilut_factor(a, n_elim, tau, maxfill, tau_s, safeguard)
+           safeguard: float = DIAG_SAFEGUARD, sections=None) -> DevFactors:
+    """sections: pointer arrays of the independent diagonal blocks, one per row section ([interiors | exteriors] or
+    one section) -- the ILUT kernel then works on all blocks at once (`_ilut.interleaved_order`); the result does
+    not depend on it."""
+    from ._ilut import d_ilut_factor, interleaved_order
+    order = interleaved_order(a.n_rows, sections) if sections is not None else None
+    return d_ilut_factor(a, n_elim, tau, maxfill, tau_s, safeguard, order)
 
 
-def d_factorize(a: D.DeviceCsr, rule: FillRule, safeguard: float = DIAG_SAFEGUARD) -> DevFactors:
+def d_factorize(a: D.DeviceCsr, rule: FillRule, safeguard: float = DIAG_SAFEGUARD, sections=None) -> DevFactors:
     if rule.kind == "ilu0" or rule.kind == "iluk":
         return d_factor_level0(a, a.n_rows, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
-    return d_ilut(a, a.n_rows, rule.tau, rule.maxfill, 0.0, safeguard)
+    return d_ilut(a, a.n_rows, rule.tau, rule.maxfill, 0.0, safeguard, sections)
 
 
 class DevPartial:
@@ -295,17 +299,19 @@ def d_drop_small_rows(m: D.DeviceCsr, tol: float) -> D.DeviceCsr:
 
 
 def d_partial_ilu(a: D.DeviceCsr, n_interior: int, rule: FillRule, schur_drop_tol: float = 0.0,
-                  factor_schur: bool = True, safeguard: float = DIAG_SAFEGUARD) -> DevPartial:
-    """factor.py:825-883."""
+                  factor_schur: bool = True, safeguard: float = DIAG_SAFEGUARD, blocks=None) -> DevPartial:
+    """factor.py:825-883.  blocks = (interior pointers, interface pointers) of the independent subdomain blocks
+    when a is block-diagonal by subdomain (a scheduling hint for ILUT, see d_ilut)."""
     if rule.kind == "ilut":
-        f = d_ilut(a, n_interior, rule.tau, rule.maxfill, schur_drop_tol, safeguard)
+        f = d_ilut(a, n_interior, rule.tau, rule.maxfill, schur_drop_tol, safeguard, sections=blocks)
         drop_tol = 0.0
     else:
         f = d_factor_level0(a, n_interior, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
         drop_tol = schur_drop_tol
     l_b, u_b, w, z, _, s_tilde = d_carve(f, n_interior)
     s_tilde = d_drop_small_rows(s_tilde, drop_tol)
-    schur = d_factorize(s_tilde, rule, safeguard) if factor_schur else None
+    schur = d_factorize(s_tilde, rule, safeguard, sections=blocks[1:] if blocks is not None else None) \
+        if factor_schur else None
     return DevPartial(DevFactors(l_b, u_b), w, z, s_tilde, schur, n_interior)
 
 

@@ -493,7 +493,8 @@ class BjIluPrecond(_DDPrecond):
             if int(missing.item()):
                 raise NotImplementedError("l1bj on a matrix with structurally missing diagonal entries")
             mat = D.DeviceCsr(mat.n_rows, mat.n_cols, mat.rp, mat.ci, vals, mat.nnz)
-        self._f = d_factorize(mat, rule).prepare(part=self.system.tile_part("all"))
+        self._f = d_factorize(mat, rule, sections=(self.system.int_ptr, self.system.ext_ptr)).prepare(
+            part=self.system.tile_part("all"))
         self._factors = None
 
     @property
@@ -521,7 +522,8 @@ class SchurIluPrecond(_DDPrecond):
         super().__init__(a, layout, use_rcm)
         s = self.system
         self.rule, self.inner_iters = rule, inner_iters
-        self._p = d_partial_ilu(s.a_dom, s.n_int, rule, schur_drop_tol=schur_drop_tol, factor_schur=True)
+        self._p = d_partial_ilu(s.a_dom, s.n_int, rule, schur_drop_tol=schur_drop_tol, factor_schur=True,
+                                blocks=(s.int_ptr, s.ext_ptr))
         self._p.interior.prepare(part=s.lazy_tile_part_interior(), cluster_seg=s.int_ptr)
         self._p.schur.prepare(seg_ptr=s.ext_ptr, part=s.tile_part("ext"))   # interface factors: one block per subdomain
         self._coupling = s.coupling()

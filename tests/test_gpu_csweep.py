@@ -155,3 +155,30 @@ def test_pipeline_same_with_and_without_cluster_sweep(P):
         assert it1 == it0
         assert np.array_equal(z1, z0)
         assert np.array_equal(x1, x0)
+
+
+def test_ilut_interleaved_blocks_same_factors(P):
+    """The ILUT kernel takes the rows of the independent subdomain blocks round-robin (all blocks advance at once
+    instead of one after the other): patterns and values of L_B, U_B, W, Z, S~ and of the factors of S~ are the bits
+    of the index-order run (factor.py:482-656 is order-independent across independent blocks)."""
+    import torch
+    from paper_2303_08881_b200 import factor as F
+    dims = (14, 13, 12)
+    a = P.convdiff27(*dims)
+    layout = P.classify_and_order(a, P.partition(a, 4, dims), 4)
+    m = P.make_preconditioner("schur", a, layout, P.FillRule.parse("ilut:0.001,20"))
+    s = m.system
+    rule = P.FillRule.parse("ilut:0.001,20")
+    plain = F.d_partial_ilu(s.a_dom, s.n_int, rule, factor_schur=True)
+    inter = F.d_partial_ilu(s.a_dom, s.n_int, rule, factor_schur=True, blocks=(s.int_ptr, s.ext_ptr))
+    from paper_2303_08881_b200._ilut import interleaved_order
+    order = interleaved_order(s.n_loc, (s.int_ptr, s.ext_ptr))
+    assert order is not None and sorted(order.cpu().tolist()) == list(range(s.n_loc))
+    assert order[:4].cpu().tolist() == [int(s.int_ptr[k]) for k in range(4)]      # row 0 of every block first
+    pairs = [(plain.interior.lower, inter.interior.lower), (plain.interior.upper, inter.interior.upper),
+             (plain.w, inter.w), (plain.z, inter.z), (plain.s_tilde, inter.s_tilde),
+             (plain.schur.lower, inter.schur.lower), (plain.schur.upper, inter.schur.upper)]
+    for x, y in pairs:
+        assert x.nnz == y.nnz
+        assert torch.equal(x.rp, y.rp) and torch.equal(x.ci[: x.nnz], y.ci[: y.nnz])
+        assert torch.equal(x.val[: x.nnz], y.val[: y.nnz])
