@@ -276,6 +276,7 @@ def run_ours(args):
                 "setup_s": float(np.mean([r["setup_s"] for r in e2e_recs])),
                 "solve_s": float(np.mean([r["solve_s"] for r in e2e_recs]))},
         "gpu_launches": launches,
+        "comm": comm.transport,
         "clocks": clocks,
         "roofline": {"bound": "hbm", "kernel": f"{trsv_name[6:]} (interior L_B / U_B solves)", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
@@ -512,6 +513,9 @@ def main():
         relaunch_under_torchrun(args)
     else:
         run_ours(args)
+        from paper_2303_08881_b200 import dist as _dist
+        if hasattr(_dist.get_comm(), "close"):          # peer-memory transport: unmap the other ranks' mailboxes
+            _dist.get_comm().close()
 
 
 if __name__ == "__main__":

@@ -213,6 +213,8 @@ class LocalSystem:
         sf = sflags[: comm.size * self.n_ext].view(comm.size, self.n_ext) > 0
         self.send_counts = sf.sum(dim=1).cpu().numpy().astype(int).tolist()
         self.send_idx = torch.nonzero(sf)[:, 1].to(D.I32).contiguous()
+        if hasattr(comm, "reserve"):            # peer-memory transport: mailbox room for the largest message (collective)
+            comm.reserve(max(max(self.send_counts), max(self.recv_counts), 1))
         return D.index_map(n, halo_nodes, offset=self.n_loc, base=colmap)
 
     def exchange_halo(self, src_ext: torch.Tensor, halo_out: torch.Tensor, async_op: bool = False):

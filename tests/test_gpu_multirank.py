@@ -24,11 +24,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _solve_all(P):
+def _solve_all(P, cases=None):
     out = {}
     a = P.aniso3d(*DIMS)
     b = P.default_rhs(a) if False else None
-    for pc, p in CASES:
+    for pc, p in (cases or CASES):
         a = P.aniso3d(*DIMS)
         layout = P.classify_and_order(a, P.partition(a, p, DIMS), p)
         m = P.make_preconditioner(pc, a, layout)
@@ -46,15 +46,20 @@ def _solve_all(P):
     return out
 
 
-def _worker(rank, world, port, path, backend="gloo"):
+def _worker(rank, world, port, path, backend="gloo", cases=None, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
-                      LOCAL_RANK=str(rank) if backend == "nccl" else "0")
+                      LOCAL_RANK=str(rank) if backend == "nccl" else "0", DDILU_PEER="1" if peer else "0")
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import paper_2303_08881_b200 as P
     from paper_2303_08881_b200 import dist
     comm = dist.init_from_env(backend=backend)
     assert comm.size == world and comm.rank == rank
-    res = _solve_all(P)
+    assert isinstance(comm, dist.PeerComm) == bool(peer)
+    res = _solve_all(P, cases)
+    if peer:
+        comm.check()                      # no bounded wait ran out
+        res["_peer"] = {"reductions": comm.red_seq, "halo_exchanges": comm.halo_seq}
+        comm.close()
     with open(f"{path}.{rank}", "w") as fh:
         json.dump(res, fh)
     import torch.distributed as tdist
@@ -62,12 +67,12 @@ def _worker(rank, world, port, path, backend="gloo"):
     tdist.destroy_process_group()
 
 
-def _run_two_ranks(tmp_path, backend):
+def _run_two_ranks(tmp_path, backend, cases=None, peer=False):
     import paper_2303_08881_b200 as P
-    single = _solve_all(P)
+    single = _solve_all(P, cases)
     world, port, path = 2, _free_port(), str(tmp_path / "res")
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_worker, args=(r, world, port, path, backend)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, path, backend, cases, peer)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -75,6 +80,9 @@ def _run_two_ranks(tmp_path, backend):
         assert p.exitcode == 0
     for rank in range(world):
         multi = json.load(open(f"{path}.{rank}"))
+        if peer:
+            used = multi.pop("_peer")
+            assert used["reductions"] > 100 and used["halo_exchanges"] > 100, used     # the peer kernels carried the solve
         for key, ref in single.items():
             got = multi[key]
             assert got["n_halo"] > 0 and got["n_loc"] < ref["n_loc"], key      # really distributed
@@ -97,3 +105,12 @@ def test_two_ranks_nccl(tmp_path):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs (NCCL path; covered over gloo by test_two_ranks_match_single_rank)")
     _run_two_ranks(tmp_path, "nccl")
+
+
+def test_two_ranks_peer_memory(tmp_path):
+    """The same comparison with the exchanges over PEER MEMORY (csrc/peer.cu, dist.PeerComm): halo values stored
+    straight into the other rank's mailbox (CUDA IPC mapping) and published by sequence flags, dot / norm scalars
+    reduced by one kernel per rank that polls its own flags -- no collective call on the solve path.  Two processes
+    share the one GPU here (their kernels alternate by time slicing, every hand-over costs a time slice); with one
+    GPU per rank the same code runs over NVLink."""
+    _run_two_ranks(tmp_path, "gloo", cases=[("schur", 8), ("bj", 4)], peer=True)
