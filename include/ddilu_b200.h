@@ -200,19 +200,22 @@ int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const in
  * CUDA IPC; the tables `slots` / `data` / `flags` / `acks` hold, per rank, the address of that rank's region in THIS
  * process.  seq = 1, 2, ... per exchange kind; waits are bounded by spin_cycles (*err != 0: a peer never arrived).
  * ddilu_peer_allreduce: out[i] = sum over ranks, in rank order, of partial_r[i] (i < k <= kmax); one launch.
- * ddilu_peer_send: send[off[d] .. off[d+1]) into rank d's data[seq & 1][rank][..], then its halo flag [rank] = seq
- * (after rank d acknowledged seq - 2: `ack` = my acknowledgement flags).
+ * ddilu_peer_send: message values off[d] .. off[d+1] (value j = send[j], or send[idx[j]]: the pack of the interface
+ * values fused into the send) into rank d's data[seq & 1][rank][..], then its halo flag [rank] = seq (after rank d
+ * acknowledged seq - 2: `ack` = my acknowledgement flags).
  * ddilu_peer_recv: recv[off[s] .. off[s+1]) from my data[seq & 1][s][..] once my halo flag [s] >= seq (the own part
  * from self_send + self_off), then rank s's acknowledgement flag [rank] = seq. */
 int ddilu_peer_allreduce(int k, int kmax, const double *partial, double *out, const unsigned long long *slots,
                          const unsigned long long *flags, int rank, int size, long long seq, long long spin_cycles,
                          int *err, void *stream);
-int ddilu_peer_send(int size, int rank, int total, const double *send, const int *off, const unsigned long long *data,
+int ddilu_peer_send(int size, int rank, int total, const double *send, const int *idx, const int *off,
+                    const unsigned long long *data,
                     const unsigned long long *flags, const long long *ack, long long cap, long long seq,
                     long long spin_cycles, unsigned int *counter, int *err, void *stream);
 int ddilu_peer_recv(int size, int rank, int total, double *recv, const int *off, const double *mydata,
-                    const long long *myflags, const unsigned long long *acks, const double *self_send, int self_off,
-                    long long cap, long long seq, long long spin_cycles, unsigned int *counter, int *err, void *stream);
+                    const long long *myflags, const unsigned long long *acks, const double *self_send,
+                    const int *self_idx, int self_off, long long cap, long long seq, long long spin_cycles,
+                    unsigned int *counter, int *err, void *stream);
 
 /* ---- factor.py:198-216 `_split_counts` + :435-443 `_row_inf_norms` */
 int ddilu_split_count(int n, const int *a_rp, const int *a_ci, const double *a_v, int n_elim, int *pc, int *kc,

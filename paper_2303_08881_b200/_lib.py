@@ -66,8 +66,8 @@ SIGNATURES = {
     "ddilu_csweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _L, _P, _P, _P, _P, _P, _P]),
     "ddilu_csweep_solve": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_peer_allreduce": (_I, [_I, _I, _P, _P, _P, _P, _I, _I, _L, _L, _P, _P]),
-    "ddilu_peer_send": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _L, _L, _L, _P, _P, _P]),
-    "ddilu_peer_recv": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P]),
+    "ddilu_peer_send": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _L, _L, _P, _P, _P]),
+    "ddilu_peer_recv": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P]),
     "ddilu_split_count": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ddilu_split_fill": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_ilu0_numeric": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _D, _P, _P, _P]),

@@ -73,9 +73,11 @@ __global__ void peer_allreduce_kernel(int k, int kmax, const double *__restrict_
     }
 }
 
-// send[off[d] .. off[d + 1]) -> rank d's halo buffer data[buf][rank][0 ..), then data_seq_d[rank] = seq.
+// value j of the message = send[j], or send[idx[j]] when idx is given (the pack of the interface values fused into
+// the send).  Values off[d] .. off[d + 1] -> rank d's halo buffer data[buf][rank][0 ..), then data_seq_d[rank] = seq.
 // ack[d]: my flag that rank d raises when it has consumed a message (seq - 2 used the same buffer).
-__global__ void peer_send_kernel(int size, int rank, const double *__restrict__ send, const int *__restrict__ off,
+__global__ void peer_send_kernel(int size, int rank, const double *__restrict__ send, const int *__restrict__ idx,
+                                 const int *__restrict__ off,
                                  const unsigned long long *__restrict__ data, const unsigned long long *__restrict__ flags,
                                  const long long *ack, long long cap, long long seq, long long spin_cycles,
                                  unsigned int *counter, int *err) {
@@ -92,7 +94,7 @@ __global__ void peer_send_kernel(int size, int rank, const double *__restrict__ 
             int d = 0;
             while (off[d + 1] <= j) ++d;          // a handful of ranks
             if (d == rank) continue;
-            ((double *)data[d])[((size_t)buf * size + rank) * cap + (j - off[d])] = send[j];
+            ((double *)data[d])[((size_t)buf * size + rank) * cap + (j - off[d])] = send[idx ? idx[j] : j];
         }
     }
     __threadfence_system();
@@ -112,8 +114,8 @@ __global__ void peer_send_kernel(int size, int rank, const double *__restrict__ 
 __global__ void peer_recv_kernel(int size, int rank, double *__restrict__ recv, const int *__restrict__ off,
                                  const double *__restrict__ mydata, const long long *myflags,
                                  const unsigned long long *__restrict__ acks, const double *__restrict__ self_send,
-                                 int self_off, long long cap, long long seq, long long spin_cycles,
-                                 unsigned int *counter, int *err) {
+                                 const int *__restrict__ self_idx, int self_off, long long cap, long long seq,
+                                 long long spin_cycles, unsigned int *counter, int *err) {
     __shared__ int ok;
     if (threadIdx.x == 0) ok = 1;
     __syncthreads();
@@ -126,7 +128,8 @@ __global__ void peer_recv_kernel(int size, int rank, double *__restrict__ recv, 
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gridDim.x * blockDim.x) {
             int s = 0;
             while (off[s + 1] <= j) ++s;
-            recv[j] = s == rank ? self_send[self_off + (j - off[s])]
+            const int q = self_off + (j - off[s]);
+            recv[j] = s == rank ? self_send[self_idx ? self_idx[q] : q]
                                 : peer_ld_l2(mydata + ((size_t)buf * size + s) * cap + (j - off[s]));
         }
     }
@@ -158,7 +161,7 @@ extern "C" int ddilu_peer_allreduce(int k, int kmax, const double *partial, doub
     return DDILU_OK;
 }
 
-extern "C" int ddilu_peer_send(int size, int rank, int total, const double *send, const int *off,
+extern "C" int ddilu_peer_send(int size, int rank, int total, const double *send, const int *idx, const int *off,
                                const unsigned long long *data, const unsigned long long *flags, const long long *ack,
                                long long cap, long long seq, long long spin_cycles, unsigned int *counter, int *err,
                                void *stream) {
@@ -166,22 +169,22 @@ extern "C" int ddilu_peer_send(int size, int rank, int total, const double *send
     const int threads = 256;
     int grid = div_up(total > 0 ? total : 1, threads * 4);
     if (grid > 64) grid = 64;
-    peer_send_kernel<<<grid, threads, 0, ST(stream)>>>(size, rank, send, off, data, flags, ack, cap, seq, spin_cycles,
-                                                       counter, err);
+    peer_send_kernel<<<grid, threads, 0, ST(stream)>>>(size, rank, send, idx, off, data, flags, ack, cap, seq,
+                                                       spin_cycles, counter, err);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
 
 extern "C" int ddilu_peer_recv(int size, int rank, int total, double *recv, const int *off, const double *mydata,
                                const long long *myflags, const unsigned long long *acks, const double *self_send,
-                               int self_off, long long cap, long long seq, long long spin_cycles,
+                               const int *self_idx, int self_off, long long cap, long long seq, long long spin_cycles,
                                unsigned int *counter, int *err, void *stream) {
     if (size < 1 || size > 64 || rank < 0 || rank >= size) return DDILU_ERR_ARG;
     const int threads = 256;
     int grid = div_up(total > 0 ? total : 1, threads * 4);
     if (grid > 64) grid = 64;
-    peer_recv_kernel<<<grid, threads, 0, ST(stream)>>>(size, rank, recv, off, mydata, myflags, acks, self_send, self_off,
-                                                       cap, seq, spin_cycles, counter, err);
+    peer_recv_kernel<<<grid, threads, 0, ST(stream)>>>(size, rank, recv, off, mydata, myflags, acks, self_send, self_idx,
+                                                       self_off, cap, seq, spin_cycles, counter, err);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -198,22 +198,30 @@ class PeerComm(Comm):
             self._offs[key] = (torch.tensor(off, dtype=torch.int32, device=self._dev), off)
         return self._offs[key]
 
-    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor, recv_counts, send_counts, async_op: bool = False):
+    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor, recv_counts, send_counts, async_op: bool = False,
+                   idx: torch.Tensor | None = None):
+        """Variable-size exchange; with idx (int32) value j of the outgoing message is send[idx[j]] -- the pack of
+        the interface values is fused into the sending kernel."""
         if not self.active:
             return None
         if max(max(recv_counts), max(send_counts)) > self.cap:
+            if idx is not None:
+                packed = torch.empty(idx.numel(), dtype=send.dtype, device=send.device)
+                self._D.gather(idx.numel(), idx, send, packed)
+                send = packed
             return self.base.all_to_all(recv, send, recv_counts, send_counts, async_op=async_op)
         soff_d, soff = self._offsets(send_counts)
         roff_d, roff = self._offsets(recv_counts)
         self.halo_seq += 1
         seq = self.halo_seq
         call = self._D.call
-        call("ddilu_peer_send", self.size, self.rank, soff[-1], send, soff_d, self._data, self._halo_flags, self._my_ack,
-             self.cap, seq, self.spin_cycles, self._counters[0:1], self.err)
+        call("ddilu_peer_send", self.size, self.rank, soff[-1], send, idx, soff_d, self._data, self._halo_flags,
+             self._my_ack, self.cap, seq, self.spin_cycles, self._counters[0:1], self.err)
 
         def finish():
             call("ddilu_peer_recv", self.size, self.rank, roff[-1], recv, roff_d, self._my_data, self._my_halo_flags,
-                 self._ack_flags, send, soff[self.rank], self.cap, seq, self.spin_cycles, self._counters[1:2], self.err)
+                 self._ack_flags, send, idx, soff[self.rank], self.cap, seq, self.spin_cycles, self._counters[1:2],
+                 self.err)
 
         if async_op:
             return _PeerWork(finish)

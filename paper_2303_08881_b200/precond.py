@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import device as D
-from .dist import Comm, domains_of_rank, get_comm
+from .dist import Comm, PeerComm, domains_of_rank, get_comm
 from .factor import (DevFactors, DevPartial, FillRule, IluFactors, MiluVectors, PartialIluFactors, TwoLevelBlocks,
                      d_carve, d_factor_level0, d_factorize, d_partial_ilu, solve_with_product)
 from .krylov import InnerGmres, KrylovConfig, restarted_device
@@ -224,6 +224,9 @@ class LocalSystem:
         if not self.comm.active:
             return None
         ns = sum(self.send_counts)
+        if isinstance(self.comm, PeerComm):      # peer memory: the pack is part of the sending kernel
+            return self.comm.all_to_all(halo_out[: self.n_halo], src_ext, self.recv_counts, self.send_counts,
+                                        async_op=async_op, idx=self.send_idx)
         D.gather(ns, self.send_idx, src_ext, self._sendbuf)
         return self.comm.all_to_all(halo_out[: self.n_halo], self._sendbuf[:ns], self.recv_counts, self.send_counts,
                                     async_op=async_op)
