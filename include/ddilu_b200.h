@@ -89,11 +89,13 @@ int ddilu_sptrsv_sell(int n, int n_slots, int n_levels, const int *order, const 
 
 /* ---- factor.py:270-369 `_iluk_symbolic`: level-of-fill pattern (levels <= klevel), rows >= n_elim keep
  * their trailing block un-eliminated.  Row slabs of row_cap entries: p_* = pivot (L) part, k_* = kept
- * (U / Schur) part with fill levels; *status != 0: a row outgrew row_cap (retry with a larger one).
+ * (U / Schur) part with fill levels; *status != 0: a row outgrew row_cap (retry with a larger one).  order (NULL =
+ * index order): processing order of the rows, any permutation in which a row follows its pivot rows.
  * ddilu_compact_cols: slab -> CSR columns; ddilu_prefill: factor.py:372-390 `_prefill`. */
 long long ddilu_iluk_smem_bytes(int row_cap);
 int ddilu_iluk_symbolic(int n, const int *a_rp, const int *a_ci, int n_elim, int klevel, int row_cap, int *p_cnt,
-                        int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status, void *stream);
+                        int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status, const int *order,
+                        void *stream);
 int ddilu_compact_cols(int n, int cap, const int *cnt, const int *ci, const int *out_rp, int *out_ci, void *stream);
 int ddilu_prefill(int n, const int *a_rp, const int *a_ci, const double *a_v, const int *rp, const int *ci, double *v,
                   int n_elim, int upper_part, void *stream);

@@ -10,8 +10,9 @@ MAX_ROW_CAP = 3000  # 4 warps x 16 B x cap must fit the 200 KB shared-memory bud
 MIN_ROW_CAP = 32    # first try: max(MIN_ROW_CAP, 2 (level + 1) (longest row + 1)); doubled on overflow
 
 
-def d_iluk_split(a: D.DeviceCsr, n_elim: int, level: int):
-    """(L pattern + prefilled values, kept pattern + prefilled values) of ILU(level)."""
+def d_iluk_split(a: D.DeviceCsr, n_elim: int, level: int, order=None):
+    """(L pattern + prefilled values, kept pattern + prefilled values) of ILU(level); order: processing order of the
+    rows for the symbolic kernel (`_ilut.interleaved_order`), the pattern does not depend on it."""
     n = a.n_rows
     lens = D.empty_i32(max(n, 1))
     call("ddilu_row_lengths", n, a.rp, lens)
@@ -23,7 +24,7 @@ def d_iluk_split(a: D.DeviceCsr, n_elim: int, level: int):
         slots = max(1, n * row_cap)
         p_ci, k_ci, k_lv = D.empty_i32(slots), D.empty_i32(slots), D.empty_i32(slots)
         call("ddilu_iluk_symbolic", n, a.rp, a.ci, int(n_elim), int(level), int(row_cap), p_cnt, p_ci, k_cnt, k_ci,
-             k_lv, done, status)
+             k_lv, done, status, order)
         if int(status.item()) == 0:
             break
         if row_cap >= MAX_ROW_CAP:

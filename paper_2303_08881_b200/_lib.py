@@ -37,7 +37,7 @@ SIGNATURES = {
     "ddilu_compose_wait": (_I, [_I, _P, _P, _P, _P, _P]),
     "ddilu_sptrsv_sell": (_I, [_I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),
     "ddilu_iluk_smem_bytes": (_L, [_I]),
-    "ddilu_iluk_symbolic": (_I, [_I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_iluk_symbolic": (_I, [_I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ddilu_compact_cols": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "ddilu_prefill": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "ddilu_tile_box_keys": (_I, [_I, _P, _I, _P, _P, _P, _P, _P, _P]),

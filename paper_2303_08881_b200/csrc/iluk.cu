@@ -27,14 +27,17 @@ constexpr int ILUK_WARPS = 4;
 
 __global__ void __launch_bounds__(ILUK_WARPS * 32)
 iluk_symbolic_kernel(int n, const int *__restrict__ a_rp, const int *__restrict__ a_ci, int n_elim, int klevel, int cap,
-                     int *p_cnt, int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status) {
+                     int *p_cnt, int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status,
+                     const int *__restrict__ order) {
     extern __shared__ int iluk_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int *ca = iluk_smem + (size_t)wib * (4 * cap + 32), *cb = ca + cap, *la = cb + cap, *lb = la + cap;
     int *insj = lb + cap;
     const long long W = (long long)gridDim.x * ILUK_WARPS;
-    for (long long row = (long long)blockIdx.x * ILUK_WARPS + wib; row < n; row += W) {
-        const int i = (int)row;
+    // rows in PROCESSING order (order[slot], any order in which a row follows its pivot rows: the caller interleaves
+    // the independent diagonal blocks so that all of them advance at once), else index order
+    for (long long slot = (long long)blockIdx.x * ILUK_WARPS + wib; slot < n; slot += W) {
+        const int i = order ? order[slot] : (int)slot;
         const int lim = i < n_elim ? i : n_elim;
         const int a0 = a_rp[i], len0 = a_rp[i + 1] - a0;
         bool overflow = false;
@@ -191,7 +194,7 @@ extern "C" long long ddilu_iluk_smem_bytes(int row_cap) {
 
 extern "C" int ddilu_iluk_symbolic(int n, const int *a_rp, const int *a_ci, int n_elim, int klevel, int row_cap,
                                    int *p_cnt, int *p_ci, int *k_cnt, int *k_ci, int *k_lv, int *done, int *status,
-                                   void *stream) {
+                                   const int *order, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) return DDILU_OK;
     if (row_cap < 2 || klevel < 0) return DDILU_ERR_ARG;
@@ -207,7 +210,8 @@ extern "C" int ddilu_iluk_symbolic(int n, const int *a_rp, const int *a_ci, int 
     const long long need = div_up(n, ILUK_WARPS);
     if (grid > need) grid = need;
     int g = (int)grid;
-    void *args[] = {&n, &a_rp, &a_ci, &n_elim, &klevel, &row_cap, &p_cnt, &p_ci, &k_cnt, &k_ci, &k_lv, &done, &status};
+    void *args[] = {&n, &a_rp, &a_ci, &n_elim, &klevel, &row_cap, &p_cnt, &p_ci, &k_cnt, &k_ci, &k_lv, &done, &status,
+                    &order};
     DDILU_CHECK(cudaLaunchCooperativeKernel((void *)iluk_symbolic_kernel, g, ILUK_WARPS * 32, args, smem, st));
     return DDILU_OK;
 }

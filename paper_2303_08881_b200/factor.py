@@ -230,13 +230,15 @@ def d_level0_split(a: D.DeviceCsr, n_elim: int):
 
 
 def d_factor_level0(a: D.DeviceCsr, n_elim: int, milu: bool = False, target: torch.Tensor | None = None,
-                    wvec: torch.Tensor | None = None, safeguard: float = DIAG_SAFEGUARD, level: int = 0) -> DevFactors:
+                    wvec: torch.Tensor | None = None, safeguard: float = DIAG_SAFEGUARD, level: int = 0,
+                    sections=None) -> DevFactors:
     """factor.py:446-458 `_factor_on_pattern`: split (level 0) or symbolic level-of-fill pattern
     (level > 0, factor.py:704-720, 855-863), schedule, numeric sweep."""
     n = a.n_rows
     if level > 0 and n:
         from ._iluk import d_iluk_split
-        lo, up = d_iluk_split(a, n_elim, level)
+        from ._ilut import interleaved_order
+        lo, up = d_iluk_split(a, n_elim, level, interleaved_order(n, sections) if sections is not None else None)
         rownorm = D.empty_f64(n)                     # row inf-norms of A: by-product of the split's count pass
         D.call("ddilu_split_count", n, a.rp, a.ci, a.val, int(n_elim), D.empty_i32(n + 1), D.empty_i32(n + 1), rownorm)
     else:
@@ -260,7 +262,8 @@ def d_ilut(a: D.DeviceCsr, n_elim: int, tau: float, maxfill: int, tau_s: float,
 
 def d_factorize(a: D.DeviceCsr, rule: FillRule, safeguard: float = DIAG_SAFEGUARD, sections=None) -> DevFactors:
     if rule.kind == "ilu0" or rule.kind == "iluk":
-        return d_factor_level0(a, a.n_rows, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
+        return d_factor_level0(a, a.n_rows, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0,
+                               sections=sections)
     return d_ilut(a, a.n_rows, rule.tau, rule.maxfill, 0.0, safeguard, sections)
 
 
@@ -306,7 +309,8 @@ def d_partial_ilu(a: D.DeviceCsr, n_interior: int, rule: FillRule, schur_drop_to
         f = d_ilut(a, n_interior, rule.tau, rule.maxfill, schur_drop_tol, safeguard, sections=blocks)
         drop_tol = 0.0
     else:
-        f = d_factor_level0(a, n_interior, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0)
+        f = d_factor_level0(a, n_interior, safeguard=safeguard, level=rule.level if rule.kind == "iluk" else 0,
+                            sections=blocks)
         drop_tol = schur_drop_tol
     l_b, u_b, w, z, _, s_tilde = d_carve(f, n_interior)
     s_tilde = d_drop_small_rows(s_tilde, drop_tol)
