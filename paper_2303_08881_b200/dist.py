@@ -143,6 +143,14 @@ class PeerComm(Comm):
         handles = [None] * size
         tdist.all_gather_object(handles, (fn, args), group=self.group)
         self._peers = [self._mail if r == self.rank else handles[r][0](*handles[r][1]) for r in range(size)]
+        # kernels of THIS device dereference the peers' pointers: make sure peer access is on (torch enables it on
+        # the first device-to-device copy between a pair of devices) and refuse pairs without it
+        probe = torch.zeros(1, dtype=torch.int64, device=self._dev)
+        for r, t in enumerate(self._peers):
+            if r != self.rank and t.device != self._dev:
+                if not torch.cuda.can_device_access_peer(self._dev.index, t.device.index):
+                    raise RuntimeError(f"no peer access from {self._dev} to {t.device}")
+                probe.copy_(t[-1:])               # (the last word of a mailbox: halo data, zero at this point)
         base = [int(t.data_ptr()) for t in self._peers]
         i64 = torch.int64
 
