@@ -914,13 +914,14 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         rlen = (fac.rp[1:] - fac.rp[:-1]).to(i64)
         erow = torch.repeat_interleave(rows, rlen)
         ecol = fac.ci[:nnz].to(i64)
-        if bool((blk[ecol] != blk[erow]).any().item()):
+        cta_r, cta_c = cta[erow], cta[ecol]                    # CTA of the reader / of the dependency, per entry
+        if bool((cta_r // csize != cta_c // csize).any().item()):      # a dependency leaves its block
             return None
         dep = ecol != erow
         # halo: (consumer CTA, producer row) pairs whose CTAs differ; a CTA numbers the values it holds level by
         # level -- own rows of the level, then the level's halo values (in row order)
-        remote = dep & (cta[erow] != cta[ecol])
-        hkey_e = cta[erow] * n + ecol
+        remote = dep & (cta_r != cta_c)
+        hkey_e = cta_r * n + ecol
         hu = torch.unique(hkey_e[remote])                      # sorted by (consumer CTA, producer row)
         h_cta, h_row = hu // n, hu % n
         h_lev = lv[h_row]
@@ -941,7 +942,7 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
             hit = torch.searchsorted(hu, hkey_e[remote])
             e_wpos = e_wpos.clone()
             e_wpos[remote] = h_wpos[hit]
-        need = torch.where(dep, wend.reshape(-1)[cta[erow] * nlev + lv[erow]] - e_wpos, torch.zeros_like(ecol))
+        need = torch.where(dep, wend.reshape(-1)[cta_r * nlev + lv[erow]] - e_wpos, torch.zeros_like(ecol))
         max_need = int(need.max().item()) if nnz else 1
         # push targets of every row: the other CTAs that hold its value, (slot << 4 | rank)
         NP = query("ddilu_csweep_max_push")
@@ -954,9 +955,13 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         max_lev = int(nlev_b.max().item())
         width_cta = int(ncl.max().item())
         # chunks that are ranges of consecutive rows need no row ids
-        row_lo = torch.full((nb * csize * nlev,), n, dtype=i64, device=d).scatter_reduce_(0, ckey, rows, "amin")
-        row_hi = torch.full((nb * csize * nlev,), -1, dtype=i64, device=d).scatter_reduce_(0, ckey, rows, "amax")
+        # (`order` lists the rows by block, level, index, and a chunk is a run of it: first and last row by lookup)
         nclf = ncl.reshape(-1)
+        blk_first = (seg[:-1].view(nb, 1) + lev_start).view(nb, 1, nlev)          # run of a (block, level) in `order`
+        run0 = (blk_first + ranks * cs.view(nb, 1, nlev)).expand(nb, csize, nlev).reshape(-1)
+        some = nclf > 0
+        row_lo = torch.where(some, order[torch.where(some, run0, torch.zeros_like(run0))], torch.full_like(run0, n))
+        row_hi = torch.where(some, order[torch.where(some, run0 + nclf - 1, torch.zeros_like(run0))], torch.full_like(run0, -1))
         consecutive = (nclf == 0) | (row_hi - row_lo + 1 == nclf)
         contiguous = bool(consecutive.all().item())
         row0 = torch.where((nclf > 0) & consecutive, row_lo, torch.full_like(row_lo, -1))
