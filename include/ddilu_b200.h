@@ -174,18 +174,19 @@ int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const 
  * into chunks, one per CTA; a CTA keeps the values it needs (own results and halo values of other CTAs) in a
  * shared-memory window; a producer pushes a result into the windows of the other CTAs that need it through
  * distributed shared memory (st.async completing bytes on the consumer's mbarrier); one mbarrier wait per level.
- * ddilu_csweep_fill: operands of a factor in CTA-local schedule order (k = operand slots per row: 3 or 4;
+ * ddilu_csweep_fill: operands of a factor in CTA-local schedule order (k = operand slots per row: 3, 4 or 20;
  * gpos = position of the row in the operand arrays, dep_slot = per stored entry the window slot of that dependency
  * in the READER's CTA; np = length of the position space; coef[k][np]; code[code_words(k)][np]: the 16-bit halves
- * of a row's words are its k dependency slots (filled here) and then its max_push push targets slot << 4 | rank,
- * 0xffff = none (filled by the caller); rowid[np]; piv[2][np] = pivot and its reciprocal (upper only)).
+ * of a row's words are its k dependency slots (filled here) and then its max_push(k) push targets
+ * slot << rank_bits(k) | rank, 0xffff = none (filled by the caller); rowid[np]; piv[2][np] = pivot and its reciprocal (upper only)).
  * ddilu_csweep_solve: ctas = 4 ints per CTA {first position, rows, first step, steps}; steps = 8 ints per step
  * {start (a multiple of 4), end (positions, at most `threads` rows), window slot of the first row, first row when
  * the rows are consecutive else -1 (rowid is read), halo bytes arriving for the level (first step of a level),
  * flags 1 = first | 2 = last step of its level, 0, 0}; depth = stages of the operand ring (2..4). */
-int ddilu_csweep_threads(void);
-int ddilu_csweep_window(void);
-int ddilu_csweep_max_push(void);
+int ddilu_csweep_threads(int k);      /* k selects the kernel shape: 3, 4 = short rows, 20 = long rows (27-point / ILUT) */
+int ddilu_csweep_window(int k);
+int ddilu_csweep_max_push(int k);
+int ddilu_csweep_rank_bits(int k);    /* a push target is slot << rank_bits | rank: clusters of <= 1 << rank_bits CTAs */
 int ddilu_csweep_code_words(int k);
 long long ddilu_csweep_smem_bytes(int k, int upper, int depth, int max_steps);
 int ddilu_csweep_active_clusters(int cluster_size, int k, int depth, int max_steps);

@@ -57,9 +57,10 @@ SIGNATURES = {
     "ddilu_sweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "ddilu_sweep_rhs": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ddilu_sweep_solve": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
-    "ddilu_csweep_threads": (_I, []),
-    "ddilu_csweep_window": (_I, []),
-    "ddilu_csweep_max_push": (_I, []),
+    "ddilu_csweep_threads": (_I, [_I]),
+    "ddilu_csweep_window": (_I, [_I]),
+    "ddilu_csweep_max_push": (_I, [_I]),
+    "ddilu_csweep_rank_bits": (_I, [_I]),
     "ddilu_csweep_code_words": (_I, [_I]),
     "ddilu_csweep_smem_bytes": (_L, [_I, _I, _I, _I]),
     "ddilu_csweep_active_clusters": (_I, [_I, _I, _I, _I]),

@@ -39,24 +39,42 @@
 
 namespace ddilu {
 
-constexpr int CS_WINDOW = 4095;       // doubles per CTA; slot CS_WINDOW holds 0.0
 constexpr int CS_STEP_INTS = 8;       // per CTA and step: first / end operand position, window slot of the first row,
                                       // first row (-1: row ids), halo bytes of the level, flags, 0, 0
 constexpr int CS_CTA_INTS = 4;        // per CTA: first position in the operand arrays, signal mask | arrivals << 16, first step, number of steps
-constexpr int CS_NP = 3;              // push targets per row
 constexpr unsigned CS_NO_PUSH = 0xffffu;
 constexpr int CS_WAIT = 1, CS_ARRIVE = 2;   // step flags: first / last step of its level
-constexpr int CS_NT = 768;            // compute threads of a CTA = rows of a step at most; one more warp feeds the ring
-constexpr int CS_THREADS = CS_NT + 32;
 constexpr int CS_MAX_DEPTH = 4;
-__host__ __device__ constexpr int cs_words(int K) { return (K + CS_NP + 1) / 2; }   // 32-bit words holding a row's K slots and CS_NP push targets
+
+// Two shapes of the kernel, chosen by the operand slots per row K:
+//   short rows (K <= 4: 5- / 7-point ILU(0) factors): wide levels -- 768 compute threads, a window of 4 095 doubles,
+//     three push targets per row as slot << 4 | rank (clusters up to 16), the step table in shared memory;
+//   long rows (K = 20: 27-point / ILUT factors): narrow deep levels that reach further back -- 256 compute threads, a
+//     window of 8 191 doubles, four push targets as slot << 3 | rank (clusters up to 8), the step table (thousands
+//     of levels) read from global memory one step ahead.
+template <int K>
+struct CsCfg {
+    static constexpr bool LONG = K > 4;
+    static constexpr int NT = LONG ? 256 : 768;           // compute threads = rows of a step at most; one more warp feeds the ring
+    static constexpr int WIN = LONG ? 8191 : 4095;        // doubles per CTA; slot WIN holds 0.0
+    static constexpr int RB = LONG ? 3 : 4;               // rank bits of a push target
+    static constexpr int NP = LONG ? 4 : 3;               // push targets per row
+    static constexpr int NW = (K + NP + 1) / 2;           // 32-bit words holding a row's K slots and NP push targets
+    static constexpr bool TABLE_IN_SMEM = !LONG;
+};
+__host__ __device__ constexpr bool cs_long(int K) { return K > 4; }
+__host__ __device__ constexpr int cs_nt(int K) { return cs_long(K) ? 256 : 768; }
+__host__ __device__ constexpr int cs_win(int K) { return cs_long(K) ? 8191 : 4095; }
+__host__ __device__ constexpr int cs_rb(int K) { return cs_long(K) ? 3 : 4; }
+__host__ __device__ constexpr int cs_np(int K) { return cs_long(K) ? 4 : 3; }
+__host__ __device__ constexpr int cs_words(int K) { return (K + cs_np(K) + 1) / 2; }
 
 struct CSweepArgs {
     const int *ctas;                  // CS_CTA_INTS per CTA (block-major, rank-minor)
     const int *steps;                 // CS_STEP_INTS per CTA and step
     const double *coef;               // [K][np]
-    const unsigned *code;             // [cs_words(K)][np]: 16-bit halves = K window slots of the dependencies, then CS_NP
-                                      // push targets slot << 4 | rank (0xffff = none)
+    const unsigned *code;             // [cs_words(K)][np]: 16-bit halves = K window slots of the dependencies, then the
+                                      // push targets slot << rank bits | rank (0xffff = none)
     const int *rowid;                 // [np]
     const double *piv;                // [2][np]: pivot, reciprocal (upper)
     const double *b;                  // right-hand side by row
@@ -70,11 +88,14 @@ struct CSweepArgs {
 // a stage of the operand ring (structure of arrays, slot = row of the step):
 // coef[K][NT] | pivot pairs[2][NT] (upper) | rhs[NT + 2] | words[NW][NT] | row ids[NT]
 __host__ __device__ constexpr int cs_stage_bytes(int K, bool upper) {
-    return CS_NT * (8 * K + (upper ? 16 : 0) + 4 * cs_words(K) + 4) + 8 * (CS_NT + 2);
+    return cs_nt(K) * (8 * K + (upper ? 16 : 0) + 4 * cs_words(K) + 4) + 8 * (cs_nt(K) + 2);
 }
 __host__ __device__ inline size_t cs_ctl_bytes() { return (2 + 2 * CS_MAX_DEPTH) * 8; }   // level pair, full[], empty[]
+__host__ __device__ inline size_t cs_table_bytes(int K, int max_steps) {
+    return cs_long(K) ? 0 : (size_t)max_steps * CS_STEP_INTS * 4;
+}
 __host__ __device__ inline size_t cs_smem_bytes(int K, bool upper, int depth, int max_steps) {
-    size_t b = cs_ctl_bytes() + (size_t)max_steps * CS_STEP_INTS * 4 + ((size_t)CS_WINDOW + 1) * 8;
+    size_t b = cs_ctl_bytes() + cs_table_bytes(K, max_steps) + ((size_t)cs_win(K) + 1) * 8;
     b = (b + 127) & ~(size_t)127;
     return b + (size_t)depth * cs_stage_bytes(K, upper);
 }
@@ -184,9 +205,11 @@ __device__ __forceinline__ uint32_t cs_half(const uint32_t *w, int i) {     // 1
 //                        K window loads, multiply / subtract chain [, division], window store, pushes;
 //                        (last step of a level) arrive at every CTA's mbarrier of the level; result to global memory
 template <int K, bool UPPER>
-__global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs a) {
-    constexpr int NT = CS_NT;
-    constexpr int NW = cs_words(K);
+__global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSweepArgs a) {
+    using Cfg = CsCfg<K>;
+    constexpr int NT = Cfg::NT, NW = Cfg::NW, CS_WINDOW = Cfg::WIN, CS_NP = Cfg::NP, RB = Cfg::RB;
+    constexpr int CS_THREADS = NT + 32;
+    constexpr uint32_t RMASK = (1u << RB) - 1u;
     constexpr int STAGE = cs_stage_bytes(K, UPPER);
     constexpr int OFF_PIV = 8 * K * NT, OFF_RHS = OFF_PIV + (UPPER ? 16 * NT : 0), OFF_W = OFF_RHS + 8 * (NT + 2),
                   OFF_ID = OFF_W + 4 * NW * NT;
@@ -205,20 +228,20 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
     const int D = a.depth;
     uint64_t *bars = (uint64_t *)cs_smem;                     // [2]: levels of even / odd index, then full[], empty[]
     int4 *steps = (int4 *)(cs_smem + cs_ctl_bytes());
-    double *xs = (double *)((unsigned char *)steps + (size_t)a.max_steps * CS_STEP_INTS * 4);
-    size_t ring_off = cs_ctl_bytes() + (size_t)a.max_steps * CS_STEP_INTS * 4 + ((size_t)CS_WINDOW + 1) * 8;
+    double *xs = (double *)((unsigned char *)steps + cs_table_bytes(K, a.max_steps));
+    size_t ring_off = cs_ctl_bytes() + cs_table_bytes(K, a.max_steps) + ((size_t)CS_WINDOW + 1) * 8;
     ring_off = (ring_off + 127) & ~(size_t)127;
-    {
-        const int4 *src = (const int4 *)a.steps + 2 * (size_t)step_off;
-        for (int i = tid; i < 2 * nsteps; i += CS_THREADS) steps[i] = src[i];
-    }
+    const int4 *gsteps = (const int4 *)a.steps + 2 * (size_t)step_off;      // this CTA's step table
+    if (Cfg::TABLE_IN_SMEM)
+        for (int i = tid; i < 2 * nsteps; i += CS_THREADS) steps[i] = gsteps[i];
     const uint32_t bar_u32 = cs_smem_u32(bars), full_u32 = bar_u32 + 16, empty_u32 = full_u32 + 8 * CS_MAX_DEPTH;
     if (tid == 0) {
         xs[CS_WINDOW] = 0.0;                  // padded operands: coefficient 0 times this slot
         cs_mbar_init(bar_u32, (NT / 32) * signallers);
         cs_mbar_init(bar_u32 + 8, (NT / 32) * signallers);
         for (int s = 0; s < D; ++s) {
-            cs_mbar_init(full_u32 + 8 * s, 2);    // the feeder's arrive.expect_tx and its asynchronous cp.async arrive
+            // the feeder's arrive.expect_tx and its asynchronous cp.async arrive
+            cs_mbar_init(full_u32 + 8 * s, 2);
             cs_mbar_init(empty_u32 + 8 * s, NT / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -227,6 +250,10 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
     cs_cluster_sync();                        // every CTA of the cluster is running, its mbarriers are initialised
     const uint32_t st_u32 = cs_smem_u32(steps), xs_u32 = cs_smem_u32(xs), ring_u32 = cs_smem_u32(cs_smem + ring_off);
     const long long np = a.np;
+    // half h (0: positions, slot, first row; 1: halo bytes, flags) of the table entry of step i
+    auto entry = [&](int i, int h) -> int4 {
+        return Cfg::TABLE_IN_SMEM ? cs_lds_v4(st_u32 + 32u * (uint32_t)i + 16u * (uint32_t)h) : __ldg(gsteps + 2 * i + h);
+    };
 
     if (tid >= NT) {
         // ------------------------------------------------------------ feeder (one lane)
@@ -235,10 +262,12 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
             const unsigned *cd = a.code + base;
             const int *ids = a.rowid + base;
             const double *pv = a.piv + base;
+            const int4 none = make_int4(0, 0, 0, 0);
+            int4 sv = nsteps > 0 ? entry(0, 0) : none;      // (long rows: the table is in global memory, an entry ahead)
             int s = 0;
             uint32_t round = 0;               // how often the ring has wrapped
             for (int i = 0; i < nsteps; ++i) {
-                const int4 sv = cs_lds_v4(st_u32 + 32u * (uint32_t)i);
+                const int4 sv1 = i + 1 < nsteps ? entry(i + 1, 0) : none;
                 const int rows = sv.y - sv.x;
                 const uint32_t st = ring_u32 + (uint32_t)(s * STAGE), full = full_u32 + 8u * (uint32_t)s;
                 if (round) cs_mbar_wait(empty_u32 + 8u * (uint32_t)s, (round - 1) & 1u);
@@ -283,6 +312,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
                     cs_mbar_arrive(full);
                     cs_mbar_arrive(full);
                 }
+                sv = sv1;
                 if (++s == D) {
                     s = 0;
                     ++round;
@@ -318,15 +348,15 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
         // the table entry of a step is loaded one step ahead (its two shared-memory loads head the step's chain)
         int4 sv_n = make_int4(0, 0, 0, 0), tf_n = sv_n;
         if (nsteps) {
-            sv_n = cs_lds_v4(st_u32);
-            tf_n = cs_lds_v4(st_u32 + 16u);
+            sv_n = entry(0, 0);
+            tf_n = entry(0, 1);
         }
         for (int i = 0; i < nsteps; ++i) {
             const int4 sv = sv_n;
             const int4 tf = tf_n;                                            // halo bytes of the level, flags
             if (i + 1 < nsteps) {
-                sv_n = cs_lds_v4(st_u32 + 32u * (uint32_t)(i + 1));
-                tf_n = cs_lds_v4(st_u32 + 32u * (uint32_t)(i + 1) + 16u);
+                sv_n = entry(i + 1, 0);
+                tf_n = entry(i + 1, 1);
             }
             const uint32_t mybar = bar_u32 + 8u * (uint32_t)(lev & 1);       // phase of this level: own and (offset) peers'
             // the halo bytes of the level (before this warp's arrive: the phase cannot complete without them)
@@ -351,8 +381,8 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
                 if (sv.w >= 0) {
                     id = sv.w + tid;
                     rhs = cs_lds_at<OFF_RHS>(my8 + so + 8u * (uint32_t)(sv.w & 1));
-                } else {                                // rows by id: a dependent load on the spot (rare layouts)
-                    id = (int)cs_lds_u32_at<OFF_ID>(my4 + so);
+                } else {                                // rows by id (27-point blocks under RCM): a dependent load on the
+                    id = (int)cs_lds_u32_at<OFF_ID>(my4 + so);      // spot -- a gather by the feeder warp measured slower
                     rhs = __ldg(a.b + id);
                 }
 #pragma unroll
@@ -388,7 +418,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
 #pragma unroll
                     for (int k = 0; k < CS_NP; ++k) {
                         const uint32_t pp = cs_half(w, K + k);
-                        if (pp != CS_NO_PUSH) cs_push(cs_mapa(xs_u32 + 8u * (pp >> 4), pp & 15u), sum, cs_mapa(mybar, pp & 15u));
+                        if (pp != CS_NO_PUSH) cs_push(cs_mapa(xs_u32 + 8u * (pp >> RB), pp & RMASK), sum, cs_mapa(mybar, pp & RMASK));
                     }
                 }
                 res = sum;
@@ -422,7 +452,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) csweep_kernel(const CSweepArgs 
 template <bool UPPER>
 __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int *__restrict__ ci,
                                    const double *__restrict__ val, int K, const int *__restrict__ gpos,
-                                   const int *__restrict__ dep_slot, long long np, double *coef,
+                                   const int *__restrict__ dep_slot, int window, long long np, double *coef,
                                    unsigned short *code, int *rowid, double *piv, int *bad_row) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n) return;
@@ -446,7 +476,7 @@ __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int 
     }
     for (; kk < K; ++kk) {       // padding: coefficient 0 times the zero slot
         coef[(long long)kk * np + g] = 0.0;
-        code[2 * ((long long)(kk >> 1) * np + g) + (kk & 1)] = (unsigned short)CS_WINDOW;
+        code[2 * ((long long)(kk >> 1) * np + g) + (kk & 1)] = (unsigned short)window;
     }
     rowid[g] = row;
     if (UPPER) {
@@ -476,11 +506,11 @@ int cs_prepare(size_t smem) {
     return DDILU_OK;
 }
 
-inline void cs_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int n_clusters, int csize, size_t smem,
-                      cudaStream_t st) {
+inline void cs_config(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int n_clusters, int csize, int threads,
+                      size_t smem, cudaStream_t st) {
     cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3((unsigned)(n_clusters * csize));
-    cfg.blockDim = dim3((unsigned)CS_THREADS);
+    cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -498,7 +528,7 @@ int cs_launch(int n_blocks, int csize, const CSweepArgs &a, cudaStream_t st) {
     if (rc) return rc;
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
-    cs_config(cfg, at, n_blocks, csize, smem, st);
+    cs_config(cfg, at, n_blocks, csize, cs_nt(K) + 32, smem, st);
     DDILU_CHECK(cudaLaunchKernelEx(&cfg, csweep_kernel<K, UPPER>, a));
     return DDILU_OK;
 }
@@ -509,7 +539,7 @@ int cs_active(int csize, size_t smem, int *out) {
     if (rc) return rc;
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
-    cs_config(cfg, at, 64, csize, smem, nullptr);
+    cs_config(cfg, at, 64, csize, cs_nt(K) + 32, smem, nullptr);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, csweep_kernel<K, UPPER>, &cfg) != cudaSuccess) {
         cudaGetLastError();
@@ -533,14 +563,18 @@ extern "C" int ddilu_csweep_set_debug(long long *buf) {
 }
 #endif
 
+/* k = operand slots per row (3, 4: short rows; 20: long rows) selects the shape of the kernel */
 /* compute threads of a CTA of the cluster sweep = rows of a step at most */
-extern "C" int ddilu_csweep_threads(void) { return CS_NT; }
+extern "C" int ddilu_csweep_threads(int k) { return cs_nt(k); }
 
 /* doubles of a CTA's window (own and halo values): no row may read further back (device.build_csweep checks) */
-extern "C" int ddilu_csweep_window(void) { return CS_WINDOW; }
+extern "C" int ddilu_csweep_window(int k) { return cs_win(k); }
 
 /* CTAs other than its own that may need a row's result */
-extern "C" int ddilu_csweep_max_push(void) { return CS_NP; }
+extern "C" int ddilu_csweep_max_push(int k) { return cs_np(k); }
+
+/* a push target is slot << rank_bits | rank: clusters of at most 1 << rank_bits CTAs */
+extern "C" int ddilu_csweep_rank_bits(int k) { return cs_rb(k); }
 
 /* 32-bit words per row holding its k dependency slots and its push targets */
 extern "C" int ddilu_csweep_code_words(int k) { return cs_words(k); }
@@ -555,6 +589,7 @@ extern "C" int ddilu_csweep_active_clusters(int cluster_size, int k, int depth, 
     int n = 0, rc = DDILU_ERR_ARG;
     if (k == 3) rc = cs_active<3, true>(cluster_size, cs_smem_bytes(3, true, depth, max_steps), &n);
     if (k == 4) rc = cs_active<4, true>(cluster_size, cs_smem_bytes(4, true, depth, max_steps), &n);
+    if (k == 20) rc = cs_active<20, true>(cluster_size, cs_smem_bytes(20, true, depth, max_steps), &n);
     return rc == DDILU_OK ? n : 0;
 }
 
@@ -562,14 +597,16 @@ extern "C" int ddilu_csweep_fill(int n, const int *row_ptr, const int *col_idx, 
                                  const int *gpos, const int *dep_slot, long long np, double *coef, unsigned *code,
                                  int *rowid, double *piv, int *bad_row, void *stream) {
     if (n <= 0) return DDILU_OK;
-    if (k != 3 && k != 4) return DDILU_ERR_ARG;
+    if (k != 3 && k != 4 && k != 20) return DDILU_ERR_ARG;
     const int threads = 256, grid = div_up(n, threads);
     if (upper)
-        csweep_fill_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, np,
-                                                                   coef, (unsigned short *)code, rowid, piv, bad_row);
+        csweep_fill_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot,
+                                                                   cs_win(k), np, coef, (unsigned short *)code, rowid,
+                                                                   piv, bad_row);
     else
-        csweep_fill_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot, np,
-                                                                    coef, (unsigned short *)code, rowid, piv, bad_row);
+        csweep_fill_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, gpos, dep_slot,
+                                                                    cs_win(k), np, coef, (unsigned short *)code, rowid,
+                                                                    piv, bad_row);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }
@@ -584,5 +621,9 @@ extern "C" int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *cta
     CSweepArgs a{ctas, steps, coef, code, rowid, piv, b, out, np, max_steps, depth, g_csweep_dbg};
     if (k == 3) return upper ? cs_launch<3, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<3, false>(n_blocks, cluster_size, a, ST(stream));
     if (k == 4) return upper ? cs_launch<4, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<4, false>(n_blocks, cluster_size, a, ST(stream));
+    if (k == 20) {
+        if (cluster_size > (1 << cs_rb(20))) return DDILU_ERR_ARG;
+        return upper ? cs_launch<20, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<20, false>(n_blocks, cluster_size, a, ST(stream));
+    }
     return DDILU_ERR_ARG;
 }

@@ -807,6 +807,7 @@ CSWEEP_NSET = int(os.environ.get("DDILU_CSWEEP_DEPTH", "4"))         # stages of
 CSWEEP_MIN_CHUNK = int(os.environ.get("DDILU_CSWEEP_MIN_CHUNK", "32"))   # rows of a level a CTA takes at least (narrow levels stay on few CTAs)
 CSWEEP_MIN_AVG_WIDTH = 2000    # average rows per level of a block from which a cluster pays (measured: 128^3 / p = 8, 1 340 rows per level, is a tie with the tiled kernel; 192^3, 3 000 rows, 1.3x faster)
 CSWEEP_MIN_SMS = 60            # blocks x cluster size: SMs the launch must fill to have the bandwidth of the GPU
+CSWEEP_LONG_ROWS = os.environ.get("DDILU_CSWEEP_LONG", "1") == "1"    # 20-slot instance for 27-point / ILUT factors
 _csweep_active = {}
 
 
@@ -858,23 +859,26 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
     d = dev()
     i64 = torch.int64
     debug = bool(os.environ.get("DDILU_DEBUG_SWEEP"))
-    if n / (nb * max(nlev_l, nlev_u)) < CSWEEP_MIN_AVG_WIDTH:
-        return None
     kl = int((lower.rp[1:] - lower.rp[:-1]).max().item())
     ku = int((upper.rp[1:] - upper.rp[:-1]).max().item()) - 1
     kmax = max(kl, ku, 1)
-    k = next((c for c in (3, 4) if kmax <= c), None)
+    k = next((c for c in ((3, 4, 20) if CSWEEP_LONG_ROWS else (3, 4)) if kmax <= c), None)
     if k is None:
         return None
-    W = query("ddilu_csweep_window")
+    # short rows (7-point ILU(0)): the tiled kernel is the better one for narrow levels; long rows (27-point / ILUT):
+    # the alternative is the sync-free warp-per-row solve at ~1.3 us per level, a cluster wins at any width
+    if k <= 4 and n / (nb * max(nlev_l, nlev_u)) < CSWEEP_MIN_AVG_WIDTH:
+        return None
+    W = query("ddilu_csweep_window", k)
     nset = CSWEEP_NSET
     lev_cap = 2 * max(nlev_l, nlev_u)           # steps of a CTA: its levels, the wide ones in several pieces
     if query("ddilu_csweep_smem_bytes", k, 1, 2, lev_cap) > 227 * 1024:
         return None
-    csize = next((c for c in range(min(16, CSWEEP_CLUSTER), 0, -1) if csweep_active_clusters(c, k, 2, lev_cap) >= nb), 0)
+    cmax = min(16, CSWEEP_CLUSTER, 1 << query("ddilu_csweep_rank_bits", k))
+    csize = next((c for c in range(cmax, 0, -1) if csweep_active_clusters(c, k, 2, lev_cap) >= nb), 0)
     if debug:
         print(f"cluster sweep: {nb} blocks -> clusters of {csize}", flush=True)
-    if not csize or nb * csize < CSWEEP_MIN_SMS:
+    if not csize or (k <= 4 and nb * csize < CSWEEP_MIN_SMS):
         return None
     seg = torch.tensor([int(v) for v in seg_ptr], dtype=i64, device=d)
     if int(seg[-1].item()) != n or int(seg[0].item()) != 0:
@@ -945,7 +949,8 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         need = torch.where(dep, wend.reshape(-1)[cta_r * nlev + lv[erow]] - e_wpos, torch.zeros_like(ecol))
         max_need = int(need.max().item()) if nnz else 1
         # push targets of every row: the other CTAs that hold its value, (slot << 4 | rank)
-        NP = query("ddilu_csweep_max_push")
+        NP = query("ddilu_csweep_max_push", k)
+        RB = query("ddilu_csweep_rank_bits", k)
         porder = torch.argsort(h_row, stable=True)
         prow = h_row[porder]
         pidx = torch.arange(prow.numel(), dtype=i64, device=d) - torch.searchsorted(prow, prow)
@@ -965,7 +970,7 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         consecutive = (nclf == 0) | (row_hi - row_lo + 1 == nclf)
         contiguous = bool(consecutive.all().item())
         row0 = torch.where((nclf > 0) & consecutive, row_lo, torch.full_like(row_lo, -1))
-        NT = query("ddilu_csweep_threads")
+        NT = query("ddilu_csweep_threads", k)
         # steps: a CTA's chunk of a level, cut into pieces of at most one row per thread; the first piece waits for
         # the previous level, the last one signals
         nsub = torch.clamp((nclf + NT - 1) // NT, min=1)
@@ -1014,7 +1019,7 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         coef = torch.zeros(k * npos, dtype=F64, device=d)
         code = torch.full((NWD * npos * 2,), -1, dtype=torch.int16, device=d)      # halves; 0xffff: no push target
         if prow.numel():
-            pcode = ((h_wpos[porder] % W) << 4) | (h_cta[porder] % csize)
+            pcode = ((h_wpos[porder] % W) << RB) | (h_cta[porder] % csize)
             half = k + pidx                                                          # half index of the push target
             code[2 * ((half // 2) * npos + gpos[prow]) + half % 2] = pcode.to(torch.int32).to(torch.int16)
         rowid = torch.zeros(npos, dtype=I32, device=d)

@@ -88,6 +88,34 @@ def test_cluster_sweep_bit_exact(P, orc, dims, p, pc, cluster, nset, min_chunk):
         assert np.array_equal(xlu.cpu().numpy(), ref_lu), ("LU", rep)
 
 
+@pytest.mark.parametrize("dims,p,cluster", [((14, 13, 12), 4, 8), ((20, 20, 20), 8, 4), ((16, 16, 16), 1, 8)])
+def test_cluster_sweep_long_rows_27_point(P, orc, dims, p, cluster):
+    """The 20-slot instance (27-point stencil, ILUT(1e-3, 20) interior factors: up to 19 dependencies per row, deep
+    narrow levels, an 8 191-double window, up to four push targets, the step table read from global memory): L, U
+    and U^-1 L^-1 against the oracle."""
+    import torch
+    with _Knobs(cluster, 3, 8) as D:
+        a = P.convdiff27(*dims)
+        layout = P.classify_and_order(a, P.partition(a, p, dims), p)
+        m = P.make_preconditioner("schur", a, layout, P.FillRule.parse("ilut:0.001,20"))
+    f = m._p.interior
+    cp = f._cs
+    assert cp is not None and cp.k == 20 and cp.csize <= 8, "27-point interior factors did not get the long-row plan"
+    rng = np.random.default_rng(29)
+    for rep in range(2):
+        b = rng.standard_normal(f.n)
+        bd = D.to_device_f64(b)
+        ref_l, ref_u, ref_lu = _oracle_solves(P, orc, f, b)
+        xl, xu, xlu = D.empty_f64(f.n), D.empty_f64(f.n), D.empty_f64(f.n)
+        f.lower_solve(bd, xl)
+        f.upper_solve(bd, xu)
+        f.solve(bd, xlu)
+        torch.cuda.synchronize()
+        assert np.array_equal(xl.cpu().numpy(), ref_l), ("L", rep)
+        assert np.array_equal(xu.cpu().numpy(), ref_u), ("U", rep)
+        assert np.array_equal(xlu.cpu().numpy(), ref_lu), ("LU", rep)
+
+
 def test_cluster_sweep_levels_wider_than_the_cta(P, orc):
     """A 48^3 block on ONE CTA: the widest levels have more than twice as many rows as the CTA has threads (they
     are cut into three steps; only the first waits, only the last signals)."""
@@ -97,7 +125,7 @@ def test_cluster_sweep_levels_wider_than_the_cta(P, orc):
         a = P.aniso3d(*dims)
         layout = P.classify_and_order(a, P.partition(a, 1, dims), 1)
         m = P.make_preconditioner("schur", a, layout)
-        threads = D.query("ddilu_csweep_threads")
+        threads = D.query("ddilu_csweep_threads", 3)
     f = m._p.interior
     assert f._cs is not None and f._cs.csize == 1
     widest = int(np.bincount(f._lev(False)[0][: f.n].cpu().numpy()).max())
@@ -114,14 +142,16 @@ def test_cluster_sweep_levels_wider_than_the_cta(P, orc):
 
 
 def test_cluster_sweep_refuses_unsuitable_factors(P):
-    """No plan for: rows with more than 4 dependencies (27-point), dependencies further back than the window (one
-    CTA for a 64^3 block), problems below the production thresholds; the factors then solve through the tiled /
+    """No plan for: rows with more than 20 dependencies (27-point ILU(1)), dependencies further back than the window
+    (one CTA for a 64^3 block), problems below the production thresholds; the factors then solve through the tiled /
     sync-free kernels."""
     with _Knobs(16, 3, 32) as D:
-        a27 = P.convdiff27(16, 16, 16)
-        lay = P.classify_and_order(a27, P.partition(a27, 8, (16, 16, 16)), 8)
-        m = P.make_preconditioner("schur", a27, lay)
-        assert m._p.interior._cs is None
+        a27 = P.convdiff27(12, 12, 12)
+        lay = P.classify_and_order(a27, P.partition(a27, 8, (12, 12, 12)), 8)
+        m = P.make_preconditioner("schur", a27, lay, P.FillRule.parse("iluk:1"))
+        f27 = m._p.interior
+        assert int((f27.upper.rp[1:] - f27.upper.rp[:-1]).max().item()) - 1 > 20
+        assert f27._cs is None
     with _Knobs(1, 3, 32) as D:
         a = P.aniso3d(64, 64, 64)
         lay = P.classify_and_order(a, P.partition(a, 1, (64, 64, 64)), 1)
