@@ -193,9 +193,18 @@ int ddilu_csweep_active_clusters(int cluster_size, int k, int depth, int max_ste
 int ddilu_csweep_fill(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
                       const int *gpos, const int *dep_slot, long long np, double *coef, unsigned *code, int *rowid,
                       double *piv, int *bad_row, void *stream);
+/* long rows (k = 20): the operands lie STEP BY STEP in one blob -- per step a block coef[k][r4] | piv[2][r4] (upper) |
+ * words[code_words][r4] | row ids[r4] with r4 = rows of the step rounded up to 4, so that the feeder moves a step
+ * with one bulk copy; steps[..][6] = byte offset of the block / 16.  ddilu_csweep_fill_long writes a row's operands
+ * (blk_base / r4 / off: byte offset of its step's block, r4 of that step, its entry), push targets start as 0xffff. */
+int ddilu_csweep_long_record_bytes(int k, int upper);
+int ddilu_csweep_fill_long(int n, const int *row_ptr, const int *col_idx, const double *values, int upper, int k,
+                           const long long *blk_base, const int *r4, const int *off, const int *dep_slot,
+                           unsigned char *blob, int *bad_row, void *stream);
 int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps, const double *coef,
-                       const unsigned *code, const int *rowid, const double *piv, long long np, int k, int upper,
-                       int max_steps, int depth, const double *b, double *out, void *stream);
+                       const unsigned *code, const int *rowid, const double *piv, const unsigned char *blob,
+                       long long np, int k, int upper, int max_steps, int depth, const double *b, double *out,
+                       void *stream);
 
 /* ---- peer-memory exchanges (csrc/peer.cu) for the multi-GPU path, SURVEY.md 8e / PAPER.md:701-705: the halo of
  * interface values and the sum of dot / norm scalars without a collective library call.  Every rank owns a mailbox

@@ -65,7 +65,9 @@ SIGNATURES = {
     "ddilu_csweep_smem_bytes": (_L, [_I, _I, _I, _I]),
     "ddilu_csweep_active_clusters": (_I, [_I, _I, _I, _I]),
     "ddilu_csweep_fill": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _L, _P, _P, _P, _P, _P, _P]),
-    "ddilu_csweep_solve": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P]),
+    "ddilu_csweep_long_record_bytes": (_I, [_I, _I]),
+    "ddilu_csweep_fill_long": (_I, [_I, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ddilu_csweep_solve": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P]),
     "ddilu_peer_allreduce": (_I, [_I, _I, _P, _P, _P, _P, _I, _I, _L, _L, _P, _P]),
     "ddilu_peer_send": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _L, _L, _P, _P, _P]),
     "ddilu_peer_recv": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P]),

@@ -77,6 +77,9 @@ struct CSweepArgs {
                                       // push targets slot << rank bits | rank (0xffff = none)
     const int *rowid;                 // [np]
     const double *piv;                // [2][np]: pivot, reciprocal (upper)
+    const unsigned char *blob;        // long rows instead of the four arrays: the operands STEP BY STEP, one contiguous block
+                                      // per step (r4 = rows rounded up to 4): coef[K][r4] | piv[2][r4] (upper) |
+                                      // words[NW][r4] | row ids[r4] -- one bulk copy per step
     const double *b;                  // right-hand side by row
     double *out;                      // results by row
     long long np;
@@ -211,8 +214,12 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
     constexpr int CS_THREADS = NT + 32;
     constexpr uint32_t RMASK = (1u << RB) - 1u;
     constexpr int STAGE = cs_stage_bytes(K, UPPER);
-    constexpr int OFF_PIV = 8 * K * NT, OFF_RHS = OFF_PIV + (UPPER ? 16 * NT : 0), OFF_W = OFF_RHS + 8 * (NT + 2),
-                  OFF_ID = OFF_W + 4 * NW * NT;
+    // short rows: coef[K][NT] | piv[2][NT] (upper) | rhs[NT + 2] | words[NW][NT] | row ids[NT]
+    // long rows:  rhs[NT + 2] (unused: b[row id] is loaded directly) | the step's operand block as it lies in the blob
+    constexpr int OFF_PIV = 8 * K * NT, OFF_RHS = Cfg::LONG ? 0 : OFF_PIV + (UPPER ? 16 * NT : 0),
+                  OFF_W = OFF_PIV + (UPPER ? 16 * NT : 0) + 8 * (NT + 2), OFF_ID = OFF_W + 4 * NW * NT;
+    constexpr int OFF_BLK = 8 * (NT + 2);                                  // long rows
+    constexpr int REC = 8 * K + (UPPER ? 16 : 0) + 4 * NW + 4;            // operand bytes of a row
     extern __shared__ __align__(128) unsigned char cs_smem[];
     const int *cta = a.ctas + CS_CTA_INTS * blockIdx.x;
     uint32_t csize;
@@ -264,14 +271,25 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
             const double *pv = a.piv + base;
             const int4 none = make_int4(0, 0, 0, 0);
             int4 sv = nsteps > 0 ? entry(0, 0) : none;      // (long rows: the table is in global memory, an entry ahead)
+            int4 tfc = (Cfg::LONG && nsteps > 0) ? entry(0, 1) : none;
             int s = 0;
             uint32_t round = 0;               // how often the ring has wrapped
             for (int i = 0; i < nsteps; ++i) {
                 const int4 sv1 = i + 1 < nsteps ? entry(i + 1, 0) : none;
+                const int4 tf1 = (Cfg::LONG && i + 1 < nsteps) ? entry(i + 1, 1) : none;
                 const int rows = sv.y - sv.x;
                 const uint32_t st = ring_u32 + (uint32_t)(s * STAGE), full = full_u32 + 8u * (uint32_t)s;
                 if (round) cs_mbar_wait(empty_u32 + 8u * (uint32_t)s, (round - 1) & 1u);
-                if (rows > 0) {
+                if (rows > 0 && Cfg::LONG) {
+                    // long rows: the whole operand block of the step with one bulk copy (35 copies of ~1 KB each, one
+                    // per array, made the feeder the bottleneck of the deep narrow levels); b[row id] is loaded by
+                    // the compute threads (chunks of 27-point blocks are not row ranges)
+                    const uint32_t r4 = (uint32_t)(rows + 3) & ~3u;
+                    const uint32_t bytes = r4 * (uint32_t)REC;
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full) : "memory");
+                    cs_mbar_arrive_tx(full, bytes);
+                    cs_bulk_g2s(st + OFF_BLK, a.blob + 16ull * (unsigned long long)(unsigned)tfc.z, bytes, full);
+                } else if (rows > 0) {
                     const uint32_t r4 = (uint32_t)(rows + 3) & ~3u;                 // whole 16-byte pieces of every array
                     uint32_t tx = r4 * (uint32_t)(8 * K + 4 * NW + (UPPER ? 16 : 0));
                     uint32_t nb_bulk = 0;
@@ -313,6 +331,7 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
                     cs_mbar_arrive(full);
                 }
                 sv = sv1;
+                tfc = tf1;
                 if (++s == D) {
                     s = 0;
                     ++round;
@@ -369,7 +388,24 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
             double c[K], rhs = 0.0, d = 1.0, r = 0.0;
             uint32_t w[NW], ad[K];
             int id = 0;
-            if (have) {
+            if (have && Cfg::LONG) {
+                const uint32_t r4 = (uint32_t)(sv.y - sv.x + 3) & ~3u;       // the block's arrays have r4 entries each
+                const uint32_t blk = ring_u32 + so + OFF_BLK;
+                uint32_t p8 = blk + 8u * (uint32_t)tid;
+#pragma unroll
+                for (int k = 0; k < K; ++k, p8 += 8u * r4) c[k] = cs_lds(p8);
+                if (UPPER) {
+                    d = cs_lds(p8);
+                    r = cs_lds(p8 + 8u * r4);
+                }
+                uint32_t p4 = blk + (uint32_t)(8 * K + (UPPER ? 16 : 0)) * r4 + 4u * (uint32_t)tid;
+#pragma unroll
+                for (int k = 0; k < NW; ++k, p4 += 4u * r4) w[k] = cs_lds_u32_at<0>(p4);
+                id = (int)cs_lds_u32_at<0>(p4);
+                rhs = __ldg(a.b + id);
+#pragma unroll
+                for (int k = 0; k < K; ++k) ad[k] = xs_u32 + 8u * cs_half(w, k);
+            } else if (have) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) c[k] = cs_lds(my8 + so + (uint32_t)(8 * k * NT));
 #pragma unroll
@@ -482,6 +518,51 @@ __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int 
     if (UPPER) {
         piv[g] = diag;
         piv[np + g] = safe_reciprocal(diag);
+        if (!seen || fabs(diag) < 1e-300) atomicMin(bad_row, row);
+    }
+}
+
+// long rows: the record of a row inside the operand block of its step (block at byte blk_base[row], arrays of r4[row]
+// entries, the row at entry off[row])
+template <bool UPPER>
+__global__ void csweep_fill_long_kernel(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                                        const double *__restrict__ val, int K, int NW, int NP,
+                                        const long long *__restrict__ blk_base, const int *__restrict__ r4s,
+                                        const int *__restrict__ offs, const int *__restrict__ dep_slot, int window,
+                                        unsigned char *blob, int *bad_row) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    const long long r4 = r4s[row], off = offs[row];
+    unsigned char *blk = blob + blk_base[row];
+    double *cf = (double *)blk;
+    double *pv = cf + (long long)K * r4;
+    unsigned short *hv = (unsigned short *)(blk + (8LL * K + (UPPER ? 16 : 0)) * r4);
+    int *ids = (int *)(blk + (8LL * K + (UPPER ? 16 : 0) + 4LL * NW) * r4);
+    int kk = 0;
+    double diag = 1.0;
+    bool seen = false;
+    for (int k = rp[row], ke = rp[row + 1]; k < ke; ++k) {
+        const int j = ci[k];
+        if (UPPER ? j > row : j < row) {
+            if (kk < K) {
+                cf[kk * r4 + off] = val[k];
+                hv[2 * ((kk >> 1) * r4 + off) + (kk & 1)] = (unsigned short)dep_slot[k];
+            }
+            ++kk;
+        } else if (j == row) {
+            diag = val[k];
+            seen = true;
+        }
+    }
+    for (; kk < K; ++kk) {       // padding: coefficient 0 times the zero slot
+        cf[kk * r4 + off] = 0.0;
+        hv[2 * ((kk >> 1) * r4 + off) + (kk & 1)] = (unsigned short)window;
+    }
+    for (int q = K; q < K + NP; ++q) hv[2 * ((q >> 1) * r4 + off) + (q & 1)] = (unsigned short)0xffff;    // no push target (yet)
+    ids[off] = row;
+    if (UPPER) {
+        pv[off] = diag;
+        pv[r4 + off] = safe_reciprocal(diag);
         if (!seen || fabs(diag) < 1e-300) atomicMin(bad_row, row);
     }
 }
@@ -611,14 +692,36 @@ extern "C" int ddilu_csweep_fill(int n, const int *row_ptr, const int *col_idx, 
     return DDILU_OK;
 }
 
+/* long rows (k = 20): a row's operands inside the block of its step */
+extern "C" int ddilu_csweep_fill_long(int n, const int *row_ptr, const int *col_idx, const double *values, int upper,
+                                      int k, const long long *blk_base, const int *r4, const int *off,
+                                      const int *dep_slot, unsigned char *blob, int *bad_row, void *stream) {
+    if (n <= 0) return DDILU_OK;
+    if (!cs_long(k) || k != 20) return DDILU_ERR_ARG;
+    const int threads = 256, grid = div_up(n, threads);
+    if (upper)
+        csweep_fill_long_kernel<true><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, cs_words(k), cs_np(k),
+                                                                        blk_base, r4, off, dep_slot, cs_win(k), blob, bad_row);
+    else
+        csweep_fill_long_kernel<false><<<grid, threads, 0, ST(stream)>>>(n, row_ptr, col_idx, values, k, cs_words(k), cs_np(k),
+                                                                         blk_base, r4, off, dep_slot, cs_win(k), blob, bad_row);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* bytes of a row's operands in a long-row block */
+extern "C" int ddilu_csweep_long_record_bytes(int k, int upper) { return 8 * k + (upper ? 16 : 0) + 4 * cs_words(k) + 4; }
+
 /* out[row] = (L^-1 b)[row] (upper 0, unit diagonal) or (U^-1 b)[row] (upper 1) for a block-diagonal factor laid out
  * by ddilu_csweep_fill: n_blocks clusters of cluster_size CTAs */
 extern "C" int ddilu_csweep_solve(int n_blocks, int cluster_size, const int *ctas, const int *steps, const double *coef,
-                                  const unsigned *code, const int *rowid, const double *piv, long long np, int k,
-                                  int upper, int max_steps, int depth, const double *b, double *out, void *stream) {
+                                  const unsigned *code, const int *rowid, const double *piv,
+                                  const unsigned char *blob, long long np, int k, int upper, int max_steps, int depth,
+                                  const double *b, double *out, void *stream) {
     if (n_blocks <= 0) return DDILU_OK;
-    if (cluster_size < 1 || cluster_size > 16 || (upper && !piv) || depth < 2 || depth > CS_MAX_DEPTH) return DDILU_ERR_ARG;
-    CSweepArgs a{ctas, steps, coef, code, rowid, piv, b, out, np, max_steps, depth, g_csweep_dbg};
+    if (cluster_size < 1 || cluster_size > 16 || depth < 2 || depth > CS_MAX_DEPTH) return DDILU_ERR_ARG;
+    if (cs_long(k) ? !blob : (!coef || !code || !rowid || (upper && !piv))) return DDILU_ERR_ARG;
+    CSweepArgs a{ctas, steps, coef, code, rowid, piv, blob, b, out, np, max_steps, depth, g_csweep_dbg};
     if (k == 3) return upper ? cs_launch<3, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<3, false>(n_blocks, cluster_size, a, ST(stream));
     if (k == 4) return upper ? cs_launch<4, true>(n_blocks, cluster_size, a, ST(stream)) : cs_launch<4, false>(n_blocks, cluster_size, a, ST(stream));
     if (k == 20) {

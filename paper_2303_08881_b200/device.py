@@ -828,6 +828,7 @@ class ClusterSweepHalf:
     code: torch.Tensor         # 16-bit halves of the packed words: dependency slots, push targets
     rowid: torch.Tensor
     piv: torch.Tensor | None
+    blob: torch.Tensor | None  # long rows: the operands step by step in one buffer (instead of coef / code / rowid / piv)
     np: int
     max_steps: int
     depth: int                 # stages of the operand ring
@@ -1015,19 +1016,39 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
         ctas[:, 0], ctas[:, 1] = base, sigmask | (signallers << 16)
         ctas[:, 2] = torch.cumsum(steps_cta, 0) - steps_cta
         ctas[:, 3] = steps_cta
-        NWD = query("ddilu_csweep_code_words", k)
-        coef = torch.zeros(k * npos, dtype=F64, device=d)
-        code = torch.full((NWD * npos * 2,), -1, dtype=torch.int16, device=d)      # halves; 0xffff: no push target
-        if prow.numel():
-            pcode = ((h_wpos[porder] % W) << RB) | (h_cta[porder] % csize)
-            half = k + pidx                                                          # half index of the push target
-            code[2 * ((half // 2) * npos + gpos[prow]) + half % 2] = pcode.to(torch.int32).to(torch.int16)
-        rowid = torch.zeros(npos, dtype=I32, device=d)
-        piv = torch.ones(2 * npos, dtype=F64, device=d) if up else None
-        call("ddilu_csweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos.to(I32).contiguous(),
-             (e_wpos % W).to(I32).contiguous(), npos, coef, code, rowid, piv, bad)
+        pcode = (((h_wpos[porder] % W) << RB) | (h_cta[porder] % csize)).to(torch.int32).to(torch.int16) \
+            if prow.numel() else None
+        half = k + pidx                                                              # half index of a push target
+        if k > 4:
+            # long rows: the operands step by step in one blob (one bulk copy per step in the kernel)
+            REC = query("ddilu_csweep_long_record_bytes", k, int(up))
+            r4s = (s_end - s_start + 3) // 4 * 4
+            bbytes = r4s * REC
+            boff = torch.cumsum(bbytes, 0) - bbytes
+            steps[:, 6] = boff // 16
+            st_row = first[ckey] + ro // NT                                          # step of every row
+            off = ro % NT
+            blob = torch.zeros(max(16, int(bbytes.sum().item())), dtype=torch.uint8, device=d)
+            call("ddilu_csweep_fill_long", n, fac.rp, fac.ci, fac.val, int(up), k, boff[st_row].contiguous(),
+                 r4s[st_row].to(I32).contiguous(), off.to(I32).contiguous(), (e_wpos % W).to(I32).contiguous(), blob, bad)
+            if pcode is not None:
+                pr4, pst = r4s[st_row[prow]], st_row[prow]
+                at = boff[pst] + (8 * k + (16 if up else 0)) * pr4 + 4 * ((half // 2) * pr4 + off[prow]) + 2 * (half % 2)
+                blob.view(torch.int16)[at // 2] = pcode
+            coef = code = rowid = piv = None
+        else:
+            blob = None
+            NWD = query("ddilu_csweep_code_words", k)
+            coef = torch.zeros(k * npos, dtype=F64, device=d)
+            code = torch.full((NWD * npos * 2,), -1, dtype=torch.int16, device=d)      # halves; 0xffff: no push target
+            if pcode is not None:
+                code[2 * ((half // 2) * npos + gpos[prow]) + half % 2] = pcode
+            rowid = torch.zeros(npos, dtype=I32, device=d)
+            piv = torch.ones(2 * npos, dtype=F64, device=d) if up else None
+            call("ddilu_csweep_fill", n, fac.rp, fac.ci, fac.val, int(up), k, gpos.to(I32).contiguous(),
+                 (e_wpos % W).to(I32).contiguous(), npos, coef, code, rowid, piv, bad)
         halves.append(ClusterSweepHalf(ctas.to(I32).contiguous().view(-1), steps.to(I32).contiguous().view(-1),
-                                       coef, code, rowid, piv, npos, max_steps, depth, contiguous))
+                                       coef, code, rowid, piv, blob, npos, max_steps, depth, contiguous))
     return ClusterSweepPlan(n, nb, csize, k, nset, halves[0], halves[1], int(bad.item()))
 
 
@@ -1036,7 +1057,7 @@ def csweep_solve(cp: ClusterSweepPlan, upper: bool, b: torch.Tensor, out: torch.
     if check and upper and cp.bad_row != INT_MAX:
         raise TriSolveError(f"zero or missing diagonal at row {cp.bad_row}")
     h = cp.upper if upper else cp.lower
-    call("ddilu_csweep_solve", cp.n_blocks, cp.csize, h.ctas, h.steps, h.coef, h.code, h.rowid, h.piv, h.np, cp.k,
+    call("ddilu_csweep_solve", cp.n_blocks, cp.csize, h.ctas, h.steps, h.coef, h.code, h.rowid, h.piv, h.blob, h.np, cp.k,
          int(upper), h.max_steps, h.depth, b, out)
     return out
 

@@ -56,6 +56,20 @@ if "csweep" in which:
         f.solve(r, x)
         torch.cuda.synchronize()
         print("csweep", f.n, f._cs.csize, f._cs.lower.max_steps, f._cs.lower.depth, float(x.abs().max()))
+    # the 20-slot instance: 27-point ILUT interior factors (step table in global memory, operands as one block per step)
+    D.CSWEEP_CLUSTER = 8
+    d27 = (14, 13, 12)
+    a27 = P.convdiff27(*d27)
+    lay27 = P.classify_and_order(a27, P.partition(a27, 4, d27), 4)
+    m = P.make_preconditioner("schur", a27, lay27, P.FillRule.parse("ilut:0.001,20"))
+    f = m._p.interior
+    assert f._cs is not None and f._cs.k == 20
+    r = torch.randn(f.n, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(r)
+    f.lower_solve(r, x)
+    f.upper_solve(r, x)
+    torch.cuda.synchronize()
+    print("csweep long rows", f.n, f._cs.csize, f._cs.lower.max_steps, float(x.abs().max()))
     D.CSWEEP_MIN_AVG_WIDTH, D.CSWEEP_MIN_SMS, D.CSWEEP_CLUSTER = old
 
 if "sweep" in which:
