@@ -178,7 +178,7 @@ int ddilu_sweep_solve(int n_blocks, const int *blocks, const int *levtab, const 
  * gpos = position of the row in the operand arrays, dep_slot = per stored entry the window slot of that dependency
  * in the READER's CTA; np = length of the position space; coef[k][np]; code[code_words(k)][np]: the 16-bit halves
  * of a row's words are its k dependency slots (filled here) and then its max_push(k) push targets
- * slot << rank_bits(k) | rank, 0xffff = none (filled by the caller); rowid[np]; piv[2][np] = pivot and its reciprocal (upper only)).
+ * slot << rank_bits(k) | rank, 0xffff = none (filled by the caller); rowid[np]; piv[np][2] = (pivot, reciprocal) pairs (upper only)).
  * ddilu_csweep_solve: ctas = 4 ints per CTA {first position, rows, first step, steps}; steps = 8 ints per step
  * {start (a multiple of 4), end (positions, at most `threads` rows), window slot of the first row, first row when
  * the rows are consecutive else -1 (rowid is read), halo bytes arriving for the level (first step of a level),

@@ -76,7 +76,7 @@ struct CSweepArgs {
     const unsigned *code;             // [cs_words(K)][np]: 16-bit halves = K window slots of the dependencies, then the
                                       // push targets slot << rank bits | rank (0xffff = none)
     const int *rowid;                 // [np]
-    const double *piv;                // [2][np]: pivot, reciprocal (upper)
+    const double *piv;                // [np][2]: pivot, reciprocal (upper)
     const unsigned char *blob;        // long rows instead of the four arrays: the operands STEP BY STEP, one contiguous block
                                       // per step (r4 = rows rounded up to 4): coef[K][r4] | piv[2][r4] (upper) |
                                       // words[NW][r4] | row ids[r4] -- one bulk copy per step
@@ -128,6 +128,11 @@ template <int OFF>
 __device__ __forceinline__ uint32_t cs_lds_u32_at(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 cs_lds_f64x2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ void cs_sts(uint32_t a, double v) {
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
     constexpr int CS_THREADS = NT + 32;
     constexpr uint32_t RMASK = (1u << RB) - 1u;
     constexpr int STAGE = cs_stage_bytes(K, UPPER);
-    // short rows: coef[K][NT] | piv[2][NT] (upper) | rhs[NT + 2] | words[NW][NT] | row ids[NT]
+    // short rows: coef[K][NT] | piv[NT][2] (upper) | rhs[NT + 2] | words[NW][NT] | row ids[NT]
     // long rows:  rhs[NT + 2] (unused: b[row id] is loaded directly) | the step's operand block as it lies in the blob
     constexpr int OFF_PIV = 8 * K * NT, OFF_RHS = Cfg::LONG ? 0 : OFF_PIV + (UPPER ? 16 * NT : 0),
                   OFF_W = OFF_PIV + (UPPER ? 16 * NT : 0) + 8 * (NT + 2), OFF_ID = OFF_W + 4 * NW * NT;
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
             const double *cf = a.coef + base;
             const unsigned *cd = a.code + base;
             const int *ids = a.rowid + base;
-            const double *pv = a.piv + base;
+            const double *pv = a.piv + 2 * base;
             const int4 none = make_int4(0, 0, 0, 0);
             int4 sv = nsteps > 0 ? entry(0, 0) : none;      // (long rows: the table is in global memory, an entry ahead)
             int4 tfc = (Cfg::LONG && nsteps > 0) ? entry(0, 1) : none;
@@ -317,10 +322,7 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
                     for (int k = 0; k < K; ++k) cs_bulk_g2s(st + (uint32_t)(8 * k * NT), cf + (long long)k * np + sv.x, 8u * r4, full);
 #pragma unroll
                     for (int k = 0; k < NW; ++k) cs_bulk_g2s(st + OFF_W + (uint32_t)(4 * k * NT), cd + (long long)k * np + sv.x, 4u * r4, full);
-                    if (UPPER) {
-                        cs_bulk_g2s(st + OFF_PIV, pv + sv.x, 8u * r4, full);
-                        cs_bulk_g2s(st + OFF_PIV + 8u * NT, pv + np + sv.x, 8u * r4, full);
-                    }
+                    if (UPPER) cs_bulk_g2s(st + OFF_PIV, pv + 2 * (long long)sv.x, 16u * r4, full);      // (pivot, reciprocal) pairs
                     if (sv.w >= 0) {
                         if (nb_bulk) cs_bulk_g2s(bdst, bsrc, nb_bulk, full);
                     } else {
@@ -411,8 +413,9 @@ __global__ void __launch_bounds__(CsCfg<K>::NT + 32, 1) csweep_kernel(const CSwe
 #pragma unroll
                 for (int k = 0; k < NW; ++k) w[k] = cs_lds_u32_at<OFF_W>(my4 + so + (uint32_t)(4 * k * NT));
                 if (UPPER) {
-                    d = cs_lds_at<OFF_PIV>(my8 + so);
-                    r = cs_lds_at<OFF_PIV + 8 * NT>(my8 + so);
+                    const double2 dr = cs_lds_f64x2(ring_u32 + so + OFF_PIV + 16u * (uint32_t)tid);
+                    d = dr.x;
+                    r = dr.y;
                 }
                 if (sv.w >= 0) {
                     id = sv.w + tid;
@@ -516,8 +519,8 @@ __global__ void csweep_fill_kernel(int n, const int *__restrict__ rp, const int 
     }
     rowid[g] = row;
     if (UPPER) {
-        piv[g] = diag;
-        piv[np + g] = safe_reciprocal(diag);
+        piv[2 * g] = diag;
+        piv[2 * g + 1] = safe_reciprocal(diag);
         if (!seen || fabs(diag) < 1e-300) atomicMin(bad_row, row);
     }
 }
