@@ -9,27 +9,30 @@
 // THREAD-BLOCK CLUSTER of up to 16 CTAs owns a block and walks its levels together:
 //
 //   * every level of the block is cut into contiguous chunks, chunk r belongs to CTA r of the cluster;
-//   * a CTA keeps every value IT needs in a window of W = 4095 doubles of its OWN shared memory: its own results
-//     and the results of other CTAs that its rows depend on (halo values), numbered level by level (own rows of
-//     the level, then the level's halo values), value p in xs[p mod W]; setup checks that no row reads further
-//     back than W positions behind the end of its own level.  A dependency is a 16-bit window slot, read with a
-//     plain shared-memory load; slot W holds 0.0 for padded operands;
-//   * a producer PUSHES a result to the (<= 3) other CTAs that need it: st.async through distributed shared memory
-//     into the consumer's window slot, completing bytes on the consumer's mbarrier -- data and signal travel
-//     together, no fence, no cluster-scope release (barrier.cluster.arrive.release costs a MEMBAR.ALL.GPU per
-//     level, ~700 cycles: measured, see DESIGN.md);
+//   * a CTA keeps every value IT needs in a window of W doubles (4 095; 8 191 for long rows) of its OWN shared memory:
+//     its own results and the results of other CTAs that its rows depend on (halo values), numbered level by level
+//     (own rows of the level, then the level's halo values), value p in xs[p mod W]; setup checks that no row reads
+//     further back than W positions behind the end of its own level.  A dependency is a 16-bit window slot, read
+//     with a plain shared-memory load; slot W holds 0.0 for padded operands;
+//   * a producer PUSHES a result to the (<= 3; long rows: 4) other CTAs that need it: st.async through distributed
+//     shared memory into the consumer's window slot, completing bytes on the consumer's mbarrier -- data and signal
+//     travel together, no fence, no cluster-scope release (barrier.cluster.arrive.release costs a MEMBAR.ALL.GPU per
+//     level, ~700 cycles: measured, see DESIGN.md 5.8);
 //   * ONE mbarrier wait per level: the phase of level l completes when all warps of the own CTA have stored their
 //     level-l rows, all halo bytes of level l have landed (expect_tx) and every warp of every CTA this one exchanges
-//     values with has finished level l (a token arrive -- the flow control that makes the window slots safe to overwrite;
-//     CTAs that exchange nothing are not coupled);
-//   * operands are one 48-byte record per row (4 coefficients, 8 halves: K slots and <= 3 push targets; + the pivot
-//     pair for U; the row id only when a level chunk is not a contiguous row range) in the CTA's schedule order and
-//     travel to thread-private shared-memory slots by cp.async, D - 1 steps ahead (coalesced); a step is at
-//     most one row per thread, chunks wider than the CTA are cut into several steps at setup; the results leave
-//     by row after the arrive.  Every thread computes: there are no helper warps and no flags.
+//     values with has finished level l (a token arrive -- the flow control that makes the window slots safe to
+//     overwrite; CTAs that exchange nothing are not coupled);
+//   * a STEP is (a part of) a CTA's chunk of a level, at most one row per compute thread; chunks wider than the CTA
+//     are cut into several steps at setup.  Operands are structure-of-arrays in the CTA's schedule order (K
+//     coefficients, K slots + push targets packed in 32-bit words, (pivot, reciprocal) pairs for U, the row id
+//     only when a chunk is not a range of consecutive rows); ONE lane of a 25th warp streams them into a ring of
+//     shared-memory stages with bulk copies (cp.async.bulk + complete_tx on full[stage]), the compute threads take
+//     them with plain loads and free the stage through empty[stage]; the results leave by row after the arrive.
+//     (Operands prefetched into registers stalled every consumer on the youngest load in flight -- six scoreboards
+//     per warp --, per-thread cp.async cost ~200 warp instructions per step: DESIGN.md 5.8.)
 //
-// Bytes moved per row: 48 (+ 16 pivot pair) (+ 4 row id) operands + 8 right-hand side + 8 result = 64 (L) / 80 (U),
-// against the algorithmic 12 nnz + 4 + 16 = 56 / 68 for three dependencies.
+// Bytes moved per row (three dependencies): 24 + 12 (+ 16 pivot pair) operands + 8 right-hand side + 8 result = 52 (L)
+// / 68 (U), against the algorithmic 12 nnz + 4 + 16 = 56 / 68.
 #include <stdint.h>
 
 #include <mutex>
