@@ -150,7 +150,11 @@ class PeerComm(Comm):
             if r != self.rank and t.device != self._dev:
                 if not torch.cuda.can_device_access_peer(self._dev.index, t.device.index):
                     raise RuntimeError(f"no peer access from {self._dev} to {t.device}")
-                probe.copy_(t[-1:])               # (the last word of a mailbox: halo data, zero at this point)
+                # torch switches peer access on for "source device may access destination device" on the first copy of
+                # a pair: the copy FROM this device INTO the peer's mailbox is the direction our kernels need (the
+                # last word of a mailbox is halo data, unused at this point: read it, write the same value back)
+                probe.copy_(t[-1:])
+                t[-1:].copy_(probe)
         base = [int(t.data_ptr()) for t in self._peers]
         i64 = torch.int64
 
