@@ -185,6 +185,8 @@ def run_ours(args):
         for _ in range(steps):
             rec, x, m = step(resident)
             recs.append(rec)
+            if os.environ.get("DDILU_BENCH_DEBUG"):
+                print(f"step: setup {rec['setup_s']:.4f} s, solve {rec['solve_s']:.4f} s, {rec['its']} its", file=sys.stderr, flush=True)
         e1.record()
         torch.cuda.synchronize()
         comm.barrier()
