@@ -851,8 +851,10 @@ def build_csweep(lower: DeviceCsr, upper: DeviceCsr, lev_l: torch.Tensor, nlev_l
                  nlev_u: int, seg_ptr) -> "ClusterSweepPlan | None":
     """Plan of the cluster sweep for the factor pair (L strictly lower, U with its diagonal) whose independent
     diagonal blocks are the row ranges seg_ptr (host ints); None when the pair does not qualify (a dependency
-    leaves its block, more than 4 dependencies per row, blocks too few / too narrow for clusters, a dependency
-    further back than the window, clusters cannot be resident)."""
+    leaves its block, more than 20 dependencies per row, short-row blocks too few / too narrow for clusters, a
+    dependency further back than the window, a result needed by too many other CTAs, clusters cannot be resident).
+    Up to 4 dependencies per row: the short-row shape of the kernel (7-point ILU(0)); 5 .. 20: the long-row shape
+    (27-point / ILUT / ILU(k) factors)."""
     n = lower.n_rows
     nb = len(seg_ptr) - 1
     if not USE_CSWEEP or n == 0 or nb < 1 or nlev_l == 0 or nlev_u == 0:

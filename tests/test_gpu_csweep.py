@@ -1,7 +1,8 @@
 """GPU parity of the cluster sweep (csrc/csweep.cu): the interior factors L_B / U_B solved by one thread-block
-cluster per subdomain block (x in a window distributed over the CTAs' shared memory, hardware cluster barrier per
-level) -- bit-exact against the CPU oracle's row-serial solves (sparse.py:228-272) and against the tiled kernel;
-factor pairs that do not qualify must be refused."""
+cluster per subdomain block (x in windows distributed over the CTAs' shared memory, results pushed through
+distributed shared memory, one mbarrier wait per level; short-row shape for 7-point ILU(0), long-row shape for
+27-point ILUT factors) -- bit-exact against the CPU oracle's row-serial solves (sparse.py:228-272) and against the
+tiled kernel; factor pairs that do not qualify must be refused.  Also here: the processing order of the ILUT kernel."""
 
 import numpy as np
 import pytest
