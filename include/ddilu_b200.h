@@ -282,6 +282,15 @@ long long ddilu_mgs_ws_bytes(void);
 int ddilu_mgs_max_block(void);
 int ddilu_mgs_block(long long n, long long ld, int kp, const double *vprev, const double *raw_prev, double *hout,
                     double *w, int kn, const double *vnext, double *out, void *ws, int reverse, void *stream);
+/* krylov.py:236-256, one Arnoldi step of `fixed_gmres` on a SHORT vector (the interface unknowns) in ONE cooperative
+ * launch: w orthogonalised in place against v[0..k) (k <= ddilu_mgs_small_max(), leading dimension ld),
+ * hout[0..k) = the MGS coefficients, hout[k] = <w, w>, vout = w / sqrt(<w, w>).  The phases are the three launches
+ * it replaces -- ddilu_mgs_block(0, k), ddilu_mgs_block(k, 0), ddilu_scale -- with the same grid, loops and
+ * reduction order (same bits), separated by grid barriers; falls back to those launches when the grid cannot be
+ * resident at once.  raw: scratch of k + k(k-1)/2 doubles (fallback only); ws as for ddilu_mgs_block. */
+int ddilu_mgs_small_max(void);
+int ddilu_mgs_small_step(long long n, long long ld, int k, const double *v, double *w, double *hout, double *vout,
+                         double *raw, void *ws, int reverse_dots, int reverse_update, void *stream);
 /* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
 int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
                 double *y, void *stream);

@@ -133,6 +133,7 @@ constexpr int MGS_NRED = MGS_K + MGS_K * (MGS_K - 1) / 2;
 struct MgsWs {
     double partial[MGS_NRED][RED_MAX_BLOCKS];
     unsigned int ticket;
+    unsigned int bar[3];  // grid barriers of mgs_small_step_kernel (two counters + the exit ticket that clears them)
 };
 
 template <int NA>
@@ -286,6 +287,209 @@ static void mgs_launch_kn(int kn, int grid, cudaStream_t st, long long n, long l
         DDILU_MGS_CASE(8)
     }
 #undef DDILU_MGS_CASE
+}
+
+// ---- one Arnoldi step on a SHORT vector in one launch (the inner GMRES of the two-level preconditioners works on
+// the interface unknowns: a few hundred thousand doubles, every kernel there is launch-bound).  Phases = the three
+// launches it replaces, with the same grid, the same per-thread loops and the same reduction order, so the bits
+// are the same: (1) mgs_block_kernel<0, K>: raw sums of v_0..v_{K-1} against w, (2) mgs_block_kernel<K, 0>:
+// w -= sum h_l v_l, <w, w>, (3) scale_kernel: vout = w / sqrt(<w, w>).  Between the phases a grid barrier (the grid
+// is launched cooperatively: all CTAs resident) after which EVERY CTA adds the partials in the order the last CTA
+// of the separate kernels would.  hout[0..K) = h, hout[K] = <w, w>.
+__device__ __forceinline__ void grid_barrier(unsigned int *counter) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+        while (ld_l2(reinterpret_cast<const int *>(counter)) < (int)gridDim.x) __nanosleep(20);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(VEC_THREADS, 4) mgs_small_step_kernel(long long n, long long ld,
+                                                                        const double *__restrict__ v, double *w,
+                                                                        double *hout, double *vout, MgsWs *ws,
+                                                                        int reverse_dots, int reverse_update) {
+    constexpr int NA = K + K * (K - 1) / 2;
+    constexpr int ROW2 = MGS_NRED - 1;   // partial row of the phase-2 sum: phase-1 rows may still be read by slower CTAs
+    __shared__ double sm[NA][VEC_THREADS / 32];
+    __shared__ double tot[NA + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool al = ((((uintptr_t)w | (uintptr_t)v) & 15) == 0) && ((ld & 1) == 0);
+    const long long n2 = al ? n >> 1 : 0, ld2 = ld >> 1;
+    double2 *w2 = reinterpret_cast<double2 *>(w);
+    const double2 *p2 = reinterpret_cast<const double2 *>(v);
+    const long long q0 = (long long)blockIdx.x * VEC_THREADS + threadIdx.x, qs = (long long)gridDim.x * VEC_THREADS;
+
+    // phase 1: raw sums (mgs_block_kernel<0, K>)
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    for (long long q = q0; q < n2; q += qs) {
+        const long long i = reverse_dots ? n2 - 1 - q : q;
+        const double2 b = w2[i];
+        double2 c[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) c[j] = p2[j * ld2 + i];
+        int g = K;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            acc[j] += c[j].x * b.x;
+            acc[j] += c[j].y * b.y;
+#pragma unroll
+            for (int l = 0; l < j; ++l) {
+                acc[g] += c[j].x * c[l].x;
+                acc[g] += c[j].y * c[l].y;
+                ++g;
+            }
+        }
+    }
+    for (long long i = 2 * n2 + q0; i < n; i += qs) {
+        const double b = w[i];
+        double c[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) c[j] = v[j * ld + i];
+        int g = K;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            acc[j] += c[j] * b;
+#pragma unroll
+            for (int l = 0; l < j; ++l) acc[g++] += c[j] * c[l];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+        const double t = warp_sum(acc[a]);
+        if (lane == 0) sm[a][warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < NA) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC_THREADS / 32; ++q) t += sm[threadIdx.x][q];
+        st_l2(&ws->partial[threadIdx.x][blockIdx.x], t);
+        __threadfence();
+    }
+    grid_barrier(&ws->bar[0]);
+    for (int a = warp; a < NA; a += VEC_THREADS / 32) {
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += ld_l2(&ws->partial[a][b]);
+        s = warp_sum(s);
+        if (lane == 0) tot[a] = s;
+    }
+    __syncthreads();
+
+    // phase 2: coefficients of the block recurrence, update, <w, w> (mgs_block_kernel<K, 0>)
+    double h[K], nh[K];
+    {
+        int g = K;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            double s = tot[i];
+#pragma unroll
+            for (int l = 0; l < i; ++l) s -= h[l] * tot[g++];
+            h[i] = s;
+            nh[i] = -s;
+        }
+    }
+    double ww = 0.0;
+    for (long long q = q0; q < n2; q += qs) {
+        const long long i = reverse_update ? n2 - 1 - q : q;
+        double2 b = w2[i];
+        double2 a[K];
+#pragma unroll
+        for (int l = 0; l < K; ++l) a[l] = p2[l * ld2 + i];
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+            b.x += nh[l] * a[l].x;
+            b.y += nh[l] * a[l].y;
+        }
+        w2[i] = b;
+        ww += b.x * b.x;
+        ww += b.y * b.y;
+    }
+    for (long long i = 2 * n2 + q0; i < n; i += qs) {
+        double b = w[i];
+#pragma unroll
+        for (int l = 0; l < K; ++l) b += nh[l] * v[l * ld + i];
+        w[i] = b;
+        ww += b * b;
+    }
+    __syncthreads();   // sm[0] is reused
+    {
+        const double t = warp_sum(ww);
+        if (lane == 0) sm[0][warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC_THREADS / 32; ++q) t += sm[0][q];
+        st_l2(&ws->partial[ROW2][blockIdx.x], t);
+        __threadfence();
+    }
+    grid_barrier(&ws->bar[1]);
+    if (warp == 0) {
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += ld_l2(&ws->partial[ROW2][b]);
+        s = warp_sum(s);
+        if (lane == 0) tot[NA] = s;
+    }
+    __syncthreads();
+    const double w_sq = tot[NA];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) hout[i] = h[i];
+        hout[K] = w_sq;
+        ws->bar[0] = 0;   // every CTA is past the first barrier
+    }
+
+    // phase 3: vout = w / sqrt(<w, w>) (scale_kernel); a thread reads back what it stored itself
+    const double sc = sqrt(w_sq);
+    const bool alo = al && (((uintptr_t)vout & 15) == 0);
+    double2 *o2 = reinterpret_cast<double2 *>(vout);
+    for (long long q = q0; q < n2; q += qs) {
+        const long long i = reverse_update ? n2 - 1 - q : q;
+        const double2 b = w2[i];
+        if (alo) {
+            o2[i] = make_double2(b.x / sc, b.y / sc);
+        } else {
+            vout[2 * i] = b.x / sc;
+            vout[2 * i + 1] = b.y / sc;
+        }
+    }
+    for (long long i = 2 * n2 + q0; i < n; i += qs) vout[i] = w[i] / sc;
+
+    // the last CTA to get here clears the second barrier and the exit ticket for the next launch
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(&ws->bar[2], 1u);
+        if (t == gridDim.x - 1) {
+            ws->bar[1] = 0;
+            ws->bar[2] = 0;
+        }
+    }
+}
+
+// all CTAs of `grid` resident at once?  (cooperative launches fail otherwise; asked once per instance)
+template <int K>
+static bool small_step_fits(int grid) {
+    static int resident = -1;
+    if (resident < 0) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_small_step_kernel<K>, VEC_THREADS, 0) != cudaSuccess)
+            per_sm = 0;
+        resident = per_sm * device_info().sm_count;
+    }
+    return grid <= resident;
+}
+
+template <int K>
+static cudaError_t small_step_launch(int grid, cudaStream_t st, long long n, long long ld, const double *v, double *w,
+                                     double *hout, double *vout, MgsWs *ws, int r1, int r2) {
+    void *args[] = {&n, &ld, &v, &w, &hout, &vout, &ws, &r1, &r2};
+    return cudaLaunchCooperativeKernel((const void *)mgs_small_step_kernel<K>, dim3(grid), dim3(VEC_THREADS), args, 0, st);
 }
 
 // y = x / s, y = x * s or y = copy, with s = *alpha_dev (optionally sqrt'ed) or alpha_host
@@ -474,6 +678,47 @@ extern "C" int ddilu_mgs_block(long long n, long long ld, int kp, const double *
         case 7: mgs_launch_kn<7>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
         case 8: mgs_launch_kn<8>(kn, grid, st, n, ld, vprev, raw_prev, hout, w, vnext, m, out, reverse); break;
     }
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* One Arnoldi step of the inner GMRES (krylov.py:236-256) on a short vector in ONE cooperative launch: the k <=
+ * ddilu_mgs_small_max() basis vectors v[0..k) (leading dimension ld), w orthogonalised in place,
+ * hout[0..k) = the MGS coefficients, hout[k] = <w, w>, vout = w / sqrt(<w, w>).  Same bits as
+ * ddilu_mgs_block(0, k) + ddilu_mgs_block(k, 0) + ddilu_scale (which it falls back to when the grid of the
+ * reductions cannot be resident at once); raw = scratch of k + k(k-1)/2 doubles for that fallback. */
+extern "C" int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt,
+                           int mode, double *y, void *stream);
+extern "C" int ddilu_mgs_small_max(void) { return 4; }
+extern "C" int ddilu_mgs_small_step(long long n, long long ld, int k, const double *v, double *w, double *hout,
+                                    double *vout, double *raw, void *ws, int reverse_dots, int reverse_update,
+                                    void *stream) {
+    if (k < 1 || k > 4 || n <= 0 || !v || !w || !hout || !vout || !raw || !ws) return DDILU_ERR_ARG;
+    const int grid = red_grid(n);
+    cudaStream_t st = (cudaStream_t)stream;
+    MgsWs *m = (MgsWs *)ws;
+    bool fits = false;
+    switch (k) {
+        case 1: fits = small_step_fits<1>(grid); break;
+        case 2: fits = small_step_fits<2>(grid); break;
+        case 3: fits = small_step_fits<3>(grid); break;
+        case 4: fits = small_step_fits<4>(grid); break;
+    }
+    if (!fits) {
+        int rc = ddilu_mgs_block(n, ld, 0, nullptr, nullptr, nullptr, w, k, v, raw, ws, reverse_dots, stream);
+        if (rc != DDILU_OK) return rc;
+        rc = ddilu_mgs_block(n, ld, k, v, raw, hout, w, 0, nullptr, hout + k, ws, reverse_update, stream);
+        if (rc != DDILU_OK) return rc;
+        return ddilu_scale(n, w, hout + k, 0.0, 1, 0, vout, stream);
+    }
+    cudaError_t e = cudaSuccess;
+    switch (k) {
+        case 1: e = small_step_launch<1>(grid, st, n, ld, v, w, hout, vout, m, reverse_dots, reverse_update); break;
+        case 2: e = small_step_launch<2>(grid, st, n, ld, v, w, hout, vout, m, reverse_dots, reverse_update); break;
+        case 3: e = small_step_launch<3>(grid, st, n, ld, v, w, hout, vout, m, reverse_dots, reverse_update); break;
+        case 4: e = small_step_launch<4>(grid, st, n, ld, v, w, hout, vout, m, reverse_dots, reverse_update); break;
+    }
+    DDILU_CHECK(e);
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -1461,6 +1461,14 @@ class Reducer:
         _lib.profile_tag = None
 
 
+    def mgs_small_step(self, n, ld, k, v, w, hout, vout, raw, reverse_dots=False, reverse_update=False):
+        """One Arnoldi step on a short vector in one cooperative launch (`ddilu_mgs_small_step`)."""
+        if self.mgs_ws is None:
+            self.mgs_ws = torch.zeros(query("ddilu_mgs_ws_bytes") // 8 + 1, dtype=F64, device=dev())
+        call("ddilu_mgs_small_step", int(n), int(ld), int(k), v, w, hout, vout, raw, self.mgs_ws, int(reverse_dots),
+             int(reverse_update))
+
+
 def axpy(n, alpha, v, w, alpha_dev=None):
     call("ddilu_axpy_dot", int(n), alpha_dev, float(alpha), v, w, None, None, None)
 

@@ -164,6 +164,20 @@ class Arnoldi:
                       reverse=alt and (npass & 1) == 0)
         comm.allreduce_sum_(h[j + 1:j + 2])
 
+    def small_step_ok(self, j: int) -> bool:
+        """One-launch Arnoldi step (`ddilu_mgs_small_step`): single rank, all of V[0..j] in one block of the
+        blocked Gram-Schmidt, a vector short enough to stay in L2 between the phases."""
+        return (SMALL_STEP and MGS_BLOCK > 1 and not self.comm.active and 0 < self.n <= SMALL_STEP_MAX_N
+                and j + 1 <= min(MGS_BLOCK, D.query("ddilu_mgs_small_max"), D.query("ddilu_mgs_max_block")))
+
+    def mgs_normalise_small(self, j: int, h: torch.Tensor):
+        """`mgs(j, h)` + `normalise_into(j, h)` in one launch: same passes, same directions, same bits."""
+        if self.raw is None:
+            self.raw = torch.zeros(((self.m + MGS_BLOCK) // MGS_BLOCK + 1, 40), dtype=D.F64, device=D.dev())
+        alt = ALTERNATE_MGS
+        self.red.mgs_small_step(self.n, self.ld, j + 1, self.V, self.w, h, self.V[j + 1], self.raw[0],
+                                reverse_dots=alt, reverse_update=False)
+
     def normalise_into(self, j: int, h: torch.Tensor | None = None):
         """V[j+1] = w / hnext with hnext = sqrt(h[j+1]) read on the device (krylov.py:156)."""
         h = self.hdev if h is None else h
@@ -204,6 +218,8 @@ def release_workspace() -> None:
 DEVICE_COEF = os.environ.get("DDILU_DEVICE_COEF", "1") == "1"   # inner GMRES: rotations / back substitution on the device (no host read per application)
 L2_PERSIST_W = False  # pin the Arnoldi work vector in the persisting part of L2 during a solve (measured: slower)
 MGS_BLOCK = int(os.environ.get("DDILU_MGS_BLOCK", "4"))  # basis vectors per pass of the blocked Gram-Schmidt (1: the vector-by-vector launches)
+SMALL_STEP = os.environ.get("DDILU_SMALL_STEP", "1") == "1"   # inner GMRES: dots + update + normalisation of a step in one cooperative launch
+SMALL_STEP_MAX_N = 4 << 20                                     # ... for vectors that stay in L2 between the phases
 ALTERNATE_MGS = True  # consecutive MGS steps traverse the vectors in alternating directions (L2 reuse)
 
 
@@ -347,8 +363,11 @@ class InnerGmres:
                 apply_a(self.z, w)
             else:
                 apply_a(V[j], w)
-            ws.mgs(j, H[j])
-            ws.normalise_into(j, H[j])
+            if ws.small_step_ok(j):
+                ws.mgs_normalise_small(j, H[j])
+            else:
+                ws.mgs(j, H[j])
+                ws.normalise_into(j, H[j])
         if DEVICE_COEF and not self.safe and m <= D.query("ddilu_gmres_small_max"):
             # rotations + back substitution on the device: nothing is read back; an early exit of the
             # reference raises self.flag and the caller redoes the application with safe = True

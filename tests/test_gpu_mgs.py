@@ -94,3 +94,40 @@ def test_blocked_mgs_column_stays_on_device():
     got = buf.cpu().numpy()
     assert np.allclose(got[: nv + 1], h_ref, rtol=0, atol=1e-12 * np.linalg.norm(wh))
     assert np.all(got[nv + 1:] == -7.0)
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 100003, 390152, (1 << 20) + 5])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_small_step_is_the_three_launches_bit_for_bit(n, k):
+    """`ddilu_mgs_small_step` (one cooperative launch per Arnoldi step of the inner GMRES, krylov.py:236-256)
+    against `mgs` + `normalise_into`: coefficients, <w, w>, the updated w and the new basis vector identical to
+    the last bit, repeatedly on the same workspace (the grid-barrier counters must come back to zero)."""
+    import torch
+    from paper_2303_08881_b200 import krylov as K
+    from paper_2303_08881_b200.dist import Comm
+    rng = np.random.default_rng(77 * k + n % 991)
+    ws = K.Arnoldi(n, 5, Comm(), flexible=False, pad=3)
+    assert ws.small_step_ok(k - 1)
+    Vh = rng.standard_normal((k, n))
+    Vh /= np.linalg.norm(Vh, axis=1)[:, None]
+    if n > 1:
+        Vh[1:] += 0.05 * Vh[:-1]
+    ws.V.zero_()
+    ws.V[:k, :n] = torch.from_numpy(Vh).cuda()
+    for rep in range(3):
+        wh = rng.standard_normal(n) * (rep + 1.5)
+        h_a = torch.zeros(8, dtype=torch.float64, device="cuda")
+        ws.w.zero_()
+        ws.w[:n] = torch.from_numpy(wh).cuda()
+        ws.mgs(k - 1, h_a)
+        ws.normalise_into(k - 1, h_a)
+        ref = (h_a.cpu().numpy().copy(), ws.w[:n].cpu().numpy().copy(), ws.V[k, :n].cpu().numpy().copy())
+        h_b = torch.zeros(8, dtype=torch.float64, device="cuda")
+        ws.w.zero_()
+        ws.w[:n] = torch.from_numpy(wh).cuda()
+        ws.V[k].zero_()
+        ws.mgs_normalise_small(k - 1, h_b)
+        torch.cuda.synchronize()
+        got = (h_b.cpu().numpy(), ws.w[:n].cpu().numpy(), ws.V[k, :n].cpu().numpy())
+        for a, b in zip(ref, got):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
