@@ -1,6 +1,6 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck); logs -> profiles/r2_sanitizer_*.log.
 
-    compute-sanitizer --tool memcheck python scripts/sanitize_case.py [tiled|sweep|mgs|ilut|rcm|pipeline ...]
+    compute-sanitizer --tool memcheck python scripts/sanitize_case.py [tiled|sweep|mgs|smallstep|ilut|rcm|pipeline ...]
 
 tiled: sptrsv_tiled on interior + interface factors; csweep: the cluster sweep on interior factors (clusters of 4 and
 of the largest size that fits, a 32^3 block on one CTA: levels in several steps); sweep: the block sweep (L, U, fused, with product and add);
@@ -122,6 +122,21 @@ if "mgs" in which:
             red.mgs_block(n, ld, min(4, 8 - kn), V[kn], raw[1], h[kn:kn + min(4, 8 - kn)], w, 0, None, h[9:10])
     torch.cuda.synchronize()
     print("mgs ok")
+
+if "smallstep" in which:
+    # the one-launch Arnoldi step of the inner GMRES (cooperative grid, two grid barriers), repeated on one workspace
+    red = D.Reducer()
+    for n in (1, 33, 1000, 40001, 390152):
+        ld = (n + 1) & ~1
+        V = torch.randn((6, ld), dtype=torch.float64, device="cuda")
+        raw = torch.zeros(40, dtype=torch.float64, device="cuda")
+        h = torch.zeros(16, dtype=torch.float64, device="cuda")
+        for k in (1, 2, 3, 4):
+            for rep in range(2):
+                w = torch.randn(ld, dtype=torch.float64, device="cuda")
+                red.mgs_small_step(n, ld, k, V, w, h, V[k], raw, reverse_dots=True, reverse_update=False)
+    torch.cuda.synchronize()
+    print("smallstep ok", float(h[0]))
 
 if "ilut" in which:
     a27 = P.convdiff27(9, 8, 7)
