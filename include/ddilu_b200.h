@@ -291,6 +291,10 @@ int ddilu_mgs_block(long long n, long long ld, int kp, const double *vprev, cons
 int ddilu_mgs_small_max(void);
 int ddilu_mgs_small_step(long long n, long long ld, int k, const double *v, double *w, double *hout, double *vout,
                          double *raw, void *ws, int reverse_dots, int reverse_update, void *stream);
+/* krylov.py:226-232, the start of `fixed_gmres` on one rank: *out = <x, x>, y = x / sqrt(<x, x>) in ONE cooperative
+ * launch (= ddilu_dot + ddilu_scale(take_sqrt), same bits; falls back to those when the grid cannot be resident at
+ * once).  ws: workspace of ddilu_mgs_block, red_ws: workspace of ddilu_dot (fallback only). */
+int ddilu_norm_scale_small(long long n, const double *x, double *out, double *y, void *ws, void *red_ws, void *stream);
 /* y = x / s (mode 0) or x * s (mode 1); s = *alpha_dev or alpha_host, sqrt'ed if take_sqrt */
 int ddilu_scale(long long n, const double *x, const double *alpha_dev, double alpha_host, int take_sqrt, int mode,
                 double *y, void *stream);

@@ -90,6 +90,7 @@ SIGNATURES = {
     "ddilu_mgs_block": (_I, [_L, _L, _I, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P]),
     "ddilu_mgs_small_max": (_I, []),
     "ddilu_mgs_small_step": (_I, [_L, _L, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
+    "ddilu_norm_scale_small": (_I, [_L, _P, _P, _P, _P, _P, _P]),
     "ddilu_scale": (_I, [_L, _P, _P, _D, _I, _I, _P, _P]),
     "ddilu_l2_persist_window": (_I, [_P, _L, _P]),
     "ddilu_multi_axpy": (_I, [_L, _I, _P, _L, _P, _P, _I, _P]),

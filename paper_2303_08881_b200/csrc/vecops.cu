@@ -472,6 +472,50 @@ __global__ void __launch_bounds__(VEC_THREADS, 4) mgs_small_step_kernel(long lon
     }
 }
 
+// y = x / sqrt(<x, x>), *out = <x, x> in one cooperative launch: dot_kernel (its loop, block_sum and the order in
+// which the last CTA adds the partials) + scale_kernel(take_sqrt) with one grid barrier in between -- the first two
+// launches of an inner GMRES solve (krylov.py:226-232: beta = ||b||, v_0 = b / beta).  Same bits as the two launches.
+__global__ void __launch_bounds__(VEC_THREADS, 4) norm_scale_small_kernel(long long n, const double *__restrict__ x,
+                                                                          double *out, double *y, MgsWs *ws) {
+    constexpr int ROW2 = MGS_NRED - 1;
+    __shared__ double tot;
+    double acc = 0.0;
+    const bool al = aligned16(x, x);
+    const long long n2 = al ? n >> 1 : 0;
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
+    const long long q0 = (long long)blockIdx.x * VEC_THREADS + threadIdx.x, qs = (long long)gridDim.x * VEC_THREADS;
+    for (long long q = q0; q < n2; q += qs) {
+        const double2 a = x2[q];
+        acc += a.x * a.x;
+        acc += a.y * a.y;
+    }
+    for (long long i = 2 * n2 + q0; i < n; i += qs) acc += x[i] * x[i];
+    const double part = block_sum(acc);
+    if (threadIdx.x == 0) {
+        st_l2(&ws->partial[ROW2][blockIdx.x], part);
+        __threadfence();
+    }
+    grid_barrier(&ws->bar[1]);
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) s += ld_l2(&ws->partial[ROW2][b]);
+        s = warp_sum(s);
+        if (threadIdx.x == 0) tot = s;
+    }
+    __syncthreads();
+    const double xx = tot;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out = xx;
+    const double sc = sqrt(xx);
+    for (long long i = q0; i < n; i += qs) y[i] = x[i] / sc;
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(&ws->bar[2], 1u);
+        if (t == gridDim.x - 1) {
+            ws->bar[1] = 0;
+            ws->bar[2] = 0;
+        }
+    }
+}
+
 // all CTAs of `grid` resident at once?  (cooperative launches fail otherwise; asked once per instance)
 template <int K>
 static bool small_step_fits(int grid) {
@@ -719,6 +763,33 @@ extern "C" int ddilu_mgs_small_step(long long n, long long ld, int k, const doub
         case 4: e = small_step_launch<4>(grid, st, n, ld, v, w, hout, vout, m, reverse_dots, reverse_update); break;
     }
     DDILU_CHECK(e);
+    DDILU_LAUNCH_CHECK();
+    return DDILU_OK;
+}
+
+/* krylov.py:226-232, the start of `fixed_gmres` on one rank: *out = <x, x>, y = x / sqrt(<x, x>) in ONE cooperative
+ * launch (ddilu_dot + ddilu_scale(take_sqrt) with a grid barrier in between; same bits, falls back to the two
+ * launches when the grid cannot be resident at once).  ws: the ddilu_mgs_block workspace, red_ws: ddilu_dot's. */
+extern "C" int ddilu_norm_scale_small(long long n, const double *x, double *out, double *y, void *ws, void *red_ws,
+                                      void *stream) {
+    if (n <= 0 || !x || !out || !y || !ws || !red_ws) return DDILU_ERR_ARG;
+    const int grid = red_grid(n);
+    static int resident = -1;
+    if (resident < 0) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, norm_scale_small_kernel, VEC_THREADS, 0) != cudaSuccess)
+            per_sm = 0;
+        resident = per_sm * device_info().sm_count;
+    }
+    if (grid > resident) {
+        int rc = ddilu_dot(n, x, x, out, red_ws, stream);
+        if (rc != DDILU_OK) return rc;
+        return ddilu_scale(n, x, out, 0.0, 1, 0, y, stream);
+    }
+    MgsWs *m = (MgsWs *)ws;
+    void *args[] = {&n, &x, &out, &y, &m};
+    DDILU_CHECK(cudaLaunchCooperativeKernel((const void *)norm_scale_small_kernel, dim3(grid), dim3(VEC_THREADS), args, 0,
+                                            (cudaStream_t)stream));
     DDILU_LAUNCH_CHECK();
     return DDILU_OK;
 }

@@ -1469,6 +1469,13 @@ class Reducer:
              int(reverse_update))
 
 
+    def norm_scale_small(self, n, x, out, y):
+        """out = <x, x>, y = x / sqrt(out) in one cooperative launch (`ddilu_norm_scale_small`)."""
+        if self.mgs_ws is None:
+            self.mgs_ws = torch.zeros(query("ddilu_mgs_ws_bytes") // 8 + 1, dtype=F64, device=dev())
+        call("ddilu_norm_scale_small", int(n), x, out, y, self.mgs_ws, self.ws)
+
+
 def axpy(n, alpha, v, w, alpha_dev=None):
     call("ddilu_axpy_dot", int(n), alpha_dev, float(alpha), v, w, None, None, None)
 

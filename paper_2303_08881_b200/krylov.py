@@ -354,9 +354,12 @@ class InnerGmres:
         H = self.hcols
         V, w = ws.V, ws.w
         bb = H[self.m, 0:1]                      # <b, b>
-        ws.red.dot(n, b, b, bb)
-        self.comm.allreduce_sum_(bb)
-        D.scale(n, b, V[0], alpha_dev=bb, take_sqrt=True)
+        if ws.small_step_ok(0):
+            ws.red.norm_scale_small(n, b, bb, V[0])       # the two launches below in one
+        else:
+            ws.red.dot(n, b, b, bb)
+            self.comm.allreduce_sum_(bb)
+            D.scale(n, b, V[0], alpha_dev=bb, take_sqrt=True)
         for j in range(m):
             if apply_m is not None:
                 apply_m(V[j], self.z)

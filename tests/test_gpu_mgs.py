@@ -131,3 +131,29 @@ def test_small_step_is_the_three_launches_bit_for_bit(n, k):
         got = (h_b.cpu().numpy(), ws.w[:n].cpu().numpy(), ws.V[k, :n].cpu().numpy())
         for a, b in zip(ref, got):
             assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 100003, 390152, (1 << 20) + 5])
+def test_norm_scale_small_is_dot_plus_scale_bit_for_bit(n):
+    """`ddilu_norm_scale_small` (krylov.py:226-232: beta = ||b||, v_0 = b / beta in one cooperative launch)
+    against `ddilu_dot` + `ddilu_scale`, interleaved with the one-launch Arnoldi step on the same workspace."""
+    import torch
+    from paper_2303_08881_b200 import device as D
+    from paper_2303_08881_b200 import krylov as K
+    from paper_2303_08881_b200.dist import Comm
+    rng = np.random.default_rng(n % 983)
+    ws = K.Arnoldi(n, 3, Comm(), flexible=False, pad=1)
+    for rep in range(3):
+        x = torch.from_numpy(rng.standard_normal(n) * (rep + 0.5)).cuda()
+        s_a = torch.zeros(1, dtype=torch.float64, device="cuda")
+        y_a = torch.zeros(n, dtype=torch.float64, device="cuda")
+        ws.red.dot(n, x, x, s_a)
+        D.scale(n, x, y_a, alpha_dev=s_a, take_sqrt=True)
+        s_b = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws.red.norm_scale_small(n, x, s_b, ws.V[0])
+        h = torch.zeros(8, dtype=torch.float64, device="cuda")
+        ws.w[:n].copy_(x * 0.3 + 1.0)
+        ws.mgs_normalise_small(0, h)                 # shares the barrier counters
+        torch.cuda.synchronize()
+        assert np.array_equal(s_a.cpu().numpy().view(np.uint64), s_b.cpu().numpy().view(np.uint64))
+        assert np.array_equal(y_a.cpu().numpy().view(np.uint64), ws.V[0, :n].cpu().numpy().view(np.uint64))
