@@ -175,6 +175,12 @@ def run_ours(args):
                 "converged": rep.converged}, x, m
 
     def timed(resident: bool, steps: int):
+        import gc
+        gc.collect()
+        gc_was_on = gc.isenabled()
+        if os.environ.get("DDILU_BENCH_GC", "0") != "1":
+            gc.disable()            # like timeit: no cyclic-collector pause inside the timed steps (objects are
+                                    # freed by reference count; DDILU_BENCH_GC=1 leaves the collector on)
         comm.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -183,6 +189,8 @@ def run_ours(args):
         recs = []
         m = None
         for _ in range(steps):
+            m = x = None            # the previous step's preconditioner and solution are released BEFORE the next
+                                    # setup (two alive at once force fresh device / pinned allocations: +50 ms)
             rec, x, m = step(resident)
             recs.append(rec)
             if os.environ.get("DDILU_BENCH_DEBUG"):
@@ -190,6 +198,8 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         comm.barrier()
+        if gc_was_on:
+            gc.enable()
         total = e0.elapsed_time(e1) * 1e-3
         t = torch.tensor([total], dtype=torch.float64, device="cuda")
         if comm.active:
